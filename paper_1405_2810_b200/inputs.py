@@ -1,0 +1,335 @@
+"""Seeded synthetic inputs shared by the CUDA path and the CPU oracle.
+
+This module holds NO arithmetic of the LRBMS method (no mobility, no operator,
+no projection, no solve, no flux, no transport).  It only draws the seeded
+inputs a user of the method supplies:
+
+* the fine grid and coarse partition;
+* the permeability field K (stands in for the paper's raster, which is
+  only a figure);
+* the boundary data as *links* -- a Dirichlet boundary face or a well cell
+  with a fixed pressure p_L and an external saturation s_ext (
+  reading R6/A13 in DESIGN.md);
+* the local reduced bases Phi_E, as generic full-rank local
+  spaces: orthonormalised tensor monomials on each subdomain (a coarse-scale
+  piecewise polynomial space, first column the normalised subdomain indicator,
+  cf. the coarse unit functions P:1110-1111), or a seeded random orthogonal
+  full space (Phi_E = full n_loc space: the fine space, pin P1);
+* the initial saturation s0.
+
+Both `oracle/` and the CUDA binding consume exactly these arrays.
+"""
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+from typing import Optional
+
+import numpy as np
+
+# ----------------------------------------------------------------------------
+# configurations (BASELINE.json "configs", in order C1..C5)
+# ----------------------------------------------------------------------------
+
+CONFIGS = {
+    # 2D 16x16, 2x2 subdomains of 8x8, ln K ~ N(0,1) iid, mu_w = mu_o = 1, N = 4, 20 steps, CFL 0.5
+    "C1": dict(dim=2, nx=16, ny=16, nz=1, sx=8, sy=8, sz=1, N=4, mu_o=1.0, n_steps=20,
+               field="iid", sigma=1.0, corr=None, bc="left_right"),
+    # 2D 64x64, 4x4 subdomains of 16x16, ln K = 1.5 Z (corr 4), mu_o/mu_w = 5, N = 10, 100 steps
+    "C2": dict(dim=2, nx=64, ny=64, nz=1, sx=16, sy=16, sz=1, N=10, mu_o=5.0, n_steps=100,
+               field="gauss", sigma=1.5, corr=(4.0, 4.0, 0.0), bc="left_right"),
+    # 2D 60x220 channelised, 6x22 subdomains of 10x10, quarter five-spot, ratio 10, N = 16, 500 steps
+    "C3": dict(dim=2, nx=60, ny=220, nz=1, sx=10, sy=10, sz=1, N=16, mu_o=10.0, n_steps=500,
+               field="channels", sigma=2.0, corr=None, bc="corner_wells_2d"),
+    # 2D 512x512, 32x32 subdomains of 16x16, ln K = 2 Z (corr 8), ratio 10, N = 24, 1000 steps
+    "C4": dict(dim=2, nx=512, ny=512, nz=1, sx=16, sy=16, sz=1, N=24, mu_o=10.0, n_steps=1000,
+               field="gauss", sigma=2.0, corr=(8.0, 8.0, 0.0), bc="left_right"),
+    # 3D 128x128x64, 16x16x8 subdomains of 8x8x8, layered ln K = 2 Z (corr 16,16,2), ratio 10,
+    # injector / producer well columns at opposite corners, N = 32, 200 steps
+    "C5": dict(dim=3, nx=128, ny=128, nz=64, sx=8, sy=8, sz=8, N=32, mu_o=10.0, n_steps=200,
+               field="gauss", sigma=2.0, corr=(16.0, 16.0, 2.0), bc="corner_columns_3d"),
+}
+CONFIG_INDEX = {name: i + 1 for i, name in enumerate(CONFIGS)}
+
+
+@dataclasses.dataclass
+class Scenario:
+    """One LRBMS online problem: everything the C ABI's create/set calls take."""
+    name: str
+    dim: int
+    nx: int
+    ny: int
+    nz: int
+    sx: int          # subdomain size in fine cells (x)
+    sy: int
+    sz: int
+    N: int           # local reduced basis size per subdomain
+    hx: float = 1.0
+    hy: float = 1.0
+    hz: float = 1.0
+    mu_w: float = 1.0
+    mu_o: float = 1.0
+    swr: float = 0.0
+    sor: float = 0.0
+    nw: float = 2.0   # Corey exponents (2 = quadratic Corey of BASELINE.json; 1 = paper's linear k_r)
+    no: float = 2.0
+    cfl: float = 0.5
+    n_steps: int = 1
+    K: Optional[np.ndarray] = None          # [n] permeability, x fastest
+    phi: Optional[np.ndarray] = None        # [n] porosity or None (= 1)
+    link_cell: Optional[np.ndarray] = None  # [n_links] int32 fine cell index
+    link_axis: Optional[np.ndarray] = None  # [n_links] int32 face normal axis (0,1,2)
+    link_p: Optional[np.ndarray] = None     # [n_links] fixed pressure p_L
+    link_s: Optional[np.ndarray] = None     # [n_links] external (inflow) saturation
+    Phi: Optional[np.ndarray] = None        # [n_s][N][n_loc]  (ABI layout)
+    s0: Optional[np.ndarray] = None         # [n] initial saturation
+
+    # -- derived sizes -------------------------------------------------------
+    @property
+    def n(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    @property
+    def Sx(self) -> int:
+        return self.nx // self.sx
+
+    @property
+    def Sy(self) -> int:
+        return self.ny // self.sy
+
+    @property
+    def Sz(self) -> int:
+        return self.nz // self.sz
+
+    @property
+    def n_s(self) -> int:
+        return self.Sx * self.Sy * self.Sz
+
+    @property
+    def n_loc(self) -> int:
+        return self.sx * self.sy * self.sz
+
+    @property
+    def n_links(self) -> int:
+        return 0 if self.link_cell is None else int(self.link_cell.shape[0])
+
+    def digest(self) -> str:
+        h = hashlib.sha256()
+        for a in (self.K, self.phi, self.link_cell, self.link_axis, self.link_p, self.link_s,
+                  self.Phi, self.s0):
+            if a is not None:
+                h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()[:16]
+
+
+# ----------------------------------------------------------------------------
+# permeability fields
+# ----------------------------------------------------------------------------
+
+def gaussian_correlated(shape_zyx, corr_zyx, seed: int) -> np.ndarray:
+    """Zero-mean unit-sample-std Gaussian random field (reading A18).
+
+    iid N(0,1) on a grid padded by 3*l, convolved with a Gaussian kernel of
+    std l cells per axis (truncated at 3*l), cropped, divided by its sample std.
+    """
+    from scipy import ndimage
+
+    rng = np.random.default_rng(seed)
+    pad = [int(np.ceil(3.0 * c)) for c in corr_zyx]
+    noise = rng.standard_normal([s + 2 * p for s, p in zip(shape_zyx, pad)])
+    sm = ndimage.gaussian_filter(noise, sigma=[max(c, 0.0) for c in corr_zyx],
+                                 mode="constant", truncate=3.0)
+    sl = tuple(slice(p, p + s) for s, p in zip(shape_zyx, pad))
+    z = sm[sl]
+    z = z - z.mean()
+    return z / z.std()
+
+
+def channel_field(nx: int, ny: int, seed: int) -> np.ndarray:
+    """C3: seeded sinusoidal high-permeability channels along y in a log-normal background."""
+    rng = np.random.default_rng(seed)
+    lnK = 2.0 * rng.standard_normal((ny, nx))
+    K = np.maximum(np.exp(lnK), 1e-3)
+    xs = np.arange(nx) + 0.5
+    for _ in range(5):
+        x0 = rng.uniform(5.0, 55.0)
+        amp = rng.uniform(3.0, 10.0)
+        L = rng.uniform(60.0, 220.0)
+        psi = rng.uniform(0.0, 2.0 * np.pi)
+        hw = int(rng.integers(1, 3))
+        kc = 10.0 ** rng.uniform(3.0, 4.0)
+        for j in range(ny):
+            xc = x0 + amp * np.sin(2.0 * np.pi * (j + 0.5) / L + psi)
+            K[j, np.abs(xs - xc) <= hw] = kc
+    return K
+
+
+def make_permeability(cfg: dict, seed: int, nx: int, ny: int, nz: int) -> np.ndarray:
+    if cfg["field"] == "iid":
+        rng = np.random.default_rng(seed)
+        lnK = cfg["sigma"] * rng.standard_normal((nz, ny, nx))
+        return np.exp(lnK).reshape(-1)
+    if cfg["field"] == "gauss":
+        cx, cy, cz = cfg["corr"]
+        z = gaussian_correlated((nz, ny, nx), (cz if nz > 1 else 0.0, cy, cx), seed)
+        return np.exp(cfg["sigma"] * z).reshape(-1)
+    if cfg["field"] == "channels":
+        return channel_field(nx, ny, seed).reshape(-1)
+    raise ValueError(cfg["field"])
+
+
+# ----------------------------------------------------------------------------
+# boundary links
+# ----------------------------------------------------------------------------
+
+def links_for(bc: str, nx: int, ny: int, nz: int):
+    """Dirichlet faces / wells as links (cell, axis, p_L, s_ext) -- readings R6, A13."""
+    cells, axes, ps, ss = [], [], [], []
+
+    def add(c, ax, p, s):
+        cells.append(c); axes.append(ax); ps.append(p); ss.append(s)
+
+    if bc == "left_right":          # left p=1 with injected S=1, right p=0; other sides no-flow
+        for k in range(nz):
+            for j in range(ny):
+                add(0 + nx * (j + ny * k), 0, 1.0, 1.0)
+        for k in range(nz):
+            for j in range(ny):
+                add(nx - 1 + nx * (j + ny * k), 0, 0.0, 0.0)
+    elif bc == "corner_wells_2d":   # quarter five-spot: injector (0,0), producer (nx-1,ny-1)
+        add(0, 0, 1.0, 1.0)
+        add(nx - 1 + nx * (ny - 1), 0, 0.0, 0.0)
+    elif bc == "corner_columns_3d":  # vertical injector column (0,0,:), producer (nx-1,ny-1,:)
+        for k in range(nz):
+            add(0 + nx * (0 + ny * k), 0, 1.0, 1.0)
+        for k in range(nz):
+            add(nx - 1 + nx * (ny - 1 + ny * k), 0, 0.0, 0.0)
+    else:
+        raise ValueError(bc)
+    return (np.asarray(cells, np.int32), np.asarray(axes, np.int32),
+            np.asarray(ps, np.float64), np.asarray(ss, np.float64))
+
+
+# ----------------------------------------------------------------------------
+# local reduced bases
+# ----------------------------------------------------------------------------
+
+def _graded_exponents(dim: int, count: int):
+    out = []
+    deg = 0
+    while len(out) < count:
+        if dim == 2:
+            for ey in range(deg + 1):
+                out.append((deg - ey, ey, 0))
+        else:
+            for ez in range(deg + 1):
+                for ey in range(deg - ez + 1):
+                    out.append((deg - ey - ez, ey, ez))
+        deg += 1
+    return out[:count]
+
+
+def poly_basis(sc: Scenario, seed: int, rotate: bool = True) -> np.ndarray:
+    """Phi[E][k][l]: orthonormalised graded tensor monomials on each subdomain.
+
+    Column 0 is the normalised subdomain indicator (coarse unit function).
+    With ``rotate`` the columns 1..N-1 are mixed by a seeded random orthogonal
+    matrix per subdomain (same span, generic entries).
+    """
+    N, nl = sc.N, sc.n_loc
+    if N > nl:
+        raise ValueError("N > n_loc")
+    lz, ly, lx = np.meshgrid(np.arange(sc.sz), np.arange(sc.sy), np.arange(sc.sx), indexing="ij")
+    X = (2 * lx.reshape(-1) + 1) / sc.sx - 1.0
+    Y = (2 * ly.reshape(-1) + 1) / sc.sy - 1.0
+    Z = (2 * lz.reshape(-1) + 1) / max(sc.sz, 1) - 1.0
+    exps = _graded_exponents(sc.dim, N)
+    # monomials degenerate on small subdomains: fall back to seeded random columns
+    M = np.stack([X ** a * Y ** b * Z ** c for (a, b, c) in exps], axis=1)
+    Q, R = np.linalg.qr(M)
+    if np.min(np.abs(np.diag(R))) < 1e-8 * np.abs(R[0, 0]):
+        rng0 = np.random.default_rng(seed + 7)
+        M = np.concatenate([np.ones((nl, 1)), rng0.standard_normal((nl, N - 1))], axis=1)
+        Q, R = np.linalg.qr(M)
+    Q = Q * np.sign(np.diag(R))[None, :]
+    rng = np.random.default_rng(seed)
+    Phi = np.empty((sc.n_s, N, nl))
+    for E in range(sc.n_s):
+        if rotate and N > 2:
+            G = rng.standard_normal((N - 1, N - 1))
+            O, Rg = np.linalg.qr(G)
+            O = O * np.sign(np.diag(Rg))[None, :]
+            QE = np.concatenate([Q[:, :1], Q[:, 1:] @ O], axis=1)
+        else:
+            QE = Q
+        Phi[E] = QE.T
+    return Phi
+
+
+def random_full_basis(sc: Scenario, seed: int) -> np.ndarray:
+    """Phi_E = seeded random orthogonal n_loc x n_loc matrix (full local space; pin P1)."""
+    rng = np.random.default_rng(seed)
+    nl = sc.n_loc
+    Phi = np.empty((sc.n_s, nl, nl))
+    for E in range(sc.n_s):
+        Q, R = np.linalg.qr(rng.standard_normal((nl, nl)))
+        Phi[E] = (Q * np.sign(np.diag(R))[None, :]).T
+    return Phi
+
+
+def random_basis(sc: Scenario, seed: int) -> np.ndarray:
+    """Phi_E = N seeded random orthonormal columns (generic, no indicator)."""
+    rng = np.random.default_rng(seed)
+    Phi = np.empty((sc.n_s, sc.N, sc.n_loc))
+    for E in range(sc.n_s):
+        Q, R = np.linalg.qr(rng.standard_normal((sc.n_loc, sc.N)))
+        Phi[E] = (Q * np.sign(np.diag(R))[None, :]).T
+    return Phi
+
+
+# ----------------------------------------------------------------------------
+# scenarios
+# ----------------------------------------------------------------------------
+
+def make_scenario(name: str, basis: str = "poly", n_steps: Optional[int] = None) -> Scenario:
+    """The seeded synthetic scenario for BASELINE.json config ``name`` (C1..C5)."""
+    cfg = CONFIGS[name]
+    idx = CONFIG_INDEX[name]
+    sc = Scenario(name=name, dim=cfg["dim"], nx=cfg["nx"], ny=cfg["ny"], nz=cfg["nz"],
+                  sx=cfg["sx"], sy=cfg["sy"], sz=cfg["sz"], N=cfg["N"],
+                  mu_w=1.0, mu_o=cfg["mu_o"], cfl=0.5,
+                  n_steps=cfg["n_steps"] if n_steps is None else n_steps)
+    sc.K = make_permeability(cfg, idx, sc.nx, sc.ny, sc.nz)
+    sc.link_cell, sc.link_axis, sc.link_p, sc.link_s = links_for(cfg["bc"], sc.nx, sc.ny, sc.nz)
+    sc.s0 = np.zeros(sc.n)
+    sc.Phi = make_basis(sc, basis, 100 + idx)
+    return sc
+
+
+def make_basis(sc: Scenario, basis: str, seed: int) -> np.ndarray:
+    if basis == "poly":
+        return poly_basis(sc, seed)
+    if basis == "full":
+        sc.N = sc.n_loc
+        return random_full_basis(sc, seed)
+    if basis == "random":
+        return random_basis(sc, seed)
+    raise ValueError(basis)
+
+
+def custom_scenario(nx, ny, nz, sx, sy, sz, N, *, K=None, seed=0, bc="left_right",
+                    basis="poly", mu_w=1.0, mu_o=1.0, nw=2.0, no=2.0, cfl=0.5, n_steps=1,
+                    s0=None, hx=1.0, hy=1.0, hz=1.0, swr=0.0, sor=0.0) -> Scenario:
+    """Small scenarios for pins and edge cases (same recipes as the configs)."""
+    dim = 3 if nz > 1 else 2
+    sc = Scenario(name="custom", dim=dim, nx=nx, ny=ny, nz=nz, sx=sx, sy=sy, sz=sz, N=N,
+                  hx=hx, hy=hy, hz=hz, mu_w=mu_w, mu_o=mu_o, nw=nw, no=no, swr=swr, sor=sor,
+                  cfl=cfl, n_steps=n_steps)
+    if K is None:
+        rng = np.random.default_rng(seed)
+        K = np.exp(rng.standard_normal(sc.n))
+    sc.K = np.asarray(K, np.float64).reshape(-1)
+    sc.link_cell, sc.link_axis, sc.link_p, sc.link_s = links_for(bc, nx, ny, nz)
+    sc.s0 = np.zeros(sc.n) if s0 is None else np.asarray(s0, np.float64).reshape(-1)
+    sc.Phi = make_basis(sc, basis, 1000 + seed)
+    return sc
