@@ -1,0 +1,165 @@
+/*
+ * lrbms.h -- C ABI of the B200-native LRBMS online step (arXiv 1405.2810).
+ *
+ * One time step of the Localized Reduced Basis Multiscale two-phase scheme,
+ * alg:fullTwoPhaseScheme, with the fine mobility lambda(s^n)
+ * itself as the parameter (direct online projection; reading R3):
+ *
+ *   a1  lambda_i, f_i from s_i          eq:brooksCorey P:183-186, eq:frationalFlow P:201-206
+ *   a2  B_EE' = Phi_E^T A_EE'(lambda) Phi_E', r_E = Phi_E^T b(lambda)
+ *                                        def:coarseScalePressure P:621-631 (k = 0 SWIP, R1/R2)
+ *   a3  solve B c = r                    eq:reducedSystem P:818-821 (exact-solve reading A17)
+ *   a4  p = sum_E Phi_E c_E
+ *   a5  face fluxes + CFL time step      eq:velocityDG P:366-377 (k = 0), reading R4
+ *   a6  explicit upwind transport        eq:saturationDG P:389-399, eq:upwind P:400-417
+ *
+ * Everything is fp64 on one GPU (sm_100a).  The fine grid is a structured
+ * Cartesian grid of nx*ny*nz cells, x fastest (cell c = i + nx*(j + ny*k),
+ * P:245-262); the coarse partition is matching: subdomains of
+ * sx*sy*sz cells, E = I + Sx*(J + Sy*L), local cell l = lx + sx*(ly + sy*lz).
+ *
+ * Conventions
+ *  - Memory: the library never allocates device memory.  The caller (PyTorch in
+ *    the Python binding) owns one workspace of lrbms_workspace_bytes() bytes and
+ *    passes it to lrbms_bind().  All device work is enqueued on the bound stream.
+ *  - (dev) marks device pointers, (host) host pointers.  set_* calls copy their
+ *    inputs stream-ordered into the workspace; callers may free the inputs once
+ *    the stream has synchronised.
+ *  - Errors: no C++ exception crosses the ABI.  Every call returns a status and
+ *    lrbms_last_error() explains it.  CONFIG = invalid sizes/inputs; NUMERICAL =
+ *    non-positive pivot / breakdown, non-converged reduced solve, no flow, NaN
+ *    (device-detected, reported at the end of lrbms_run); CUDA = a CUDA runtime
+ *    error (the context is poisoned: every later call returns LRBMS_E_CUDA);
+ *    STATE = a call out of order (e.g. run before bind / set_*).
+ *  - A context is not thread-safe; separate contexts are independent.
+ */
+#ifndef LRBMS_H
+#define LRBMS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lrbms_ctx lrbms_ctx;
+
+typedef enum {
+  LRBMS_OK = 0,
+  LRBMS_E_CONFIG = 2,
+  LRBMS_E_NUMERICAL = 3,
+  LRBMS_E_IO = 4,
+  LRBMS_E_CUDA = 5,
+  LRBMS_E_STATE = 6
+} lrbms_status;
+
+/* Fine grid + coarse partition + local basis size.
+ * dim = 2 requires nz = sz = 1.  sx | nx, sy | ny, sz | nz.  1 <= N <= min(32, sx*sy*sz).
+ * hx, hy, hz > 0 are the cell widths (|F|/d_F and the cell volume follow from them). */
+typedef struct {
+  int32_t dim, nx, ny, nz;
+  double hx, hy, hz;
+  int32_t sx, sy, sz;
+  int32_t N;
+} lrbms_grid;
+
+/* Fluids (eq:brooksCorey P:183-189; reading R5): k_rw = S_e^nw, k_ro = (1 - S_e)^no,
+ * S_e = clamp((s - swr)/(1 - swr - sor), 0, 1); lambda_w = k_rw/mu_w, lambda_o = k_ro/mu_o.
+ * nw = no = 1 is the paper's linear law; BASELINE.json's configs use 2. */
+typedef struct {
+  double mu_w, mu_o, swr, sor, nw, no;
+} lrbms_fluid;
+
+/* Boundary data as links (reading R6/A13): a Dirichlet boundary face or a
+ * well cell.  Link L couples fine cell cell[L] to the fixed pressure p[L] through the
+ * face normal to axis[L] (0,1,2) at distance h/2: g_L = 2 |F|/h_axis * K_cell * lambda_cell.
+ * s_ext[L] is the saturation entering through the link on inflow (eq:upwind P:405-406).
+ * All arrays (host), n_links entries, copied at create.  Faces without a link are no-flow.
+ * At least one link is required (otherwise A(lambda) is singular). */
+typedef struct {
+  int32_t n_links;
+  const int32_t *cell;
+  const int32_t *axis;
+  const double *p;
+  const double *s_ext;
+} lrbms_links;
+
+/* Reduced-solve options (a3).  The solve is preconditioned CG (block-Jacobi on the
+ * N x N diagonal blocks + coarse correction on the subdomain-indicator coefficients),
+ * warm-started from the previous step's c, iterated until ||r||_2 <= rtol ||r_E||_2. */
+typedef struct {
+  double rtol;            /* default 1e-14 */
+  int32_t max_iters;      /* default 5000 */
+  int32_t coarse_refresh; /* rebuild the coarse-level inverse every k steps (default 10; 1 = every step) */
+  int32_t use_coarse;     /* 1 (default) = two-level, 0 = block-Jacobi only */
+} lrbms_solver_opts;
+
+typedef struct {
+  int64_t steps;          /* steps taken since set_saturation */
+  double t;               /* simulated time sum(dt) */
+  double last_dt;
+  int32_t last_iters;     /* PCG iterations of the last step */
+  int64_t total_iters;    /* PCG iterations since set_saturation */
+  int32_t coarse_rebuilds;
+  double fprime_max;      /* max f_w'(s) used by the CFL step */
+} lrbms_stats;
+
+/* Create a context (host only; no device work).  Validates the configuration. */
+lrbms_status lrbms_create(const lrbms_grid *grid, const lrbms_fluid *fluid,
+                          const lrbms_links *links, lrbms_ctx **out);
+/* Bytes of device workspace the context needs (256-byte aligned). */
+size_t lrbms_workspace_bytes(const lrbms_ctx *ctx);
+/* Bind the caller-owned device workspace (>= lrbms_workspace_bytes) and a CUDA stream
+ * (cudaStream_t passed as void*; NULL = legacy default stream). */
+lrbms_status lrbms_bind(lrbms_ctx *ctx, void *workspace, size_t bytes, void *stream);
+/* Permeability K (dev, n, natural cell order, > 0) and porosity phi (dev, n, > 0) or NULL (= 1). */
+lrbms_status lrbms_set_medium(lrbms_ctx *ctx, const double *K, const double *phi);
+/* Local reduced bases Phi (dev, [n_s][N][n_loc]: basis function k of subdomain E at local
+ * cell l).  Each Phi_E must have full column rank (B must be SPD). */
+lrbms_status lrbms_set_basis(lrbms_ctx *ctx, const double *Phi);
+/* Saturation s^0 (dev, n, natural order); resets time, step count and the warm start. */
+lrbms_status lrbms_set_saturation(lrbms_ctx *ctx, const double *s);
+lrbms_status lrbms_set_solver(lrbms_ctx *ctx, const lrbms_solver_opts *opts);
+
+/* Advance n_steps online steps a1..a6 on the bound stream, no host round trip per step.
+ * dt_fixed > 0 overrides the CFL step (the paper's fixed N_T); otherwise
+ * dt^n = cfl * min_i phi_i V_i / (f'_max Q_i) (reading R4).  dt_log (dev, n_steps) or NULL.
+ * Synchronises the stream once at the end to report device-detected errors. */
+lrbms_status lrbms_run(lrbms_ctx *ctx, int32_t n_steps, double cfl, double dt_fixed,
+                       double *dt_log);
+/* Same, end to end from HOST buffers: copies s_in (host, n, natural order; NULL = keep
+ * the current state) to the device, runs, and copies s_out / p_out (host, n; NULL = skip)
+ * back.  The call a user without device memory makes. */
+lrbms_status lrbms_run_host(lrbms_ctx *ctx, int32_t n_steps, double cfl, double dt_fixed,
+                            const double *s_in, double *s_out, double *p_out);
+/* Current state (dev pointers, natural cell order; NULL = skip): s (n), p (n, pressure of
+ * the last step), c (n_s*N, reduced coefficients of the last step). */
+lrbms_status lrbms_get_state(lrbms_ctx *ctx, double *s, double *p, double *c);
+
+/* Per-stage hooks (the same kernels lrbms_run uses), for parity tests.
+ * project: a1+a2 at the current s; blocks (dev, [n_s][1+dim][N][N]: the diagonal block,
+ *   then the coupling block to E+e_d for d < dim, zero where E has no such neighbour),
+ *   r (dev, [n_s][N]); either may be NULL.
+ * solve: a3 on the last projected system (warm start = current c); c (dev, [n_s][N]) or NULL.
+ * reconstruct: a4 from the current c; p (dev, n, natural order) or NULL.
+ * transport: a5+a6 from the current p and s; advances s; face_flux (dev, interior faces in
+ *   global order: x-faces, then y, then z, each x fastest), link_flux (dev, n_links),
+ *   dt (dev, 1); any may be NULL. */
+lrbms_status lrbms_stage_project(lrbms_ctx *ctx, double *blocks, double *r);
+lrbms_status lrbms_stage_solve(lrbms_ctx *ctx, double *c);
+lrbms_status lrbms_stage_reconstruct(lrbms_ctx *ctx, double *p);
+lrbms_status lrbms_stage_transport(lrbms_ctx *ctx, double cfl, double dt_fixed,
+                                   double *face_flux, double *link_flux, double *dt);
+
+lrbms_status lrbms_get_stats(lrbms_ctx *ctx, lrbms_stats *out);
+/* Number of kernel launches the library enqueued since create (for launch accounting). */
+int64_t lrbms_launch_count(const lrbms_ctx *ctx);
+const char *lrbms_last_error(const lrbms_ctx *ctx);
+const char *lrbms_version(void);
+void lrbms_destroy(lrbms_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRBMS_H */

@@ -1,0 +1,1391 @@
+// lrbms.cu -- B200-native (sm_100a) LRBMS online step behind the C ABI of include/lrbms.h.
+//
+// One online step (alg:fullTwoPhaseScheme, with direct projection R3):
+//   k_project    a1 + a2  one CTA per subdomain: lambda(s) fused into the k = 0 SWIP operator,
+//                         Y = A_EE Phi_E in shared memory, B_EE = Phi_E^T Y, coupling blocks
+//                         B_{E,E+e_d} = -sum_F w_F phi_a phi_b^T, r_E = Phi_E^T b
+//   k_pcg        a3       one cooperative persistent kernel: warp-per-subdomain two-level PCG
+//                         (block-Jacobi + coarse correction), device-side termination
+//   k_recon      a4       p = Phi_E c_E, coalesced streaming read of Phi
+//   k_flux_cfl   a5       face/link fluxes with lambda(s^n), per-cell Q_i, global min dt
+//   k_transport  a6       explicit upwind update
+// plus k_coarse_assemble / k_coarse_gj (coarse-level inverse, rebuilt every few steps).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/lrbms.h"
+#include "lrbms_kernels.cuh"
+
+using namespace lrbms;
+
+// ============================================================================ kernels
+
+// natural <-> internal (subdomain-major) permutations
+__global__ void k_to_internal(Geo g, const double* __restrict__ nat, double* __restrict__ in) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  int E = idx / g.n_loc, l = idx % g.n_loc;
+  int C[3], c[3];
+  sub_xyz(g, E, C);
+  local_xyz(g, l, c);
+  int i = C[0] * g.s[0] + c[0], j = C[1] * g.s[1] + c[1], k = C[2] * g.s[2] + c[2];
+  in[idx] = nat[i + g.nx * (j + g.ny * k)];
+}
+__global__ void k_to_natural(Geo g, const double* __restrict__ in, double* __restrict__ nat) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  int E = idx / g.n_loc, l = idx % g.n_loc;
+  int C[3], c[3];
+  sub_xyz(g, E, C);
+  local_xyz(g, l, c);
+  int i = C[0] * g.s[0] + c[0], j = C[1] * g.s[1] + c[1], k = C[2] * g.s[2] + c[2];
+  nat[i + g.nx * (j + g.ny * k)] = in[idx];
+}
+__global__ void k_fill(double* __restrict__ a, double v, int n) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < n) a[idx] = v;
+}
+__global__ void k_scale_phi(Geo g, double* __restrict__ phiV, int* flags) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  double v = phiV[idx];
+  if (!(v > 0.0)) atomicOr(flags, FLAG_NAN);
+  phiV[idx] = v * g.vol;
+}
+// zc[E][k] = sum_l Phi[E][k][l]: coefficients of the subdomain indicator 1_E (coarse space)
+__global__ void k_basis_indicator(Geo g, const double* __restrict__ Phi, double* __restrict__ zc) {
+  int E = blockIdx.x;
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int k = warp; k < g.N; k += nw) {
+    const double* row = Phi + ((size_t)E * g.N + k) * g.n_loc;
+    double acc = 0.0;
+    for (int l = lane; l < g.n_loc; l += 32) acc += row[l];
+    acc = warp_sum(acc);
+    if (lane == 0) zc[E * g.N + k] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------- a1 + a2
+// Shared memory (doubles): Phs[N][n_loc] | Ys[CH][n_loc] | diag[n_loc] | wp[3][n_loc] |
+//                          bl[n_loc] | wi[3][nfmax] | PhN[N][nfmax]
+struct ProjArgs {
+  Geo g;
+  Flu f;
+  Links L;
+  const double* s;
+  const double* K;
+  const double* Phi;
+  double* blocks;
+  double* rhs;
+  int CH;
+  int nfmax;
+};
+
+__global__ void __launch_bounds__(256) k_project(ProjArgs A) {
+  extern __shared__ double sm[];
+  const Geo& g = A.g;
+  const int N = g.N, nl = g.n_loc, E = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int nb1 = 1 + g.dim;
+  double* Phs = sm;
+  double* Ys = Phs + (size_t)N * nl;
+  double* diag = Ys + (size_t)A.CH * nl;
+  double* wp = diag + nl;            // [3][nl]
+  double* bl = wp + 3 * nl;
+  double* wi = bl + nl;              // [3][nfmax]
+  double* PhN = wi + 3 * A.nfmax;    // [N][nfmax]
+  int C[3];
+  sub_xyz(g, E, C);
+
+  // stage Phi_E (contiguous N * n_loc doubles)
+  const double* PhiE = A.Phi + (size_t)E * N * nl;
+  for (int i = tid; i < N * nl; i += nt) Phs[i] = PhiE[i];
+
+  // a1 + face weights: diag_l = sum of w over all faces of l; w to +a neighbour inside E
+  const size_t base = (size_t)E * nl;
+  for (int l = tid; l < nl; l += nt) {
+    int c[3];
+    local_xyz(g, l, c);
+    const double Kl = A.K[base + l];
+    const double ll = total_mobility(A.f, A.s[base + l]);
+    double d = 0.0;
+    for (int a = 0; a < 3; ++a) wp[a * nl + l] = 0.0;
+    for (int a = 0; a < g.dim; ++a) {
+      for (int dir = -1; dir <= 1; dir += 2) {
+        int nb = neighbour(g, E, C, l, c, a, dir);
+        if (nb < 0) continue;
+        const double Kn = A.K[nb];
+        const double ln = total_mobility(A.f, A.s[nb]);
+        const double w = dir > 0 ? face_weight(g.geo[a], Kl, Kn, ll, ln)
+                                 : face_weight(g.geo[a], Kn, Kl, ln, ll);
+        d += w;
+        if (dir > 0) {
+          if (c[a] + 1 < g.s[a]) wp[a * nl + l] = w;
+          else wi[a * A.nfmax + face_pos(g, c, a)] = w;
+        }
+      }
+    }
+    diag[l] = d;
+    bl[l] = 0.0;
+  }
+  __syncthreads();
+  // links of E (Dirichlet faces / wells, R6): sequential for a deterministic order
+  if (tid == 0) {
+    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
+      const int l = A.L.local[q];
+      const double gL = A.L.geo2[q] * A.K[base + l] * total_mobility(A.f, A.s[base + l]);
+      diag[l] += gL;
+      bl[l] += gL * A.L.p[q];
+    }
+  }
+  __syncthreads();
+
+  // B_EE = Phi^T (A_EE Phi), in column chunks of CH basis functions
+  double* BEE = A.blocks + (size_t)E * nb1 * N * N;
+  for (int j0 = 0; j0 < N; j0 += A.CH) {
+    const int ch = min(A.CH, N - j0);
+    for (int t = tid; t < ch * nl; t += nt) {
+      const int jj = t / nl, l = t % nl;
+      const double* ph = Phs + (size_t)(j0 + jj) * nl;
+      int c[3];
+      local_xyz(g, l, c);
+      double y = diag[l] * ph[l];
+      for (int a = 0; a < g.dim; ++a) {
+        if (c[a] + 1 < g.s[a]) y -= wp[a * nl + l] * ph[l + g.lstride[a]];
+        if (c[a] > 0) y -= wp[a * nl + l - g.lstride[a]] * ph[l - g.lstride[a]];
+      }
+      Ys[(size_t)jj * nl + l] = y;
+    }
+    __syncthreads();
+    for (int t = tid; t < N * ch; t += nt) {
+      const int i = t / ch, jj = t % ch, j = j0 + jj;
+      if (i > j) continue;
+      const double* pi = Phs + (size_t)i * nl;
+      const double* yj = Ys + (size_t)jj * nl;
+      double acc = 0.0;
+      for (int l = 0; l < nl; ++l) acc += pi[l] * yj[l];
+      BEE[i * N + j] = acc;
+      BEE[j * N + i] = acc;
+    }
+    __syncthreads();
+  }
+  // r_E = Phi_E^T b_E
+  for (int i = tid; i < N; i += nt) {
+    double acc = 0.0;
+    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
+      const int l = A.L.local[q];
+      // one term per link cell; cells with several links are summed through bl
+      bool first = true;
+      for (int q2 = A.L.sub_start[E]; q2 < q; ++q2)
+        if (A.L.local[q2] == l) first = false;
+      if (first) acc += Phs[(size_t)i * nl + l] * bl[l];
+    }
+    A.rhs[E * N + i] = acc;
+  }
+  // coupling blocks to the upper neighbours: B_{E,E+a}[i][j] = -sum_f w_f Phi_E[i][a_f] Phi_{E+a}[j][b_f]
+  for (int a = 0; a < g.dim; ++a) {
+    double* BEN = BEE + (size_t)(1 + a) * N * N;
+    if (C[a] + 1 >= g.S[a]) {
+      for (int t = tid; t < N * N; t += nt) BEN[t] = 0.0;
+      continue;
+    }
+    const int En = E + g.Estride[a], nf = g.nface[a];
+    const double* PhiN = A.Phi + (size_t)En * N * nl;
+    __syncthreads();
+    for (int t = tid; t < N * nf; t += nt) {
+      const int k = t / nf, f = t % nf;
+      PhN[(size_t)k * A.nfmax + f] = PhiN[(size_t)k * nl + face_cell(g, f, a, 0)];
+    }
+    __syncthreads();
+    for (int t = tid; t < N * N; t += nt) {
+      const int i = t / N, j = t % N;
+      double acc = 0.0;
+      for (int f = 0; f < nf; ++f)
+        acc += wi[a * A.nfmax + f] * Phs[(size_t)i * nl + face_cell(g, f, a, g.s[a] - 1)] *
+               PhN[(size_t)j * A.nfmax + f];
+      BEN[t] = -acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- a3: PCG
+struct PcgArgs {
+  Geo g;
+  const double* blocks;
+  const double* rhs;
+  const double* zc;
+  const double* Binv;   // [n_pad][n_pad] coarse inverse
+  double* x;
+  double* r;
+  double* z;
+  double* p;
+  double* q;
+  double* DinvT;        // [n_s][N][N]: DinvT[j][k] = (B_EE^-1)[k][j]
+  double* wc;           // [n_s] coarse residual
+  double* partials;     // [4][G]
+  int* iters;
+  int* flags;
+  double rtol;
+  int max_iters;
+  int n_pad;
+  int use_coarse;
+};
+
+// y_E = (B v)_E for lane k < N (warp-level; B symmetric, upper coupling blocks stored)
+__device__ __forceinline__ double spmv_warp(const Geo& g, const double* __restrict__ blocks,
+                                            const double* __restrict__ v, int E, int lane) {
+  const int N = g.N, nb1 = 1 + g.dim;
+  const double* Bd = blocks + (size_t)E * nb1 * N * N;
+  const bool act = lane < N;
+  const double vk = act ? v[E * N + lane] : 0.0;
+  double acc = 0.0;
+  for (int j = 0; j < N; ++j) {
+    const double vj = __shfl_sync(FULL, vk, j);
+    if (act) acc += Bd[j * N + lane] * vj;
+  }
+  int C[3];
+  sub_xyz(g, E, C);
+  for (int a = 0; a < g.dim; ++a) {
+    if (C[a] + 1 < g.S[a]) {   // + B_{E,E+a} v_{E+a}: row access -> warp reductions
+      const double* U = Bd + (size_t)(1 + a) * N * N;
+      const double vn = act ? v[(E + g.Estride[a]) * N + lane] : 0.0;
+      for (int k = 0; k < N; ++k) {
+        double t = act ? U[k * N + lane] * vn : 0.0;
+        t = warp_sum(t);
+        if (lane == k) acc += t;
+      }
+    }
+    if (C[a] > 0) {            // + B_{E-a,E}^T v_{E-a}: column access
+      const int Em = E - g.Estride[a];
+      const double* U = blocks + ((size_t)Em * nb1 + 1 + a) * N * N;
+      const double vm = act ? v[Em * N + lane] : 0.0;
+      for (int j = 0; j < N; ++j) {
+        const double vj = __shfl_sync(FULL, vm, j);
+        if (act) acc += U[j * N + lane] * vj;
+      }
+    }
+  }
+  return acc;
+}
+
+// In-register Gauss-Jordan inverse of the N x N diagonal block (padded to 32 with identity).
+// Lane j holds column j.  No pivoting: B_EE is SPD, pivots are Schur-complement diagonals.
+__device__ __forceinline__ void block_inverse(const double* __restrict__ Bd, double* __restrict__ DinvT,
+                                              int N, int lane, int* flags) {
+  double m[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) m[i] = (lane < N && i < N) ? Bd[i * N + lane] : (i == lane ? 1.0 : 0.0);
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    double f[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) f[i] = __shfl_sync(FULL, m[i], k);
+    const double pk = f[k];
+    bad |= !(pk > 0.0);
+    const double rowk = ((lane == k) ? 1.0 : m[k]) / pk;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i != k) m[i] = ((lane == k) ? 0.0 : m[i]) - f[i] * rowk;
+    m[k] = rowk;
+  }
+  if (bad && lane == 0) atomicOr(flags, FLAG_PIVOT);
+  if (lane < N) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < N) DinvT[lane * N + i] = m[i];
+  }
+}
+
+__global__ void __launch_bounds__(128) k_block_inverse(Geo g, const double* __restrict__ blocks,
+                                                      double* __restrict__ DinvT, int* flags) {
+  const int lane = threadIdx.x & 31;
+  const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (E >= g.n_s) return;
+  block_inverse(blocks + (size_t)E * (1 + g.dim) * g.N * g.N, DinvT + (size_t)E * g.N * g.N, g.N, lane, flags);
+}
+
+template <int W>
+__device__ __forceinline__ void cta_partial(double v, double* red, double* partials, int slot) {
+  // v is warp-uniform; sum warps in order
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < W; ++w) s += red[w];
+    partials[slot * gridDim.x + blockIdx.x] = s;
+  }
+}
+__device__ __forceinline__ double grid_total(const double* partials, int slot) {
+  const int lane = threadIdx.x & 31, G = gridDim.x;
+  double s = 0.0;
+  for (int b = lane; b < G; b += 32) s += partials[slot * G + b];
+  return warp_sum(s);
+}
+
+// z_E = DinvT^T r_E + zc_E e_E,  e_E = sum_F Binv[E][F] wc[F]; returns lane's z and r.z partial
+__device__ __forceinline__ double precond_apply(const PcgArgs& A, int E, int lane, double rk, double& zk) {
+  const int N = A.g.N;
+  const double* Di = A.DinvT + (size_t)E * N * N;
+  double acc = 0.0;
+  for (int j = 0; j < N; ++j) {
+    const double rj = __shfl_sync(FULL, rk, j);
+    if (lane < N) acc += Di[j * N + lane] * rj;
+  }
+  if (A.use_coarse) {
+    const double* row = A.Binv + (size_t)E * A.n_pad;
+    double e = 0.0;
+    for (int F = lane; F < A.g.n_s; F += 32) e += row[F] * A.wc[F];
+    e = warp_sum(e);
+    if (lane < N) acc += A.zc[E * N + lane] * e;
+  }
+  zk = lane < N ? acc : 0.0;
+  return warp_sum(zk * rk);
+}
+
+template <int W>
+__global__ void __launch_bounds__(32 * W, 1) k_pcg(PcgArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[W];
+  const Geo& g = A.g;
+  const int N = g.N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int TW = gridDim.x * W, gw = blockIdx.x * W + warp;
+  const bool act = lane < N;
+
+  // setup: block-Jacobi inverses, r = b - B x, ||b||^2, ||r||^2, coarse residual
+  double pbb = 0.0, prr = 0.0;
+  for (int E = gw; E < g.n_s; E += TW) {
+    const double bx = spmv_warp(g, A.blocks, A.x, E, lane);
+    const double bk = act ? A.rhs[E * N + lane] : 0.0;
+    const double rk = act ? bk - bx : 0.0;
+    if (act) A.r[E * N + lane] = rk;
+    pbb += warp_sum(bk * bk);
+    prr += warp_sum(rk * rk);
+    const double w = warp_sum(act ? A.zc[E * N + lane] * rk : 0.0);
+    if (lane == 0) A.wc[E] = w;
+  }
+  cta_partial<W>(pbb, red, A.partials, 0);
+  cta_partial<W>(prr, red, A.partials, 1);
+  grid.sync();
+  const double bb = grid_total(A.partials, 0);
+  double rr = grid_total(A.partials, 1);
+  const double tol2 = A.rtol * A.rtol * bb;
+  double prz = 0.0;
+  for (int E = gw; E < g.n_s; E += TW) {
+    const double rk = act ? A.r[E * N + lane] : 0.0;
+    double zk;
+    prz += precond_apply(A, E, lane, rk, zk);
+    if (act) { A.z[E * N + lane] = zk; A.p[E * N + lane] = zk; }
+  }
+  cta_partial<W>(prz, red, A.partials, 2);
+  grid.sync();
+  double rz = grid_total(A.partials, 2);
+  int it = 0;
+  if (!(rr <= tol2) && bb > 0.0) {
+    for (it = 1; it <= A.max_iters; ++it) {
+      // q = B p, p.q
+      double ppq = 0.0;
+      for (int E = gw; E < g.n_s; E += TW) {
+        const double qk = spmv_warp(g, A.blocks, A.p, E, lane);
+        const double pk = act ? A.p[E * N + lane] : 0.0;
+        if (act) A.q[E * N + lane] = qk;
+        ppq += warp_sum(act ? pk * qk : 0.0);
+      }
+      cta_partial<W>(ppq, red, A.partials, 3);
+      grid.sync();
+      const double pq = grid_total(A.partials, 3);
+      if (!(pq > 0.0)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
+        break;
+      }
+      const double alpha = rz / pq;
+      prr = 0.0;
+      for (int E = gw; E < g.n_s; E += TW) {
+        double rk = 0.0;
+        if (act) {
+          A.x[E * N + lane] += alpha * A.p[E * N + lane];
+          rk = A.r[E * N + lane] - alpha * A.q[E * N + lane];
+          A.r[E * N + lane] = rk;
+        }
+        prr += warp_sum(rk * rk);
+        const double w = warp_sum(act ? A.zc[E * N + lane] * rk : 0.0);
+        if (lane == 0) A.wc[E] = w;
+      }
+      cta_partial<W>(prr, red, A.partials, 1);
+      grid.sync();
+      rr = grid_total(A.partials, 1);
+      if (rr <= tol2) break;
+      prz = 0.0;
+      for (int E = gw; E < g.n_s; E += TW) {
+        const double rk = act ? A.r[E * N + lane] : 0.0;
+        double zk;
+        prz += precond_apply(A, E, lane, rk, zk);
+        if (act) A.z[E * N + lane] = zk;
+      }
+      cta_partial<W>(prz, red, A.partials, 2);
+      grid.sync();
+      const double rz_new = grid_total(A.partials, 2);
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      for (int E = gw; E < g.n_s; E += TW)
+        if (act) A.p[E * N + lane] = A.z[E * N + lane] + beta * A.p[E * N + lane];
+      grid.sync();
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.iters[0] = it;
+    A.iters[1] += min(it, A.max_iters);
+    if (it > A.max_iters) atomicOr(A.flags, FLAG_NOCONV);
+    if (!(rr == rr)) atomicOr(A.flags, FLAG_NAN);
+  }
+}
+
+// ---------------------------------------------------------------------------- coarse level
+// Bc[E][E'] = zc_E^T B_EE' zc_E' (Galerkin coarse operator on the subdomain indicators).
+__global__ void k_coarse_assemble(Geo g, const double* __restrict__ blocks, const double* __restrict__ zc,
+                                  double* __restrict__ Bc, int n_pad) {
+  const int lane = threadIdx.x & 31;
+  const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (E >= n_pad) return;
+  if (E >= g.n_s) {
+    if (lane == 0) Bc[(size_t)E * n_pad + E] = 1.0;
+    return;
+  }
+  const int N = g.N, nb1 = 1 + g.dim;
+  const bool act = lane < N;
+  const double* Bd = blocks + (size_t)E * nb1 * N * N;
+  const double zk = act ? zc[E * N + lane] : 0.0;
+  double t = 0.0;
+  for (int j = 0; j < N; ++j) {
+    const double zj = __shfl_sync(FULL, zk, j);
+    if (act) t += Bd[j * N + lane] * zj;
+  }
+  const double d = warp_sum(act ? t * zk : 0.0);
+  if (lane == 0) Bc[(size_t)E * n_pad + E] = d;
+  int C[3];
+  sub_xyz(g, E, C);
+  for (int a = 0; a < g.dim; ++a) {
+    if (C[a] + 1 >= g.S[a]) continue;
+    const int En = E + g.Estride[a];
+    const double* U = Bd + (size_t)(1 + a) * N * N;
+    double u = 0.0;   // (U^T zc_E)[lane]
+    for (int k = 0; k < N; ++k) {
+      const double zkk = __shfl_sync(FULL, zk, k);
+      if (act) u += U[k * N + lane] * zkk;
+    }
+    const double o = warp_sum(act ? u * zc[En * N + lane] : 0.0);
+    if (lane == 0) {
+      Bc[(size_t)E * n_pad + En] = o;
+      Bc[(size_t)En * n_pad + E] = o;
+    }
+  }
+}
+
+// Blocked in-place Gauss-Jordan inversion (sweep) of the SPD coarse matrix, 32 x 32 tiles.
+// Per panel K: A_KK <- A_KK^-1; A_KJ <- A_KK^-1 A_KJ; A_IJ -= A_IK A_KJ; A_IK <- -A_IK A_KK^-1.
+__device__ __forceinline__ void tile_load(double (*T)[33], const double* A, int n, int I, int J) {
+  for (int t = threadIdx.x; t < 1024; t += blockDim.x) {
+    const int i = t >> 5, j = t & 31;
+    T[i][j] = A[(size_t)(I * 32 + i) * n + J * 32 + j];
+  }
+}
+__global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* flags) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double P[32][33], T[32][33], F[32][33];
+  __shared__ double rowk[32], colk[32];
+  const int nb = n / 32, tid = threadIdx.x, G = gridDim.x;
+  const int ti = tid >> 3, tj = tid & 7;  // 32 rows x 8 column groups of 4
+  for (int K = 0; K < nb; ++K) {
+    if (blockIdx.x == 0) {
+      tile_load(P, A, n, K, K);
+      __syncthreads();
+      for (int k = 0; k < 32; ++k) {
+        const double pk = P[k][k];
+        if (tid < 32) {
+          rowk[tid] = ((tid == k) ? 1.0 : P[k][tid]) / pk;
+          colk[tid] = P[tid][k];
+        }
+        if (tid == 0 && !(pk > 0.0)) atomicOr(flags, FLAG_PIVOT);
+        __syncthreads();
+        for (int t = tid; t < 1024; t += blockDim.x) {
+          const int i = t >> 5, j = t & 31;
+          if (i == k) P[i][j] = rowk[j];
+          else P[i][j] = ((j == k) ? 0.0 : P[i][j]) - colk[i] * rowk[j];
+        }
+        __syncthreads();
+      }
+      for (int t = tid; t < 1024; t += blockDim.x) {
+        const int i = t >> 5, j = t & 31;
+        A[(size_t)(K * 32 + i) * n + K * 32 + j] = P[i][j];
+      }
+    }
+    grid.sync();
+    // row panel: A_KJ <- P A_KJ
+    bool loaded = false;
+    for (int J = blockIdx.x; J < nb; J += G) {
+      if (J == K) continue;
+      if (!loaded) { tile_load(P, A, n, K, K); loaded = true; }
+      tile_load(T, A, n, K, J);
+      __syncthreads();
+      double acc[4] = {0, 0, 0, 0};
+      for (int kk = 0; kk < 32; ++kk) {
+        const double a = P[ti][kk];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += a * T[kk][tj + 8 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) A[(size_t)(K * 32 + ti) * n + J * 32 + tj + 8 * q] = acc[q];
+      __syncthreads();
+    }
+    grid.sync();
+    // rank-32 update of all tiles outside row/column K
+    const int nt = (nb - 1) * (nb - 1);
+    for (int t = blockIdx.x; t < nt; t += G) {
+      int I = t / (nb - 1), J = t % (nb - 1);
+      if (I >= K) ++I;
+      if (J >= K) ++J;
+      tile_load(F, A, n, I, K);
+      tile_load(T, A, n, K, J);
+      __syncthreads();
+      double acc[4] = {0, 0, 0, 0};
+      for (int kk = 0; kk < 32; ++kk) {
+        const double a = F[ti][kk];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += a * T[kk][tj + 8 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) A[(size_t)(I * 32 + ti) * n + J * 32 + tj + 8 * q] -= acc[q];
+      __syncthreads();
+    }
+    grid.sync();
+    // column panel: A_IK <- -A_IK P
+    loaded = false;
+    for (int I = blockIdx.x; I < nb; I += G) {
+      if (I == K) continue;
+      if (!loaded) { tile_load(P, A, n, K, K); loaded = true; }
+      tile_load(F, A, n, I, K);
+      __syncthreads();
+      double acc[4] = {0, 0, 0, 0};
+      for (int kk = 0; kk < 32; ++kk) {
+        const double a = F[ti][kk];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += a * P[kk][tj + 8 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) A[(size_t)(I * 32 + ti) * n + K * 32 + tj + 8 * q] = -acc[q];
+      __syncthreads();
+    }
+    grid.sync();
+  }
+}
+
+// ---------------------------------------------------------------------------- a4: reconstruction
+__global__ void k_recon(Geo g, const double* __restrict__ Phi, const double* __restrict__ c,
+                        double* __restrict__ p, unsigned long long* dt_bits) {
+  __shared__ double cs[32];
+  const int E = blockIdx.x, N = g.N, nl = g.n_loc;
+  if (threadIdx.x < N) cs[threadIdx.x] = c[E * N + threadIdx.x];
+  if (E == 0 && threadIdx.x == 0) *dt_bits = 0x7ff0000000000000ull;  // +inf: reset the dt min
+  __syncthreads();
+  const double* PhiE = Phi + (size_t)E * N * nl;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < N; ++k) acc += PhiE[(size_t)k * nl + l] * cs[k];
+    p[(size_t)E * nl + l] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------- a5 + a6
+struct FluxArgs {
+  Geo g;
+  Flu f;
+  Links L;
+  const double* s;
+  const double* K;
+  const double* p;
+  const double* phiV;   // phi * V or nullptr (phi = 1)
+  double* s_out;
+  unsigned long long* dt_bits;
+  double* dt_log;       // [steps] or nullptr
+  double* t_acc;        // simulated time
+  double* face_flux;    // natural interior-face order or nullptr
+  double* link_flux;    // caller link order or nullptr
+  int* flags;
+  double cfl;
+  double fpmax;
+  double dt_fixed;
+  int step;
+};
+
+// flux on the face between cell (this, lower if dir > 0) and its neighbour nb; returns the
+// flux leaving this cell and, optionally, the fractional-flow-weighted flux leaving it.
+__device__ __forceinline__ double out_flux(const FluxArgs& A, int a, int dir, double Kl, double ll,
+                                           double pl, double sl, int nb, double& fwout) {
+  const double Kn = A.K[nb];
+  const double sn = A.s[nb];
+  const double ln = total_mobility(A.f, sn);
+  const double pn = A.p[nb];
+  double F, s_up;
+  if (dir > 0) {   // this = T1, nb = T2: F = w (p1 - p2), leaving this cell
+    F = face_weight(A.g.geo[a], Kl, Kn, ll, ln) * (pl - pn);
+    s_up = F >= 0.0 ? sl : sn;
+    fwout = F * frac_flow(A.f, s_up);
+    return F;
+  }
+  // nb = T1, this = T2: F = w (p1 - p2) leaves T1, i.e. -F leaves this cell
+  F = face_weight(A.g.geo[a], Kn, Kl, ln, ll) * (pn - pl);
+  s_up = F >= 0.0 ? sn : sl;
+  fwout = -(F * frac_flow(A.f, s_up));
+  return -F;
+}
+
+__device__ __forceinline__ size_t face_index(const Geo& g, int i, int j, int k, int a) {
+  const size_t nxf = (size_t)(g.nx - 1) * g.ny * g.nz;
+  const size_t nyf = (size_t)g.nx * (g.ny - 1) * g.nz;
+  if (a == 0) return i + (size_t)(g.nx - 1) * (j + (size_t)g.ny * k);
+  if (a == 1) return nxf + i + (size_t)g.nx * (j + (size_t)(g.ny - 1) * k);
+  return nxf + nyf + i + (size_t)g.nx * (j + (size_t)g.ny * k);
+}
+
+// a5: Q_i = max(sum of outflow, sum of inflow); dt = cfl min phi V / (f'max Q)   (R4)
+__global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
+  extern __shared__ double sm[];
+  const Geo& g = A.g;
+  const int E = blockIdx.x, nl = g.n_loc;
+  double* opos = sm;
+  double* oneg = sm + nl;
+  __shared__ double redmin[32];
+  int C[3];
+  sub_xyz(g, E, C);
+  const size_t base = (size_t)E * nl;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    int c[3];
+    local_xyz(g, l, c);
+    const double Kl = A.K[base + l], sl = A.s[base + l], pl = A.p[base + l];
+    const double ll = total_mobility(A.f, sl);
+    double pos = 0.0, neg = 0.0;
+    for (int a = 0; a < g.dim; ++a)
+      for (int dir = -1; dir <= 1; dir += 2) {
+        const int nb = neighbour(g, E, C, l, c, a, dir);
+        if (nb < 0) continue;
+        double fw;
+        const double F = out_flux(A, a, dir, Kl, ll, pl, sl, nb, fw);
+        pos += fmax(F, 0.0);
+        neg += fmax(-F, 0.0);
+        if (A.face_flux && dir > 0) {
+          const int i = C[0] * g.s[0] + c[0], j = C[1] * g.s[1] + c[1], k = C[2] * g.s[2] + c[2];
+          A.face_flux[face_index(g, i, j, k, a)] = F;
+        }
+      }
+    opos[l] = pos;
+    oneg[l] = neg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
+      const int l = A.L.local[q];
+      const double sl = A.s[base + l];
+      const double F = A.L.geo2[q] * A.K[base + l] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
+      opos[l] += fmax(F, 0.0);
+      oneg[l] += fmax(-F, 0.0);
+      if (A.link_flux) A.link_flux[A.L.orig[q]] = F;
+    }
+  }
+  __syncthreads();
+  double mn = INFINITY;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const double Q = fmax(opos[l], oneg[l]);
+    if (Q > 0.0) {
+      const double pv = A.phiV ? A.phiV[base + l] : g.vol;
+      mn = fmin(mn, A.cfl * pv / (A.fpmax * Q));
+    }
+    if (!(Q == Q)) atomicOr(A.flags, FLAG_NAN);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(FULL, mn, o));
+  if ((threadIdx.x & 31) == 0) redmin[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, redmin[w]);
+    if (m < INFINITY) atomicMin(A.dt_bits, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// a6: s^{n+1}_i = s^n_i - dt/(phi_i V) sum_F F_F^{out} f(chi(s^n))  (eq:saturationDG at k = 0, A5)
+__global__ void __launch_bounds__(512) k_transport(FluxArgs A) {
+  extern __shared__ double sm[];
+  const Geo& g = A.g;
+  const int E = blockIdx.x, nl = g.n_loc;
+  double* net = sm;
+  int C[3];
+  sub_xyz(g, E, C);
+  const size_t base = (size_t)E * nl;
+  double dt = A.dt_fixed;
+  if (!(dt > 0.0)) {
+    const unsigned long long bits = *((volatile unsigned long long*)A.dt_bits);
+    dt = __longlong_as_double((long long)bits);
+  }
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    int c[3];
+    local_xyz(g, l, c);
+    const double Kl = A.K[base + l], sl = A.s[base + l], pl = A.p[base + l];
+    const double ll = total_mobility(A.f, sl);
+    double acc = 0.0;
+    for (int a = 0; a < g.dim; ++a)
+      for (int dir = -1; dir <= 1; dir += 2) {
+        const int nb = neighbour(g, E, C, l, c, a, dir);
+        if (nb < 0) continue;
+        double fw;
+        out_flux(A, a, dir, Kl, ll, pl, sl, nb, fw);
+        acc += fw;
+      }
+    net[l] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
+      const int l = A.L.local[q];
+      const double sl = A.s[base + l];
+      const double F = A.L.geo2[q] * A.K[base + l] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
+      const double s_up = F >= 0.0 ? sl : A.L.s_ext[q];
+      net[l] += F * frac_flow(A.f, s_up);
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const double pv = A.phiV ? A.phiV[base + l] : g.vol;
+    const double sn = A.s[base + l] - dt / pv * net[l];
+    A.s_out[base + l] = sn;
+    if (!(sn == sn)) atomicOr(A.flags, FLAG_NAN);
+  }
+  if (E == 0 && threadIdx.x == 0) {
+    if (!(dt < INFINITY)) atomicOr(A.flags, FLAG_NOFLOW);
+    *A.t_acc += dt;
+    A.t_acc[1] = dt;
+    if (A.dt_log) A.dt_log[A.step] = dt;
+  }
+}
+
+// ============================================================================ host side
+
+namespace {
+
+struct Buf {
+  size_t off = 0, bytes = 0;
+};
+
+}  // namespace
+
+struct lrbms_ctx {
+  Geo g{};
+  Flu f{};
+  int n_links = 0;
+  std::vector<int> h_sub_start, h_local, h_orig;
+  std::vector<double> h_geo2, h_p, h_s;
+  double fpmax = 0.0;
+  lrbms_solver_opts opts{1e-14, 5000, 10, 1};
+  int n_pad = 0;
+  int pcg_W = 1, pcg_G = 1, gj_G = 1;
+  int proj_CH = 8, proj_nfmax = 1;
+  size_t proj_smem = 0;
+  // workspace layout
+  Buf K, phiV, s0, s1, p, Phi, zc, blocks, rhs, c, r, z, pv, q, DinvT, wc, Binv, partials, scal, flags,
+      iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
+  size_t ws_bytes = 0;
+  char* ws = nullptr;
+  cudaStream_t stream = nullptr;
+  bool bound = false, have_medium = false, have_phi = false, have_basis = false, have_sat = false;
+  bool poisoned = false;
+  bool have_blocks = false;
+  int cur = 0;                 // which s buffer is current
+  int64_t steps = 0, total_iters = 0, launches = 0;
+  int last_iters = 0, rebuilds = 0;
+  int64_t last_rebuild_step = -1;
+  std::string err;
+
+  template <class T>
+  T* at(const Buf& b) const { return reinterpret_cast<T*>(ws + b.off); }
+  double* s_cur() const { return at<double>(cur ? s1 : s0); }
+  double* s_nxt() const { return at<double>(cur ? s0 : s1); }
+};
+
+static lrbms_status fail(lrbms_ctx* c, lrbms_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (st == LRBMS_E_CUDA) c->poisoned = true;
+  }
+  return st;
+}
+#define CUDA_TRY(ctx, call)                                                                       \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(ctx, LRBMS_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define LAUNCH_CHECK(ctx)                                                                      \
+  do {                                                                                         \
+    (ctx)->launches++;                                                                         \
+    cudaError_t e_ = cudaGetLastError();                                                       \
+    if (e_ != cudaSuccess) return fail(ctx, LRBMS_E_CUDA, "launch: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+// f_w'(s) and its max over [swr, 1 - sor] (reading R4): dense sampling + golden section
+static double fw_prime(const Flu& f, double s) {
+  double se = (s - f.swr) / f.range;
+  se = std::min(std::max(se, 0.0), 1.0);
+  double a = std::pow(se, f.nw) / f.mu_w, b = std::pow(1.0 - se, f.no) / f.mu_o;
+  double da = f.nw * std::pow(se, f.nw - 1.0) / f.mu_w;
+  double db = -f.no * std::pow(1.0 - se, f.no - 1.0) / f.mu_o;
+  return (da * b - a * db) / ((a + b) * (a + b)) / f.range;
+}
+static double fprime_max_host(const Flu& f) {
+  const int M = 20001;
+  double lo = f.swr, hi = f.swr + f.range;
+  int kbest = 0;
+  double vbest = -1.0;
+  for (int k = 0; k < M; ++k) {
+    double x = lo + (hi - lo) * k / (M - 1);
+    double v = fw_prime(f, x);
+    if (v > vbest) { vbest = v; kbest = k; }
+  }
+  double a = lo + (hi - lo) * std::max(kbest - 1, 0) / (M - 1);
+  double b = lo + (hi - lo) * std::min(kbest + 1, M - 1) / (M - 1);
+  const double gr = (std::sqrt(5.0) - 1.0) / 2.0;
+  for (int it = 0; it < 200 && b - a >= 1e-15; ++it) {
+    double c = b - gr * (b - a), d = a + gr * (b - a);
+    if (fw_prime(f, c) >= fw_prime(f, d)) b = d; else a = c;
+  }
+  return std::max(fw_prime(f, 0.5 * (a + b)), vbest);
+}
+
+static lrbms_status check_ctx(lrbms_ctx* c, bool need_bound = true) {
+  if (!c) return LRBMS_E_STATE;
+  if (c->poisoned) return fail(c, LRBMS_E_CUDA, "context poisoned by an earlier CUDA error: %s", c->err.c_str());
+  if (need_bound && !c->bound) return fail(c, LRBMS_E_STATE, "lrbms_bind has not been called");
+  return LRBMS_OK;
+}
+
+static int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+extern "C" {
+
+const char* lrbms_version(void) { return "lrbms-b200 0.1 (sm_100a, fp64)"; }
+
+lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrbms_links* lk, lrbms_ctx** out) {
+  if (!out) return LRBMS_E_CONFIG;
+  *out = nullptr;
+  if (!gr || !fl || !lk) return LRBMS_E_CONFIG;
+  lrbms_ctx* c = new lrbms_ctx();
+  Geo& g = c->g;
+  if (gr->dim != 2 && gr->dim != 3) { lrbms_status st = fail(c, LRBMS_E_CONFIG, "dim must be 2 or 3"); *out = c; return st; }
+  auto bad = [&](const char* m) { lrbms_status st = fail(c, LRBMS_E_CONFIG, "%s", m); *out = c; return st; };
+  if (gr->nx < 1 || gr->ny < 1 || gr->nz < 1 || gr->sx < 1 || gr->sy < 1 || gr->sz < 1) return bad("sizes must be >= 1");
+  if (gr->dim == 2 && (gr->nz != 1 || gr->sz != 1)) return bad("dim = 2 requires nz = sz = 1");
+  if (gr->nx % gr->sx || gr->ny % gr->sy || gr->nz % gr->sz) return bad("subdomain size must divide the grid (matching partition, P:597-600)");
+  if (!(gr->hx > 0) || !(gr->hy > 0) || !(gr->hz > 0)) return bad("cell widths must be > 0");
+  const long long nll = (long long)gr->nx * gr->ny * gr->nz;
+  if (nll > (1LL << 30)) return bad("grid too large");
+  g.dim = gr->dim; g.nx = gr->nx; g.ny = gr->ny; g.nz = gr->nz;
+  g.s[0] = gr->sx; g.s[1] = gr->sy; g.s[2] = gr->sz;
+  g.S[0] = gr->nx / gr->sx; g.S[1] = gr->ny / gr->sy; g.S[2] = gr->nz / gr->sz;
+  g.n_s = g.S[0] * g.S[1] * g.S[2];
+  g.n_loc = gr->sx * gr->sy * gr->sz;
+  g.N = gr->N;
+  g.n = (int)nll;
+  if (g.N < 1 || g.N > 32 || g.N > g.n_loc) return bad("need 1 <= N <= min(32, n_loc)");
+  if (g.n_loc > 4096) return bad("n_loc > 4096 not supported");
+  g.lstride[0] = 1; g.lstride[1] = g.s[0]; g.lstride[2] = g.s[0] * g.s[1];
+  g.Estride[0] = 1; g.Estride[1] = g.S[0]; g.Estride[2] = g.S[0] * g.S[1];
+  for (int a = 0; a < 3; ++a) g.nface[a] = g.n_loc / g.s[a];
+  const double h[3] = {gr->hx, gr->hy, gr->hz};
+  for (int a = 0; a < 3; ++a) {
+    const double area = h[(a + 1) % 3] * h[(a + 2) % 3];
+    g.geo[a] = area / h[a];
+    g.geo2[a] = 2.0 * area / h[a];
+  }
+  g.vol = h[0] * h[1] * h[2];
+  Flu& f = c->f;
+  if (!(fl->mu_w > 0) || !(fl->mu_o > 0)) return bad("viscosities must be > 0");
+  if (!(fl->swr >= 0) || !(fl->sor >= 0) || !(fl->swr + fl->sor < 1)) return bad("need swr, sor >= 0, swr + sor < 1");
+  if (!(fl->nw >= 1) || !(fl->no >= 1)) return bad("Corey exponents must be >= 1");
+  f.mu_w = fl->mu_w; f.mu_o = fl->mu_o; f.swr = fl->swr; f.range = 1.0 - fl->swr - fl->sor;
+  f.nw = fl->nw; f.no = fl->no;
+  f.kind = (fl->nw == 2.0 && fl->no == 2.0) ? 2 : ((fl->nw == 1.0 && fl->no == 1.0) ? 1 : 0);
+  c->fpmax = fprime_max_host(f);
+  // links, bucketed by subdomain
+  if (lk->n_links < 1) return bad("at least one Dirichlet link is required (A(lambda) would be singular)");
+  if (!lk->cell || !lk->axis || !lk->p || !lk->s_ext) return bad("null link array");
+  const int nl = lk->n_links;
+  c->n_links = nl;
+  struct Rec { int E, l, orig, axis; };
+  std::vector<Rec> recs(nl);
+  for (int q = 0; q < nl; ++q) {
+    const int cell = lk->cell[q], ax = lk->axis[q];
+    if (cell < 0 || cell >= g.n) return bad("link cell out of range");
+    if (ax < 0 || ax >= g.dim) return bad("link axis out of range");
+    const int i = cell % g.nx, j = (cell / g.nx) % g.ny, k = cell / (g.nx * g.ny);
+    const int E = i / g.s[0] + g.S[0] * (j / g.s[1] + g.S[1] * (k / g.s[2]));
+    const int l = i % g.s[0] + g.s[0] * (j % g.s[1] + g.s[1] * (k % g.s[2]));
+    recs[q] = {E, l, q, ax};
+  }
+  std::stable_sort(recs.begin(), recs.end(), [](const Rec& a, const Rec& b) {
+    return a.E != b.E ? a.E < b.E : a.l < b.l;
+  });
+  c->h_sub_start.assign(g.n_s + 1, 0);
+  for (auto& r : recs) c->h_sub_start[r.E + 1]++;
+  for (int E = 0; E < g.n_s; ++E) c->h_sub_start[E + 1] += c->h_sub_start[E];
+  for (auto& r : recs) {
+    c->h_local.push_back(r.l);
+    c->h_orig.push_back(r.orig);
+    c->h_geo2.push_back(g.geo2[r.axis]);
+    c->h_p.push_back(lk->p[r.orig]);
+    c->h_s.push_back(lk->s_ext[r.orig]);
+  }
+  // launch geometry
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 148;
+  int W = 1;
+  while (W < 16 && sms * W < g.n_s) W *= 2;
+  c->pcg_W = W;
+  c->pcg_G = std::min(cdiv(g.n_s, W), sms);   // refined at bind (occupancy)
+  c->n_pad = cdiv(g.n_s, 32) * 32;
+  c->gj_G = sms;
+  int nfmax = 1;
+  for (int a = 0; a < g.dim; ++a) nfmax = std::max(nfmax, g.nface[a]);
+  c->proj_nfmax = nfmax;
+  c->proj_CH = std::min(g.N, 8);
+  c->proj_smem = sizeof(double) * ((size_t)g.N * g.n_loc + (size_t)c->proj_CH * g.n_loc + 5 * (size_t)g.n_loc +
+                                   3 * (size_t)nfmax + (size_t)g.N * nfmax);
+  if (c->proj_smem > 227 * 1024) return bad("subdomain too large for the shared-memory projection (N * n_loc too big)");
+  // workspace layout
+  size_t off = 0;
+  auto alloc = [&](Buf& b, size_t bytes) {
+    b.off = off;
+    b.bytes = bytes;
+    off += (bytes + 255) / 256 * 256;
+  };
+  const size_t n = g.n, R = (size_t)g.n_s * g.N;
+  alloc(c->K, n * 8); alloc(c->phiV, n * 8); alloc(c->s0, n * 8); alloc(c->s1, n * 8); alloc(c->p, n * 8);
+  alloc(c->tmp, n * 8);
+  alloc(c->Phi, (size_t)g.n_s * g.N * g.n_loc * 8);
+  alloc(c->zc, R * 8);
+  alloc(c->blocks, (size_t)g.n_s * (1 + g.dim) * g.N * g.N * 8);
+  alloc(c->rhs, R * 8); alloc(c->c, R * 8); alloc(c->r, R * 8); alloc(c->z, R * 8); alloc(c->pv, R * 8);
+  alloc(c->q, R * 8);
+  alloc(c->DinvT, (size_t)g.n_s * g.N * g.N * 8);
+  alloc(c->wc, (size_t)c->n_pad * 8);
+  alloc(c->Binv, (size_t)c->n_pad * c->n_pad * 8);
+  alloc(c->partials, 8 * (size_t)4 * 4096);
+  alloc(c->scal, 8 * 16);
+  alloc(c->flags, 4 * 16);
+  alloc(c->iters, 4 * 16);
+  alloc(c->l_start, 4 * (size_t)(g.n_s + 1));
+  alloc(c->l_local, 4 * (size_t)nl); alloc(c->l_orig, 4 * (size_t)nl);
+  alloc(c->l_geo2, 8 * (size_t)nl); alloc(c->l_p, 8 * (size_t)nl); alloc(c->l_s, 8 * (size_t)nl);
+  c->ws_bytes = off;
+  *out = c;
+  return LRBMS_OK;
+}
+
+size_t lrbms_workspace_bytes(const lrbms_ctx* c) { return c ? c->ws_bytes : 0; }
+
+lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
+  lrbms_status st = check_ctx(c, false);
+  if (st) return st;
+  if (!ws || bytes < c->ws_bytes) return fail(c, LRBMS_E_CONFIG, "workspace too small (%zu < %zu)", bytes, c->ws_bytes);
+  if (((uintptr_t)ws) % 256) return fail(c, LRBMS_E_CONFIG, "workspace must be 256-byte aligned");
+  c->ws = (char*)ws;
+  c->stream = (cudaStream_t)stream;
+  // occupancy-limited cooperative grids
+  int dev = 0, sms = 148;
+  CUDA_TRY(c, cudaGetDevice(&dev));
+  CUDA_TRY(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int occ = 0;
+  const int W = c->pcg_W;
+  const void* kp = W == 1 ? (const void*)k_pcg<1> : W == 2 ? (const void*)k_pcg<2> : W == 4 ? (const void*)k_pcg<4>
+                 : W == 8 ? (const void*)k_pcg<8> : (const void*)k_pcg<16>;
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kp, 32 * W, 0));
+  if (occ < 1) return fail(c, LRBMS_E_CUDA, "PCG kernel cannot be resident");
+  c->pcg_G = std::max(1, std::min(cdiv(c->g.n_s, W), sms * occ));
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_coarse_gj, 256, 0));
+  if (occ < 1) return fail(c, LRBMS_E_CUDA, "GJ kernel cannot be resident");
+  c->gj_G = sms * std::min(occ, 2);
+  CUDA_TRY(c, cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * c->g.n_loc));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_transport, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * c->g.n_loc));
+  // link tables
+  const Geo& g = c->g;
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<int>(c->l_start), c->h_sub_start.data(), 4 * (g.n_s + 1), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<int>(c->l_local), c->h_local.data(), 4 * c->n_links, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<int>(c->l_orig), c->h_orig.data(), 4 * c->n_links, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<double>(c->l_geo2), c->h_geo2.data(), 8 * c->n_links, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<double>(c->l_p), c->h_p.data(), 8 * c->n_links, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<double>(c->l_s), c->h_s.data(), 8 * c->n_links, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->flags), 0, 64, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->scal), 0, 128, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // host link vectors may be freed by the caller
+  c->bound = true;
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_set_medium(lrbms_ctx* c, const double* K, const double* phi) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!K) return fail(c, LRBMS_E_CONFIG, "K is NULL");
+  const Geo& g = c->g;
+  const int nb = cdiv(g.n, 256);
+  k_to_internal<<<nb, 256, 0, c->stream>>>(g, K, c->at<double>(c->K));
+  LAUNCH_CHECK(c);
+  if (phi) {
+    k_to_internal<<<nb, 256, 0, c->stream>>>(g, phi, c->at<double>(c->phiV));
+    LAUNCH_CHECK(c);
+    k_scale_phi<<<nb, 256, 0, c->stream>>>(g, c->at<double>(c->phiV), c->at<int>(c->flags) + 1);
+    LAUNCH_CHECK(c);
+  }
+  c->have_phi = phi != nullptr;
+  // validate K > 0 (host check of a device min would need a sync; do it once here)
+  std::vector<double> hk(g.n);
+  CUDA_TRY(c, cudaMemcpyAsync(hk.data(), K, 8 * (size_t)g.n, cudaMemcpyDeviceToHost, c->stream));
+  int hf[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(hf, c->at<int>(c->flags), 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  for (double v : hk)
+    if (!(v > 0.0) || !std::isfinite(v)) return fail(c, LRBMS_E_CONFIG, "K must be finite and > 0");
+  if (hf[1]) {
+    CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->flags) + 1, 0, 4, c->stream));
+    return fail(c, LRBMS_E_CONFIG, "phi must be > 0");
+  }
+  c->have_medium = true;
+  c->have_blocks = false;
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_set_basis(lrbms_ctx* c, const double* Phi) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!Phi) return fail(c, LRBMS_E_CONFIG, "Phi is NULL");
+  const Geo& g = c->g;
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<double>(c->Phi), Phi, c->Phi.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  k_basis_indicator<<<g.n_s, 256, 0, c->stream>>>(g, c->at<double>(c->Phi), c->at<double>(c->zc));
+  LAUNCH_CHECK(c);
+  c->have_basis = true;
+  c->have_blocks = false;
+  c->last_rebuild_step = -1;
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!s) return fail(c, LRBMS_E_CONFIG, "s is NULL");
+  const Geo& g = c->g;
+  c->cur = 0;
+  k_to_internal<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, s, c->s_cur());
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->c), 0, c->c.bytes, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->p), 0, c->p.bytes, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->scal), 0, 128, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->iters), 0, 64, c->stream));
+  c->steps = 0;
+  c->total_iters = 0;
+  c->last_iters = 0;
+  c->last_rebuild_step = -1;
+  c->have_sat = true;
+  c->have_blocks = false;
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_set_solver(lrbms_ctx* c, const lrbms_solver_opts* o) {
+  lrbms_status st = check_ctx(c, false);
+  if (st) return st;
+  if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1)
+    return fail(c, LRBMS_E_CONFIG, "invalid solver options");
+  c->opts = *o;
+  c->last_rebuild_step = -1;
+  return LRBMS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------- stage launchers
+static Links links_of(const lrbms_ctx* c) {
+  Links L;
+  L.sub_start = c->at<int>(c->l_start);
+  L.local = c->at<int>(c->l_local);
+  L.orig = c->at<int>(c->l_orig);
+  L.geo2 = c->at<double>(c->l_geo2);
+  L.p = c->at<double>(c->l_p);
+  L.s_ext = c->at<double>(c->l_s);
+  return L;
+}
+
+static lrbms_status ready(lrbms_ctx* c) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!c->have_medium || !c->have_basis || !c->have_sat)
+    return fail(c, LRBMS_E_STATE, "set_medium, set_basis and set_saturation must precede the step");
+  return LRBMS_OK;
+}
+
+static lrbms_status launch_project(lrbms_ctx* c) {
+  ProjArgs A;
+  A.g = c->g; A.f = c->f; A.L = links_of(c);
+  A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
+  A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs);
+  A.CH = c->proj_CH; A.nfmax = c->proj_nfmax;
+  k_project<<<c->g.n_s, 256, c->proj_smem, c->stream>>>(A);
+  LAUNCH_CHECK(c);
+  c->have_blocks = true;
+  return LRBMS_OK;
+}
+
+static lrbms_status launch_coarse(lrbms_ctx* c) {
+  const Geo& g = c->g;
+  double* Bc = c->at<double>(c->Binv);
+  CUDA_TRY(c, cudaMemsetAsync(Bc, 0, c->Binv.bytes, c->stream));
+  k_coarse_assemble<<<cdiv(c->n_pad, 8), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->zc), Bc, c->n_pad);
+  LAUNCH_CHECK(c);
+  int n = c->n_pad;
+  int* fl = c->at<int>(c->flags);
+  void* args[] = {&Bc, &n, &fl};
+  CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj, dim3(c->gj_G), dim3(256), args, 0, c->stream));
+  c->launches++;
+  c->rebuilds++;
+  c->last_rebuild_step = c->steps;
+  return LRBMS_OK;
+}
+
+static lrbms_status launch_solve(lrbms_ctx* c) {
+  const Geo& g = c->g;
+  const bool coarse = c->opts.use_coarse && g.n_s > 1;
+  if (coarse && (c->last_rebuild_step < 0 || c->steps - c->last_rebuild_step >= c->opts.coarse_refresh)) {
+    lrbms_status st = launch_coarse(c);
+    if (st) return st;
+  }
+  k_block_inverse<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->DinvT),
+                                                          c->at<int>(c->flags));
+  LAUNCH_CHECK(c);
+  PcgArgs A;
+  A.g = g;
+  A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs); A.zc = c->at<double>(c->zc);
+  A.Binv = c->at<double>(c->Binv);
+  A.x = c->at<double>(c->c); A.r = c->at<double>(c->r); A.z = c->at<double>(c->z); A.p = c->at<double>(c->pv);
+  A.q = c->at<double>(c->q); A.DinvT = c->at<double>(c->DinvT); A.wc = c->at<double>(c->wc);
+  A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
+  A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
+  void* args[] = {&A};
+  const int W = c->pcg_W;
+  const void* kp = W == 1 ? (const void*)k_pcg<1> : W == 2 ? (const void*)k_pcg<2> : W == 4 ? (const void*)k_pcg<4>
+                 : W == 8 ? (const void*)k_pcg<8> : (const void*)k_pcg<16>;
+  CUDA_TRY(c, cudaLaunchCooperativeKernel(kp, dim3(c->pcg_G), dim3(32 * W), args, 0, c->stream));
+  c->launches++;
+  return LRBMS_OK;
+}
+
+static lrbms_status launch_recon(lrbms_ctx* c) {
+  const Geo& g = c->g;
+  const int nt = std::min(1024, cdiv(g.n_loc, 32) * 32);
+  k_recon<<<g.n_s, nt, 0, c->stream>>>(g, c->at<double>(c->Phi), c->at<double>(c->c), c->at<double>(c->p),
+                                       (unsigned long long*)c->at<double>(c->scal));
+  LAUNCH_CHECK(c);
+  return LRBMS_OK;
+}
+
+static FluxArgs flux_args(lrbms_ctx* c, double cfl, double dt_fixed, double* dt_log, int step) {
+  FluxArgs A;
+  A.g = c->g; A.f = c->f; A.L = links_of(c);
+  A.s = c->s_cur(); A.K = c->at<double>(c->K); A.p = c->at<double>(c->p);
+  A.phiV = c->have_phi ? c->at<double>(c->phiV) : nullptr;
+  A.s_out = c->s_nxt();
+  A.dt_bits = (unsigned long long*)c->at<double>(c->scal);
+  A.t_acc = c->at<double>(c->scal) + 1;
+  A.dt_log = dt_log;
+  A.face_flux = nullptr; A.link_flux = nullptr;
+  A.flags = c->at<int>(c->flags);
+  A.cfl = cfl; A.fpmax = c->fpmax; A.dt_fixed = dt_fixed; A.step = step;
+  return A;
+}
+
+static lrbms_status launch_transport(lrbms_ctx* c, double cfl, double dt_fixed, double* dt_log, int step,
+                                     double* face_flux, double* link_flux) {
+  const Geo& g = c->g;
+  const int nt = std::min(512, cdiv(g.n_loc, 32) * 32);
+  FluxArgs A = flux_args(c, cfl, dt_fixed, dt_log, step);
+  A.face_flux = face_flux;
+  A.link_flux = link_flux;
+  k_flux_cfl<<<g.n_s, nt, 2 * 8 * g.n_loc, c->stream>>>(A);
+  LAUNCH_CHECK(c);
+  k_transport<<<g.n_s, nt, 8 * g.n_loc, c->stream>>>(A);
+  LAUNCH_CHECK(c);
+  c->cur ^= 1;
+  return LRBMS_OK;
+}
+
+static lrbms_status finish(lrbms_ctx* c, int nsteps_iters_known) {
+  (void)nsteps_iters_known;
+  int hf[4];
+  int it[2];
+  double sc[3];
+  CUDA_TRY(c, cudaMemcpyAsync(hf, c->at<int>(c->flags), 16, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(it, c->at<int>(c->iters), 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(sc, c->at<double>(c->scal), 24, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->last_iters = it[0];
+  c->total_iters = it[1];
+  if (hf[0]) {
+    std::string m;
+    if (hf[0] & FLAG_PIVOT) m += "non-positive pivot (B not SPD: rank-deficient Phi_E or lambda <= 0); ";
+    if (hf[0] & FLAG_NOCONV) m += "reduced PCG did not converge within max_iters; ";
+    if (hf[0] & FLAG_NOFLOW) m += "no flow (max Q = 0): CFL step undefined; ";
+    if (hf[0] & FLAG_NAN) m += "NaN/Inf detected; ";
+    if (hf[0] & FLAG_BREAKDOWN) m += "PCG breakdown (p.Bp <= 0); ";
+    CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->flags), 0, 16, c->stream));
+    return fail(c, LRBMS_E_NUMERICAL, "%s", m.c_str());
+  }
+  return LRBMS_OK;
+}
+
+extern "C" {
+
+lrbms_status lrbms_run(lrbms_ctx* c, int32_t n_steps, double cfl, double dt_fixed, double* dt_log) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  if (n_steps < 0) return fail(c, LRBMS_E_CONFIG, "n_steps < 0");
+  if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
+  for (int k = 0; k < n_steps; ++k) {
+    if ((st = launch_project(c))) return st;
+    if ((st = launch_solve(c))) return st;
+    if ((st = launch_recon(c))) return st;
+    if ((st = launch_transport(c, cfl, dt_fixed, dt_log, k, nullptr, nullptr))) return st;
+    c->steps++;
+  }
+  st = finish(c, n_steps);
+  return st;
+}
+
+lrbms_status lrbms_run_host(lrbms_ctx* c, int32_t n_steps, double cfl, double dt_fixed, const double* s_in,
+                            double* s_out, double* p_out) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  const Geo& g = c->g;
+  double* tmp = c->at<double>(c->tmp);
+  const int nb = cdiv(g.n, 256);
+  if (s_in) {
+    CUDA_TRY(c, cudaMemcpyAsync(tmp, s_in, 8 * (size_t)g.n, cudaMemcpyHostToDevice, c->stream));
+    k_to_internal<<<nb, 256, 0, c->stream>>>(g, tmp, c->s_cur());
+    LAUNCH_CHECK(c);
+  }
+  st = lrbms_run(c, n_steps, cfl, dt_fixed, nullptr);
+  if (st) return st;
+  if (s_out) {
+    k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->s_cur(), tmp);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaMemcpyAsync(s_out, tmp, 8 * (size_t)g.n, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (p_out) {
+    k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->at<double>(c->p), tmp);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaMemcpyAsync(p_out, tmp, 8 * (size_t)g.n, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_get_state(lrbms_ctx* c, double* s, double* p, double* cc) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  const Geo& g = c->g;
+  const int nb = cdiv(g.n, 256);
+  if (s) { k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->s_cur(), s); LAUNCH_CHECK(c); }
+  if (p) { k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->at<double>(c->p), p); LAUNCH_CHECK(c); }
+  if (cc) CUDA_TRY(c, cudaMemcpyAsync(cc, c->at<double>(c->c), c->c.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_stage_project(lrbms_ctx* c, double* blocks, double* r) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  if ((st = launch_project(c))) return st;
+  if (blocks) CUDA_TRY(c, cudaMemcpyAsync(blocks, c->at<double>(c->blocks), c->blocks.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  if (r) CUDA_TRY(c, cudaMemcpyAsync(r, c->at<double>(c->rhs), c->rhs.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_stage_solve(lrbms_ctx* c, double* cc) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  if (!c->have_blocks) return fail(c, LRBMS_E_STATE, "stage_solve needs a preceding stage_project");
+  if ((st = launch_solve(c))) return st;
+  if (cc) CUDA_TRY(c, cudaMemcpyAsync(cc, c->at<double>(c->c), c->c.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  return finish(c, 1);
+}
+
+lrbms_status lrbms_stage_reconstruct(lrbms_ctx* c, double* p) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  if ((st = launch_recon(c))) return st;
+  if (p) {
+    k_to_natural<<<cdiv(c->g.n, 256), 256, 0, c->stream>>>(c->g, c->at<double>(c->p), p);
+    LAUNCH_CHECK(c);
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_stage_transport(lrbms_ctx* c, double cfl, double dt_fixed, double* face_flux, double* link_flux,
+                                   double* dt) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
+  // dt reset normally happens in the reconstruction; do it here for a standalone call
+  const unsigned long long inf = 0x7ff0000000000000ull;
+  CUDA_TRY(c, cudaMemcpyAsync(c->at<double>(c->scal), &inf, 8, cudaMemcpyHostToDevice, c->stream));
+  if ((st = launch_transport(c, cfl, dt_fixed, nullptr, 0, face_flux, link_flux))) return st;
+  if (dt) CUDA_TRY(c, cudaMemcpyAsync(dt, c->at<double>(c->scal) + 2, 8, cudaMemcpyDeviceToDevice, c->stream));
+  c->steps++;
+  return finish(c, 0);
+}
+
+lrbms_status lrbms_get_stats(lrbms_ctx* c, lrbms_stats* o) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!o) return fail(c, LRBMS_E_CONFIG, "NULL stats");
+  double sc[3];
+  int it[2];
+  CUDA_TRY(c, cudaMemcpyAsync(sc, c->at<double>(c->scal), 24, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(it, c->at<int>(c->iters), 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  o->steps = c->steps;
+  o->t = sc[1];
+  o->last_dt = sc[2];
+  o->last_iters = it[0];
+  o->total_iters = it[1];
+  o->coarse_rebuilds = c->rebuilds;
+  o->fprime_max = c->fpmax;
+  return LRBMS_OK;
+}
+
+int64_t lrbms_launch_count(const lrbms_ctx* c) { return c ? c->launches : 0; }
+const char* lrbms_last_error(const lrbms_ctx* c) { return c ? c->err.c_str() : "null context"; }
+void lrbms_destroy(lrbms_ctx* c) { delete c; }
+
+}  // extern "C"

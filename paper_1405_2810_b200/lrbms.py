@@ -1,0 +1,277 @@
+"""Thin ctypes binding of liblrbms.so (include/lrbms.h): argument marshalling only.
+
+Every step of the LRBMS online path runs in the library's sm_100a kernels.  PyTorch is
+used for device memory (the workspace and the user's tensors) and the CUDA stream.
+There is no CPU fallback: if the library or a CUDA device is missing, this raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblrbms.so")
+
+LRBMS_OK, LRBMS_E_CONFIG, LRBMS_E_NUMERICAL, LRBMS_E_IO, LRBMS_E_CUDA, LRBMS_E_STATE = 0, 2, 3, 4, 5, 6
+STATUS_NAMES = {0: "OK", 2: "CONFIG", 3: "NUMERICAL", 4: "IO", 5: "CUDA", 6: "STATE"}
+
+# Every symbol include/lrbms.h declares (checked by tests/test_abi.py)
+EXPORTS = ["lrbms_create", "lrbms_workspace_bytes", "lrbms_bind", "lrbms_set_medium", "lrbms_set_basis",
+           "lrbms_set_saturation", "lrbms_set_solver", "lrbms_run", "lrbms_run_host", "lrbms_get_state",
+           "lrbms_stage_project", "lrbms_stage_solve", "lrbms_stage_reconstruct", "lrbms_stage_transport",
+           "lrbms_get_stats", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy"]
+
+
+class LrbmsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"lrbms {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int32), ("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("hx", ctypes.c_double), ("hy", ctypes.c_double), ("hz", ctypes.c_double),
+                ("sx", ctypes.c_int32), ("sy", ctypes.c_int32), ("sz", ctypes.c_int32), ("N", ctypes.c_int32)]
+
+
+class Fluid(ctypes.Structure):
+    _fields_ = [("mu_w", ctypes.c_double), ("mu_o", ctypes.c_double), ("swr", ctypes.c_double),
+                ("sor", ctypes.c_double), ("nw", ctypes.c_double), ("no", ctypes.c_double)]
+
+
+class Links(ctypes.Structure):
+    _fields_ = [("n_links", ctypes.c_int32), ("cell", ctypes.POINTER(ctypes.c_int32)),
+                ("axis", ctypes.POINTER(ctypes.c_int32)), ("p", ctypes.POINTER(ctypes.c_double)),
+                ("s_ext", ctypes.POINTER(ctypes.c_double))]
+
+
+class SolverOpts(ctypes.Structure):
+    _fields_ = [("rtol", ctypes.c_double), ("max_iters", ctypes.c_int32), ("coarse_refresh", ctypes.c_int32),
+                ("use_coarse", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int64), ("t", ctypes.c_double), ("last_dt", ctypes.c_double),
+                ("last_iters", ctypes.c_int32), ("total_iters", ctypes.c_int64),
+                ("coarse_rebuilds", ctypes.c_int32), ("fprime_max", ctypes.c_double)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load liblrbms.so (fails loudly; build it with paper_1405_2810_b200/build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"liblrbms.so not found at {path}: run `python -m paper_1405_2810_b200.build` "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    D = ctypes.c_double
+    I = ctypes.c_int32
+    st = ctypes.c_int
+    sig = {
+        "lrbms_create": (st, [ctypes.POINTER(Grid), ctypes.POINTER(Fluid), ctypes.POINTER(Links), ctypes.POINTER(P)]),
+        "lrbms_workspace_bytes": (ctypes.c_size_t, [P]),
+        "lrbms_bind": (st, [P, P, ctypes.c_size_t, P]),
+        "lrbms_set_medium": (st, [P, P, P]),
+        "lrbms_set_basis": (st, [P, P]),
+        "lrbms_set_saturation": (st, [P, P]),
+        "lrbms_set_solver": (st, [P, ctypes.POINTER(SolverOpts)]),
+        "lrbms_run": (st, [P, I, D, D, P]),
+        "lrbms_run_host": (st, [P, I, D, D, P, P, P]),
+        "lrbms_get_state": (st, [P, P, P, P]),
+        "lrbms_stage_project": (st, [P, P, P]),
+        "lrbms_stage_solve": (st, [P, P]),
+        "lrbms_stage_reconstruct": (st, [P, P]),
+        "lrbms_stage_transport": (st, [P, D, D, P, P, P]),
+        "lrbms_get_stats": (st, [P, ctypes.POINTER(Stats)]),
+        "lrbms_launch_count": (ctypes.c_int64, [P]),
+        "lrbms_last_error": (ctypes.c_char_p, [P]),
+        "lrbms_version": (ctypes.c_char_p, []),
+        "lrbms_destroy": (None, [P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class LrbmsContext:
+    """One LRBMS online problem on one GPU (wraps lrbms_ctx).
+
+    ``sc`` is a scenario with the fields of paper_1405_2810_b200.inputs.Scenario: grid and
+    partition sizes, fluid constants, links (cell, axis, p, s_ext), K, phi, Phi, s0.
+    """
+
+    def __init__(self, sc, device="cuda", stream=None, solver: Optional[dict] = None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("LrbmsContext needs a CUDA device (no CPU fallback)")
+        self.torch = torch
+        self.L = load_library()
+        self.sc = sc
+        self.device = torch.device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        g = Grid(sc.dim, sc.nx, sc.ny, sc.nz, sc.hx, sc.hy, sc.hz, sc.sx, sc.sy, sc.sz, sc.N)
+        f = Fluid(sc.mu_w, sc.mu_o, sc.swr, sc.sor, sc.nw, sc.no)
+        self._lk = [np.ascontiguousarray(sc.link_cell, np.int32), np.ascontiguousarray(sc.link_axis, np.int32),
+                    np.ascontiguousarray(sc.link_p, np.float64), np.ascontiguousarray(sc.link_s, np.float64)]
+        lk = Links(len(self._lk[0]),
+                   self._lk[0].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                   self._lk[1].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                   self._lk[2].ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                   self._lk[3].ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        h = ctypes.c_void_p()
+        status = self.L.lrbms_create(ctypes.byref(g), ctypes.byref(f), ctypes.byref(lk), ctypes.byref(h))
+        self.h = h
+        if status != LRBMS_OK:
+            msg = self.L.lrbms_last_error(h).decode() if h else "create failed"
+            if h:
+                self.L.lrbms_destroy(h)
+                self.h = None
+            raise LrbmsError(status, msg)
+        nbytes = self.L.lrbms_workspace_bytes(h)
+        with torch.cuda.device(self.device):
+            self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        self._ws_ptr = (base + 255) // 256 * 256
+        self._check(self.L.lrbms_bind(h, ctypes.c_void_p(self._ws_ptr), nbytes,
+                                      ctypes.c_void_p(self.stream.cuda_stream)))
+        if solver:
+            self.set_solver(**solver)
+        self.set_medium(sc.K, sc.phi)
+        self.set_basis(sc.Phi)
+        self.set_saturation(sc.s0)
+
+    # -- helpers -----------------------------------------------------------------------------
+    def _check(self, status):
+        if status != LRBMS_OK:
+            raise LrbmsError(status, self.L.lrbms_last_error(self.h).decode())
+
+    def dev(self, a, dtype=None):
+        torch = self.torch
+        dtype = dtype or torch.float64
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.device, dtype=dtype).contiguous()
+        return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=self.device)
+
+    def empty(self, *shape):
+        return self.torch.empty(*shape, dtype=self.torch.float64, device=self.device)
+
+    # -- API ---------------------------------------------------------------------------------
+    def set_medium(self, K, phi=None):
+        self._K = self.dev(K)
+        self._phi = None if phi is None else self.dev(phi)
+        self._check(self.L.lrbms_set_medium(self.h, _ptr(self._K), _ptr(self._phi)))
+
+    def set_basis(self, Phi):
+        self._Phi = self.dev(Phi)
+        self._check(self.L.lrbms_set_basis(self.h, _ptr(self._Phi)))
+        self.stream.synchronize()
+        self._Phi = None
+
+    def set_saturation(self, s):
+        t = self.dev(s)
+        self._check(self.L.lrbms_set_saturation(self.h, _ptr(t)))
+        self.stream.synchronize()
+
+    def set_solver(self, rtol=1e-14, max_iters=5000, coarse_refresh=10, use_coarse=1):
+        o = SolverOpts(rtol, max_iters, coarse_refresh, use_coarse)
+        self._check(self.L.lrbms_set_solver(self.h, ctypes.byref(o)))
+
+    def run(self, n_steps, cfl=None, dt_fixed=0.0, log_dt=False):
+        cfl = self.sc.cfl if cfl is None else cfl
+        dt_log = self.empty(max(n_steps, 1)) if log_dt else None
+        self._check(self.L.lrbms_run(self.h, int(n_steps), float(cfl), float(dt_fixed), _ptr(dt_log)))
+        return dt_log[:n_steps] if log_dt else None
+
+    def run_host(self, n_steps, s_in=None, cfl=None, dt_fixed=0.0, want_s=True, want_p=False):
+        """End-to-end from host buffers (the e2e path): returns numpy (s, p)."""
+        cfl = self.sc.cfl if cfl is None else cfl
+        n = self.sc.n
+        s_out = np.empty(n) if want_s else None
+        p_out = np.empty(n) if want_p else None
+        sp = None
+        if s_in is not None:
+            s_in = np.ascontiguousarray(s_in, np.float64)
+            sp = s_in.ctypes.data_as(ctypes.c_void_p)
+        self._check(self.L.lrbms_run_host(self.h, int(n_steps), float(cfl), float(dt_fixed), sp,
+                                          None if s_out is None else s_out.ctypes.data_as(ctypes.c_void_p),
+                                          None if p_out is None else p_out.ctypes.data_as(ctypes.c_void_p)))
+        return s_out, p_out
+
+    def run_host_ptr(self, n_steps, s_in_ptr, s_out_ptr, p_out_ptr=None, cfl=None, dt_fixed=0.0):
+        """e2e with caller-owned (e.g. pinned) host buffers given as integer addresses."""
+        cfl = self.sc.cfl if cfl is None else cfl
+        c = lambda v: None if v is None else ctypes.c_void_p(v)
+        self._check(self.L.lrbms_run_host(self.h, int(n_steps), float(cfl), float(dt_fixed), c(s_in_ptr),
+                                          c(s_out_ptr), c(p_out_ptr)))
+
+    def get_state(self):
+        sc = self.sc
+        s, p, c = self.empty(sc.n), self.empty(sc.n), self.empty(sc.n_s * sc.N)
+        self._check(self.L.lrbms_get_state(self.h, _ptr(s), _ptr(p), _ptr(c)))
+        return s, p, c.view(sc.n_s, sc.N)
+
+    def stage_project(self):
+        sc = self.sc
+        blocks = self.empty(sc.n_s, 1 + sc.dim, sc.N, sc.N)
+        r = self.empty(sc.n_s, sc.N)
+        self._check(self.L.lrbms_stage_project(self.h, _ptr(blocks), _ptr(r)))
+        return blocks, r
+
+    def stage_solve(self):
+        c = self.empty(self.sc.n_s, self.sc.N)
+        self._check(self.L.lrbms_stage_solve(self.h, _ptr(c)))
+        return c
+
+    def stage_reconstruct(self):
+        p = self.empty(self.sc.n)
+        self._check(self.L.lrbms_stage_reconstruct(self.h, _ptr(p)))
+        return p
+
+    def n_interior_faces(self):
+        sc = self.sc
+        return (sc.nx - 1) * sc.ny * sc.nz + sc.nx * (sc.ny - 1) * sc.nz + sc.nx * sc.ny * (sc.nz - 1)
+
+    def stage_transport(self, cfl=None, dt_fixed=0.0):
+        cfl = self.sc.cfl if cfl is None else cfl
+        ff = self.empty(max(self.n_interior_faces(), 1))
+        lf = self.empty(max(self.sc.n_links, 1))
+        dt = self.empty(1)
+        self._check(self.L.lrbms_stage_transport(self.h, float(cfl), float(dt_fixed), _ptr(ff), _ptr(lf), _ptr(dt)))
+        return ff[:self.n_interior_faces()], lf[:self.sc.n_links], dt
+
+    def stats(self) -> dict:
+        st = Stats()
+        self._check(self.L.lrbms_get_stats(self.h, ctypes.byref(st)))
+        return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+    def launch_count(self) -> int:
+        return int(self.L.lrbms_launch_count(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.lrbms_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

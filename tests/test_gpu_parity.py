@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star):
+  reduced coefficients c and pressures p: ||d||_inf / ||ref||_inf <= 1e-10;
+  saturations after the full run: ||d||_inf <= 1e-10 (absolute).
+Stage-level checks are tighter (same arithmetic, different summation order).
+"""
+import numpy as np
+import pytest
+
+from paper_1405_2810_b200 import inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+O = pytest.importorskip("oracle.lrbms_oracle")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1405_2810_b200 import build
+    build.build()
+
+
+def ctx_for(sc, **solver):
+    from paper_1405_2810_b200.lrbms import LrbmsContext
+    return LrbmsContext(sc, solver=solver or None)
+
+
+def rel(a, b):
+    a = np.asarray(a); b = np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+SMALL = [
+    ("C1", lambda: inputs.make_scenario("C1")),
+    ("ragged2d", lambda: inputs.custom_scenario(15, 12, 1, 5, 4, 1, 7, seed=21, mu_o=5.0)),
+    ("ragged3d", lambda: inputs.custom_scenario(9, 6, 4, 3, 3, 2, 11, seed=22, mu_o=10.0, bc="corner_columns_3d",
+                                                hx=0.5, hy=1.5, hz=2.0)),
+    ("one_subdomain", lambda: inputs.custom_scenario(8, 8, 1, 8, 8, 1, 6, seed=23, mu_o=3.0)),
+    ("linear_kr", lambda: inputs.custom_scenario(16, 8, 1, 4, 4, 1, 3, seed=24, nw=1.0, no=1.0, mu_o=4.0)),
+    ("corey3", lambda: inputs.custom_scenario(12, 12, 1, 4, 4, 1, 5, seed=25, nw=3.0, no=1.5, mu_o=2.0,
+                                              swr=0.1, sor=0.05)),
+]
+
+
+@pytest.mark.parametrize("name,make", SMALL, ids=[s[0] for s in SMALL])
+def test_stage_parity_small(name, make):
+    sc = make()
+    rng = np.random.default_rng(3)
+    s = rng.uniform(-0.05, 1.05, sc.n)        # includes values outside [0,1] (clamped mobility)
+    sc.s0 = s
+    ctx = ctx_for(sc)
+    blocks, r = ctx.stage_project()
+    lam = O.total_mobility(s, sc)
+    A, b = O.fine_operator(sc, lam)
+    ob, orr = O.project(sc, A, b)
+    assert rel(np_(blocks), ob) <= 1e-13
+    assert rel(np_(r), orr) <= 1e-13
+    c = ctx.stage_solve()
+    oc = O.solve_reduced(sc, ob, orr, method="dense")
+    assert rel(np_(c), oc) <= 1e-11
+    p = ctx.stage_reconstruct()
+    op = O.reconstruct(sc, oc)
+    assert rel(np_(p), op) <= 1e-11
+    ff, lf, dt = ctx.stage_transport()
+    oFf, oFl = O.fluxes(sc, op, lam)
+    assert rel(np_(ff), oFf) <= 1e-10
+    assert rel(np_(lf), oFl) <= 1e-10
+    odt = O.cfl_time_step(sc, oFf, oFl, O.fprime_max(sc))
+    assert abs(float(dt[0]) - odt) <= 1e-11 * odt
+    s1, _, _ = ctx.get_state()
+    os1 = O.transport(sc, s, oFf, oFl, odt)
+    assert np.max(np.abs(np_(s1) - os1)) <= 1e-12
+    ctx.close()
+
+
+@pytest.mark.parametrize("name,make", SMALL, ids=[s[0] for s in SMALL])
+def test_full_run_small(name, make):
+    sc = make()
+    n = 20
+    ref = O.run(sc, n_steps=n, keep=True)
+    ctx = ctx_for(sc)
+    dts = np_(ctx.run(n, log_dt=True))
+    s, p, c = ctx.get_state()
+    assert rel(dts, ref["dts"]) <= 1e-10
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
+    st = ctx.stats()
+    assert st["steps"] == n and st["total_iters"] > 0
+    ctx.close()
+
+
+def test_full_basis_reproduces_fine_scheme_gpu():
+    """P1 on the GPU: Phi_E = full orthogonal local space => the fine k = 0 scheme."""
+    sc = inputs.custom_scenario(16, 16, 1, 4, 4, 1, 16, seed=5, mu_o=5.0, basis="full")
+    fp = O.fprime_max(sc)
+    s = sc.s0.copy()
+    for _ in range(10):
+        s = O.fine_step(sc, s, fpmax=fp)["s"]
+    ctx = ctx_for(sc)
+    ctx.run(10)
+    sg, _, _ = ctx.get_state()
+    assert np.max(np.abs(np_(sg) - s)) <= 1e-10
+
+
+def test_dt_fixed_and_porosity():
+    sc = inputs.custom_scenario(12, 8, 1, 4, 4, 1, 5, seed=7, mu_o=5.0)
+    sc.phi = np.random.default_rng(1).uniform(0.1, 0.3, sc.n)
+    ref = O.run(sc, n_steps=6, dt_fixed=0.05)
+    ctx = ctx_for(sc)
+    ctx.run(6, dt_fixed=0.05)
+    s, _, _ = ctx.get_state()
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-11
+    sc2 = inputs.custom_scenario(12, 8, 1, 4, 4, 1, 5, seed=7, mu_o=5.0)
+    sc2.phi = sc.phi
+    ref2 = O.run(sc2, n_steps=6)
+    ctx2 = ctx_for(sc2)
+    ctx2.run(6)
+    s2, _, _ = ctx2.get_state()
+    assert np.max(np.abs(np_(s2) - ref2["s"])) <= 1e-11
+
+
+def test_run_host_matches_device_path():
+    sc = inputs.make_scenario("C1")
+    ctx = ctx_for(sc)
+    s_h, p_h = ctx.run_host(5, s_in=sc.s0, want_p=True)
+    ctx2 = ctx_for(sc)
+    ctx2.run(5)
+    s_d, p_d, _ = ctx2.get_state()
+    assert np.array_equal(s_h, np_(s_d)) and np.array_equal(p_h, np_(p_d))
+
+
+def test_determinism_bitwise():
+    sc = inputs.make_scenario("C2", n_steps=10)
+    outs = []
+    for _ in range(2):
+        ctx = ctx_for(sc)
+        ctx.run(10)
+        s, p, c = ctx.get_state()
+        outs.append((np_(s), np_(p), np_(c)))
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
+def test_metamorphic_viscosity_scaling_bitwise():
+    """P7: mu x 4 => the same s and p, dt x 4 (powers of two scale exactly)."""
+    sc = inputs.make_scenario("C1", n_steps=8)
+    ctx = ctx_for(sc)
+    d1 = np_(ctx.run(8, log_dt=True))
+    s1, p1, _ = ctx.get_state()
+    sc.mu_w *= 4; sc.mu_o *= 4
+    ctx2 = ctx_for(sc)
+    d2 = np_(ctx2.run(8, log_dt=True))
+    s2, p2, _ = ctx2.get_state()
+    assert np.allclose(d2, 4 * d1, rtol=1e-14, atol=0)
+    assert np.max(np.abs(np_(s1) - np_(s2))) <= 1e-14
+    assert np.max(np.abs(np_(p1) - np_(p2))) <= 1e-14
+
+
+def test_config_errors():
+    from paper_1405_2810_b200.lrbms import LrbmsError, LRBMS_E_CONFIG
+    sc = inputs.custom_scenario(8, 8, 1, 4, 4, 1, 4)
+    sc.N = 40
+    with pytest.raises(LrbmsError) as e:
+        ctx_for(sc)
+    assert e.value.status == LRBMS_E_CONFIG
+    sc = inputs.custom_scenario(8, 8, 1, 4, 4, 1, 4)
+    sc.sx = 3
+    with pytest.raises(LrbmsError):
+        ctx_for(sc)
+    sc = inputs.custom_scenario(8, 8, 1, 4, 4, 1, 4)
+    sc.link_cell = sc.link_cell[:0]; sc.link_axis = sc.link_axis[:0]
+    sc.link_p = sc.link_p[:0]; sc.link_s = sc.link_s[:0]
+    with pytest.raises(LrbmsError):
+        ctx_for(sc)
+    sc = inputs.custom_scenario(8, 8, 1, 4, 4, 1, 4)
+    sc.K = sc.K.copy(); sc.K[3] = -1.0
+    with pytest.raises(LrbmsError):
+        ctx_for(sc)
+
+
+def test_rank_deficient_basis_is_numerical_error():
+    from paper_1405_2810_b200.lrbms import LrbmsError, LRBMS_E_NUMERICAL
+    sc = inputs.custom_scenario(8, 8, 1, 4, 4, 1, 4)
+    sc.Phi = sc.Phi.copy()
+    sc.Phi[1, 3] = sc.Phi[1, 2]
+    ctx = ctx_for(sc)
+    with pytest.raises(LrbmsError) as e:
+        ctx.run(1)
+    assert e.value.status == LRBMS_E_NUMERICAL
+
+
+@pytest.mark.parametrize("name,steps", [("C2", 100), ("C3", 500)])
+def test_full_run_configs(name, steps):
+    sc = inputs.make_scenario(name)
+    ref = O.run(sc, n_steps=steps, keep=True)
+    ctx = ctx_for(sc)
+    dts = np_(ctx.run(steps, log_dt=True))
+    s, p, c = ctx.get_state()
+    assert rel(dts, ref["dts"]) <= 1e-10
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_size_prefix(name):
+    """Full BASELINE sizes in the bench launch configuration: stage parity on s^0 and on a
+    random saturation, then a 2-step run against the oracle."""
+    sc = inputs.make_scenario(name)
+    rng = np.random.default_rng(9)
+    s = rng.uniform(0.0, 1.0, sc.n)
+    sc.s0 = s
+    ctx = ctx_for(sc)
+    blocks, r = ctx.stage_project()
+    lam = O.total_mobility(s, sc)
+    A, b = O.fine_operator(sc, lam)
+    ob, orr = O.project(sc, A, b)
+    assert rel(np_(blocks), ob) <= 1e-13
+    assert rel(np_(r), orr) <= 1e-13
+    c = ctx.stage_solve()
+    oc = O.solve_reduced(sc, ob, orr)
+    assert rel(np_(c), oc) <= 1e-10
+    ctx.close()
+    sc = inputs.make_scenario(name)
+    ref = O.run(sc, n_steps=2, keep=True)
+    ctx = ctx_for(sc)
+    ctx.run(2)
+    sg, pg, cg = ctx.get_state()
+    assert rel(np_(cg), ref["cs"][-1]) <= 1e-10
+    assert rel(np_(pg), ref["ps"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(sg) - ref["s"])) <= 1e-10
