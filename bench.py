@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- LRBMS online time steps/s on one B200 (fp64), with roofline and CPU-oracle baselines.
+
+Contract:
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5]
+A "step" is one pass of the whole hot path a1..a6 (mobility, assembly + projection, reduced solve,
+reconstruction, fluxes + CFL step, upwind transport) over the workload BASELINE.json's metric is
+quoted on at full size: C5 (128x128x64 cells, 2048 subdomains of 8x8x8, N = 32).
+Multi-GPU: replicas only (BASELINE.json mandates one GPU, no collectives): every rank
+runs its own C5 replica; value = total steps of all ranks / max-over-ranks device time.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LRBMS online time steps/sec (1 B200, fp64) and achieved HBM GB/s vs roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--basis", default="poly")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--coarse-refresh", type=int, default=None)
+    ap.add_argument("--rtol", type=float, default=None)
+    return ap.parse_args()
+
+
+def dist_setup(use_cuda):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if use_cuda else "gloo")
+    return rank, local, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, device):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region (B200_PROFILING.md)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1])); smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def stage_bytes(sc, iters_per_launch):
+    """Algorithmic DRAM bytes per launch of each stage."""
+    n, ns, N, nl, dim = sc.n, sc.n_s, sc.N, sc.n_loc, sc.dim
+    R = ns * N
+    phi = 8.0 * ns * N * nl
+    iface = 8.0 * ns * N * sum(nl // s for s in (sc.sx, sc.sy, sc.sz)[:dim])  # neighbour interface rows
+    blocks = 8.0 * ns * (1 + dim) * N * N
+    n_pad = -(-ns // 32) * 32
+    per_iter = blocks + 8.0 * ns * N * N + 8.0 * n_pad * n_pad + 8.0 * 8 * R
+    return {
+        "project": phi + iface + 16.0 * n + blocks + 8.0 * R,
+        "block_inverse": 8.0 * ns * N * N * 2,
+        "pcg": (iters_per_launch + 1) * per_iter,
+        "recon": phi + 8.0 * n + 8.0 * R,
+        "flux_cfl": 24.0 * n,
+        "transport": 32.0 * n,
+        "coarse": 8.0 * n_pad * n_pad * 4,
+    }
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(cfg, basis, n_steps):
+    """Time the CPU oracle (as it stands) on n_steps of the same workload from s0."""
+    from oracle import lrbms_oracle as O
+    from paper_1405_2810_b200 import inputs
+    sc = inputs.make_scenario(cfg, basis=basis)
+    fp = O.fprime_max(sc)
+    s = sc.s0.copy()
+    c_prev = None
+    times = []
+    for _ in range(n_steps):
+        t0 = time.perf_counter()
+        out = O.lrbms_step(sc, s, fpmax=fp, x0=c_prev)
+        times.append(time.perf_counter() - t0)
+        s, c_prev = out["s"], out["c"]
+    return times
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    K = max(1, min(args.steps, 3))
+    W = min(args.warmup, 0)
+    times = oracle_sample(args.config, args.basis, K + W)[W:]
+    tot = sum(times)
+    value = K / tot
+    cores = cpu_threads()
+    sample = (f"{K} full oracle online steps of {args.config} from s0 (of --steps {args.steps}; capped so the "
+              "run ends within minutes); NumPy/SciPy fp64 oracle/lrbms_oracle.py as it stands")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": 1e3 * tot / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "basis": args.basis},
+            "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, local, world):
+    import torch
+    from paper_1405_2810_b200 import inputs
+    from paper_1405_2810_b200.lrbms import LrbmsContext
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl ours needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    sc = inputs.make_scenario(args.config, basis=args.basis)
+    solver = {}
+    if args.coarse_refresh:
+        solver["coarse_refresh"] = args.coarse_refresh
+    if args.rtol:
+        solver["rtol"] = args.rtol
+    ctx = LrbmsContext(sc, device=device, solver=solver or None)
+    stream = ctx.stream
+    K, W = args.steps, args.warmup
+
+    # ---- warm-up (untimed), then the timed region on device, inputs resident in HBM
+    ctx.run(W)
+    st0 = ctx.stats()
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launch_count()
+    ctx.set_profiling(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.run(K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    stages = ctx.stage_times()
+    ctx.set_profiling(False)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    st1 = ctx.stats()
+    barrier(world)
+    ms_max = max_over_ranks(ms, world, device)
+    value = world * K / (ms_max / 1e3)
+    iters = (st1["total_iters"] - st0["total_iters"]) / K
+
+    # ---- e2e: the same metric through the C ABI with HOST buffers (pinned), copies inside
+    Ke = args.e2e_steps or max(1, min(K, 50))
+    s_pin = torch.empty(sc.n, dtype=torch.float64, pin_memory=True)
+    p_pin = torch.empty(sc.n, dtype=torch.float64, pin_memory=True)
+    s_dev, _, _ = ctx.get_state()
+    s_pin.copy_(s_dev.cpu())
+    barrier(world)
+    torch.cuda.synchronize()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    t_wall0 = time.perf_counter()
+    for _ in range(Ke):
+        ctx.run_host_ptr(1, s_pin.data_ptr(), s_pin.data_ptr(), p_pin.data_ptr())
+    e3.record(stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    ms_e2e = max(e2.elapsed_time(e3), 1e3 * t_wall)
+    ms_e2e = max_over_ranks(ms_e2e, world, device)
+    e2e_value = world * Ke / (ms_e2e / 1e3)
+
+    if rank != 0:
+        return 0
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / CUDA-event launch time)
+    peak, peak_src = measured_peaks()
+    dom = max((k for k in stages if stages[k][1] > 0), key=lambda k: stages[k][0])
+    dom_ms, dom_launches = stages[dom]
+    per_launch_ms = dom_ms / max(dom_launches, 1)
+    sb = stage_bytes(sc, iters)
+    algo = sb.get(dom, 0.0)
+    achieved = algo / (per_launch_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+    # whole-step compulsory-bytes view: every stage's algorithmic bytes once
+    step_bytes = sum(sb[k] * stages[k][1] / K for k in sb if k in stages)
+    step_ms = ms / K
+    stage_share = {k: round(v[0] / max(ms, 1e-9), 4) for k, v in stages.items()}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        ts = oracle_sample(args.config, args.basis, 1)
+        cpu = {"value": 1.0 / sum(ts), "unit": "steps/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"1 oracle online step of {args.config} from s0 ({sum(ts):.1f} s), "
+                         "NumPy/SciPy fp64 oracle as it stands"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded C5 recipe of DESIGN.md; no dataset)",
+        "config": {"workload": args.config, "grid": f"{sc.nx}x{sc.ny}x{sc.nz}",
+                   "subdomains": f"{sc.Sx}x{sc.Sy}x{sc.Sz} of {sc.sx}x{sc.sy}x{sc.sz}", "N": sc.N,
+                   "cells": sc.n, "reduced_dofs": sc.n_s * sc.N, "basis": args.basis,
+                   "l2": "inputs larger than L2 (Phi = %.0f MB > 126 MB L2), no flush" % (8e-6 * sc.n_s * sc.N * sc.n_loc),
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "clocks": clk,
+        "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * sc.n,
+                "d2h_bytes_per_step": 16 * sc.n, "steps": Ke},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": algo, "avg_launch_ms": per_launch_ms},
+        "step_roofline": {"algorithmic_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (step_ms / 1e3) / 1e9,
+                          "frac": step_bytes / (step_ms / 1e3) / 1e9 / peak},
+        "stage_share": stage_share,
+        "pcg_iters_per_step": iters,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    use_cuda = args.impl == "ours"
+    rank, local, world = dist_setup(use_cuda)
+    try:
+        if args.impl == "reference":
+            return run_reference(args, rank, world)
+        return run_ours(args, rank, local, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

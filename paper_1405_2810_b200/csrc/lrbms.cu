@@ -813,6 +813,13 @@ struct lrbms_ctx {
   int last_iters = 0, rebuilds = 0;
   int64_t last_rebuild_step = -1;
   std::string err;
+  // stage profiling (CUDA events)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_pending;  // (stage, index of start event in pool)
+  size_t ev_used = 0;
+  double stage_ms[LRBMS_N_STAGES] = {0};
+  int64_t stage_launches[LRBMS_N_STAGES] = {0};
 
   template <class T>
   T* at(const Buf& b) const { return reinterpret_cast<T*>(ws + b.off); }
@@ -881,6 +888,44 @@ static lrbms_status check_ctx(lrbms_ctx* c, bool need_bound = true) {
 }
 
 static int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// stage profiling: record an event pair around each stage; resolved after the stream syncs
+static cudaEvent_t next_event(lrbms_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+struct StageScope {
+  lrbms_ctx* c;
+  int stage;
+  int64_t l0;
+  size_t idx;
+  StageScope(lrbms_ctx* c_, int st) : c(c_), stage(st), l0(c_->launches), idx(0) {
+    if (c->profiling) {
+      idx = c->ev_used;
+      cudaEventRecord(next_event(c), c->stream);
+    }
+  }
+  ~StageScope() {
+    c->stage_launches[stage] += c->launches - l0;
+    if (c->profiling) {
+      cudaEventRecord(next_event(c), c->stream);
+      c->ev_pending.push_back({stage, (int)idx});
+    }
+  }
+};
+static void resolve_events(lrbms_ctx* c) {
+  for (auto& pr : c->ev_pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev_pool[pr.second], c->ev_pool[pr.second + 1]) == cudaSuccess)
+      c->stage_ms[pr.first] += ms;
+  }
+  c->ev_pending.clear();
+  c->ev_used = 0;
+}
 
 extern "C" {
 
@@ -1145,6 +1190,7 @@ static lrbms_status ready(lrbms_ctx* c) {
 }
 
 static lrbms_status launch_project(lrbms_ctx* c) {
+  StageScope sc_(c, 0);
   ProjArgs A;
   A.g = c->g; A.f = c->f; A.L = links_of(c);
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
@@ -1157,6 +1203,7 @@ static lrbms_status launch_project(lrbms_ctx* c) {
 }
 
 static lrbms_status launch_coarse(lrbms_ctx* c) {
+  StageScope sc_(c, 1);
   const Geo& g = c->g;
   double* Bc = c->at<double>(c->Binv);
   CUDA_TRY(c, cudaMemsetAsync(Bc, 0, c->Binv.bytes, c->stream));
@@ -1179,9 +1226,13 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     lrbms_status st = launch_coarse(c);
     if (st) return st;
   }
-  k_block_inverse<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->DinvT),
-                                                          c->at<int>(c->flags));
-  LAUNCH_CHECK(c);
+  {
+    StageScope sc_(c, 2);
+    k_block_inverse<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->DinvT),
+                                                            c->at<int>(c->flags));
+    LAUNCH_CHECK(c);
+  }
+  StageScope sc_(c, 3);
   PcgArgs A;
   A.g = g;
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs); A.zc = c->at<double>(c->zc);
@@ -1200,6 +1251,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
 }
 
 static lrbms_status launch_recon(lrbms_ctx* c) {
+  StageScope sc_(c, 4);
   const Geo& g = c->g;
   const int nt = std::min(1024, cdiv(g.n_loc, 32) * 32);
   k_recon<<<g.n_s, nt, 0, c->stream>>>(g, c->at<double>(c->Phi), c->at<double>(c->c), c->at<double>(c->p),
@@ -1230,10 +1282,16 @@ static lrbms_status launch_transport(lrbms_ctx* c, double cfl, double dt_fixed, 
   FluxArgs A = flux_args(c, cfl, dt_fixed, dt_log, step);
   A.face_flux = face_flux;
   A.link_flux = link_flux;
-  k_flux_cfl<<<g.n_s, nt, 2 * 8 * g.n_loc, c->stream>>>(A);
-  LAUNCH_CHECK(c);
-  k_transport<<<g.n_s, nt, 8 * g.n_loc, c->stream>>>(A);
-  LAUNCH_CHECK(c);
+  {
+    StageScope sc_(c, 5);
+    k_flux_cfl<<<g.n_s, nt, 2 * 8 * g.n_loc, c->stream>>>(A);
+    LAUNCH_CHECK(c);
+  }
+  {
+    StageScope sc_(c, 6);
+    k_transport<<<g.n_s, nt, 8 * g.n_loc, c->stream>>>(A);
+    LAUNCH_CHECK(c);
+  }
   c->cur ^= 1;
   return LRBMS_OK;
 }
@@ -1247,6 +1305,7 @@ static lrbms_status finish(lrbms_ctx* c, int nsteps_iters_known) {
   CUDA_TRY(c, cudaMemcpyAsync(it, c->at<int>(c->iters), 8, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(sc, c->at<double>(c->scal), 24, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  resolve_events(c);
   c->last_iters = it[0];
   c->total_iters = it[1];
   if (hf[0]) {
@@ -1385,7 +1444,33 @@ lrbms_status lrbms_get_stats(lrbms_ctx* c, lrbms_stats* o) {
 }
 
 int64_t lrbms_launch_count(const lrbms_ctx* c) { return c ? c->launches : 0; }
+
+lrbms_status lrbms_set_profiling(lrbms_ctx* c, int32_t enable) {
+  lrbms_status st = check_ctx(c, false);
+  if (st) return st;
+  if (c->bound) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  resolve_events(c);
+  c->profiling = enable != 0;
+  for (int i = 0; i < LRBMS_N_STAGES; ++i) { c->stage_ms[i] = 0.0; c->stage_launches[i] = 0; }
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_get_stage_times(lrbms_ctx* c, double* ms, int64_t* launches, int32_t n) {
+  lrbms_status st = check_ctx(c, false);
+  if (st) return st;
+  if (c->bound) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  resolve_events(c);
+  for (int i = 0; i < n && i < LRBMS_N_STAGES; ++i) {
+    if (ms) ms[i] = c->stage_ms[i];
+    if (launches) launches[i] = c->stage_launches[i];
+  }
+  return LRBMS_OK;
+}
 const char* lrbms_last_error(const lrbms_ctx* c) { return c ? c->err.c_str() : "null context"; }
-void lrbms_destroy(lrbms_ctx* c) { delete c; }
+void lrbms_destroy(lrbms_ctx* c) {
+  if (!c) return;
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  delete c;
+}
 
 }  // extern "C"

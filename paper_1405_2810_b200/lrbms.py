@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "OK", 2: "CONFIG", 3: "NUMERICAL", 4: "IO", 5: "CUDA", 6: "ST
 EXPORTS = ["lrbms_create", "lrbms_workspace_bytes", "lrbms_bind", "lrbms_set_medium", "lrbms_set_basis",
            "lrbms_set_saturation", "lrbms_set_solver", "lrbms_run", "lrbms_run_host", "lrbms_get_state",
            "lrbms_stage_project", "lrbms_stage_solve", "lrbms_stage_reconstruct", "lrbms_stage_transport",
-           "lrbms_get_stats", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy"]
+           "lrbms_get_stats", "lrbms_set_profiling", "lrbms_get_stage_times", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy"]
 
 
 class LrbmsError(RuntimeError):
@@ -92,6 +92,8 @@ def load_library(path: str = LIB_PATH):
         "lrbms_stage_transport": (st, [P, D, D, P, P, P]),
         "lrbms_get_stats": (st, [P, ctypes.POINTER(Stats)]),
         "lrbms_launch_count": (ctypes.c_int64, [P]),
+        "lrbms_set_profiling": (st, [P, I]),
+        "lrbms_get_stage_times": (st, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), I]),
         "lrbms_last_error": (ctypes.c_char_p, [P]),
         "lrbms_version": (ctypes.c_char_p, []),
         "lrbms_destroy": (None, [P]),
@@ -261,6 +263,18 @@ class LrbmsContext:
         st = Stats()
         self._check(self.L.lrbms_get_stats(self.h, ctypes.byref(st)))
         return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+    STAGES = ["project", "coarse", "block_inverse", "pcg", "recon", "flux_cfl", "transport"]
+
+    def set_profiling(self, on: bool):
+        self._check(self.L.lrbms_set_profiling(self.h, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        n = len(self.STAGES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        self._check(self.L.lrbms_get_stage_times(self.h, ms, cnt, n))
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(self.STAGES)}
 
     def launch_count(self) -> int:
         return int(self.L.lrbms_launch_count(self.h))
