@@ -136,10 +136,11 @@ def stage_bytes(sc, iters_per_launch):
     iface = 8.0 * ns * N * sum(nl // s for s in (sc.sx, sc.sy, sc.sz)[:dim])  # neighbour interface rows
     blocks = 8.0 * ns * (1 + dim) * N * N
     n_pad = -(-ns // 32) * 32
-    per_iter = blocks + 8.0 * ns * N * N + 8.0 * n_pad * n_pad + 8.0 * 8 * R
+    # blocks (upper storage, each read once), fp32 block-Jacobi inverses and coarse inverse, vectors
+    per_iter = blocks + 4.0 * ns * N * N + 4.0 * n_pad * n_pad + 8.0 * 12 * R
     return {
         "project": phi + iface + 16.0 * n + blocks + 8.0 * R,
-        "block_inverse": 8.0 * ns * N * N * 2,
+        "block_inverse": 8.0 * ns * N * N + 4.0 * ns * N * N,
         "pcg": (iters_per_launch + 1) * per_iter,
         "recon": phi + 8.0 * n + 8.0 * R,
         "flux_cfl": 24.0 * n,

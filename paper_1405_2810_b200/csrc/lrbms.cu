@@ -23,6 +23,8 @@
 
 #include "../../include/lrbms.h"
 #include "lrbms_kernels.cuh"
+#include "lrbms_pcg.cuh"
+#include "lrbms_project.cuh"
 
 using namespace lrbms;
 
@@ -70,383 +72,6 @@ __global__ void k_basis_indicator(Geo g, const double* __restrict__ Phi, double*
     for (int l = lane; l < g.n_loc; l += 32) acc += row[l];
     acc = warp_sum(acc);
     if (lane == 0) zc[E * g.N + k] = acc;
-  }
-}
-
-// ---------------------------------------------------------------------------- a1 + a2
-// Shared memory (doubles): Phs[N][n_loc] | Ys[CH][n_loc] | diag[n_loc] | wp[3][n_loc] |
-//                          bl[n_loc] | wi[3][nfmax] | PhN[N][nfmax]
-struct ProjArgs {
-  Geo g;
-  Flu f;
-  Links L;
-  const double* s;
-  const double* K;
-  const double* Phi;
-  double* blocks;
-  double* rhs;
-  int CH;
-  int nfmax;
-};
-
-__global__ void __launch_bounds__(256) k_project(ProjArgs A) {
-  extern __shared__ double sm[];
-  const Geo& g = A.g;
-  const int N = g.N, nl = g.n_loc, E = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-  const int nb1 = 1 + g.dim;
-  double* Phs = sm;
-  double* Ys = Phs + (size_t)N * nl;
-  double* diag = Ys + (size_t)A.CH * nl;
-  double* wp = diag + nl;            // [3][nl]
-  double* bl = wp + 3 * nl;
-  double* wi = bl + nl;              // [3][nfmax]
-  double* PhN = wi + 3 * A.nfmax;    // [N][nfmax]
-  int C[3];
-  sub_xyz(g, E, C);
-
-  // stage Phi_E (contiguous N * n_loc doubles)
-  const double* PhiE = A.Phi + (size_t)E * N * nl;
-  for (int i = tid; i < N * nl; i += nt) Phs[i] = PhiE[i];
-
-  // a1 + face weights: diag_l = sum of w over all faces of l; w to +a neighbour inside E
-  const size_t base = (size_t)E * nl;
-  for (int l = tid; l < nl; l += nt) {
-    int c[3];
-    local_xyz(g, l, c);
-    const double Kl = A.K[base + l];
-    const double ll = total_mobility(A.f, A.s[base + l]);
-    double d = 0.0;
-    for (int a = 0; a < 3; ++a) wp[a * nl + l] = 0.0;
-    for (int a = 0; a < g.dim; ++a) {
-      for (int dir = -1; dir <= 1; dir += 2) {
-        int nb = neighbour(g, E, C, l, c, a, dir);
-        if (nb < 0) continue;
-        const double Kn = A.K[nb];
-        const double ln = total_mobility(A.f, A.s[nb]);
-        const double w = dir > 0 ? face_weight(g.geo[a], Kl, Kn, ll, ln)
-                                 : face_weight(g.geo[a], Kn, Kl, ln, ll);
-        d += w;
-        if (dir > 0) {
-          if (c[a] + 1 < g.s[a]) wp[a * nl + l] = w;
-          else wi[a * A.nfmax + face_pos(g, c, a)] = w;
-        }
-      }
-    }
-    diag[l] = d;
-    bl[l] = 0.0;
-  }
-  __syncthreads();
-  // links of E (Dirichlet faces / wells, R6): sequential for a deterministic order
-  if (tid == 0) {
-    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
-      const int l = A.L.local[q];
-      const double gL = A.L.geo2[q] * A.K[base + l] * total_mobility(A.f, A.s[base + l]);
-      diag[l] += gL;
-      bl[l] += gL * A.L.p[q];
-    }
-  }
-  __syncthreads();
-
-  // B_EE = Phi^T (A_EE Phi), in column chunks of CH basis functions
-  double* BEE = A.blocks + (size_t)E * nb1 * N * N;
-  for (int j0 = 0; j0 < N; j0 += A.CH) {
-    const int ch = min(A.CH, N - j0);
-    for (int t = tid; t < ch * nl; t += nt) {
-      const int jj = t / nl, l = t % nl;
-      const double* ph = Phs + (size_t)(j0 + jj) * nl;
-      int c[3];
-      local_xyz(g, l, c);
-      double y = diag[l] * ph[l];
-      for (int a = 0; a < g.dim; ++a) {
-        if (c[a] + 1 < g.s[a]) y -= wp[a * nl + l] * ph[l + g.lstride[a]];
-        if (c[a] > 0) y -= wp[a * nl + l - g.lstride[a]] * ph[l - g.lstride[a]];
-      }
-      Ys[(size_t)jj * nl + l] = y;
-    }
-    __syncthreads();
-    for (int t = tid; t < N * ch; t += nt) {
-      const int i = t / ch, jj = t % ch, j = j0 + jj;
-      if (i > j) continue;
-      const double* pi = Phs + (size_t)i * nl;
-      const double* yj = Ys + (size_t)jj * nl;
-      double acc = 0.0;
-      for (int l = 0; l < nl; ++l) acc += pi[l] * yj[l];
-      BEE[i * N + j] = acc;
-      BEE[j * N + i] = acc;
-    }
-    __syncthreads();
-  }
-  // r_E = Phi_E^T b_E
-  for (int i = tid; i < N; i += nt) {
-    double acc = 0.0;
-    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
-      const int l = A.L.local[q];
-      // one term per link cell; cells with several links are summed through bl
-      bool first = true;
-      for (int q2 = A.L.sub_start[E]; q2 < q; ++q2)
-        if (A.L.local[q2] == l) first = false;
-      if (first) acc += Phs[(size_t)i * nl + l] * bl[l];
-    }
-    A.rhs[E * N + i] = acc;
-  }
-  // coupling blocks to the upper neighbours: B_{E,E+a}[i][j] = -sum_f w_f Phi_E[i][a_f] Phi_{E+a}[j][b_f]
-  for (int a = 0; a < g.dim; ++a) {
-    double* BEN = BEE + (size_t)(1 + a) * N * N;
-    if (C[a] + 1 >= g.S[a]) {
-      for (int t = tid; t < N * N; t += nt) BEN[t] = 0.0;
-      continue;
-    }
-    const int En = E + g.Estride[a], nf = g.nface[a];
-    const double* PhiN = A.Phi + (size_t)En * N * nl;
-    __syncthreads();
-    for (int t = tid; t < N * nf; t += nt) {
-      const int k = t / nf, f = t % nf;
-      PhN[(size_t)k * A.nfmax + f] = PhiN[(size_t)k * nl + face_cell(g, f, a, 0)];
-    }
-    __syncthreads();
-    for (int t = tid; t < N * N; t += nt) {
-      const int i = t / N, j = t % N;
-      double acc = 0.0;
-      for (int f = 0; f < nf; ++f)
-        acc += wi[a * A.nfmax + f] * Phs[(size_t)i * nl + face_cell(g, f, a, g.s[a] - 1)] *
-               PhN[(size_t)j * A.nfmax + f];
-      BEN[t] = -acc;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------- a3: PCG
-struct PcgArgs {
-  Geo g;
-  const double* blocks;
-  const double* rhs;
-  const double* zc;
-  const double* Binv;   // [n_pad][n_pad] coarse inverse
-  double* x;
-  double* r;
-  double* z;
-  double* p;
-  double* q;
-  double* DinvT;        // [n_s][N][N]: DinvT[j][k] = (B_EE^-1)[k][j]
-  double* wc;           // [n_s] coarse residual
-  double* partials;     // [4][G]
-  int* iters;
-  int* flags;
-  double rtol;
-  int max_iters;
-  int n_pad;
-  int use_coarse;
-};
-
-// y_E = (B v)_E for lane k < N (warp-level; B symmetric, upper coupling blocks stored)
-__device__ __forceinline__ double spmv_warp(const Geo& g, const double* __restrict__ blocks,
-                                            const double* __restrict__ v, int E, int lane) {
-  const int N = g.N, nb1 = 1 + g.dim;
-  const double* Bd = blocks + (size_t)E * nb1 * N * N;
-  const bool act = lane < N;
-  const double vk = act ? v[E * N + lane] : 0.0;
-  double acc = 0.0;
-  for (int j = 0; j < N; ++j) {
-    const double vj = __shfl_sync(FULL, vk, j);
-    if (act) acc += Bd[j * N + lane] * vj;
-  }
-  int C[3];
-  sub_xyz(g, E, C);
-  for (int a = 0; a < g.dim; ++a) {
-    if (C[a] + 1 < g.S[a]) {   // + B_{E,E+a} v_{E+a}: row access -> warp reductions
-      const double* U = Bd + (size_t)(1 + a) * N * N;
-      const double vn = act ? v[(E + g.Estride[a]) * N + lane] : 0.0;
-      for (int k = 0; k < N; ++k) {
-        double t = act ? U[k * N + lane] * vn : 0.0;
-        t = warp_sum(t);
-        if (lane == k) acc += t;
-      }
-    }
-    if (C[a] > 0) {            // + B_{E-a,E}^T v_{E-a}: column access
-      const int Em = E - g.Estride[a];
-      const double* U = blocks + ((size_t)Em * nb1 + 1 + a) * N * N;
-      const double vm = act ? v[Em * N + lane] : 0.0;
-      for (int j = 0; j < N; ++j) {
-        const double vj = __shfl_sync(FULL, vm, j);
-        if (act) acc += U[j * N + lane] * vj;
-      }
-    }
-  }
-  return acc;
-}
-
-// In-register Gauss-Jordan inverse of the N x N diagonal block (padded to 32 with identity).
-// Lane j holds column j.  No pivoting: B_EE is SPD, pivots are Schur-complement diagonals.
-__device__ __forceinline__ void block_inverse(const double* __restrict__ Bd, double* __restrict__ DinvT,
-                                              int N, int lane, int* flags) {
-  double m[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) m[i] = (lane < N && i < N) ? Bd[i * N + lane] : (i == lane ? 1.0 : 0.0);
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    double f[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) f[i] = __shfl_sync(FULL, m[i], k);
-    const double pk = f[k];
-    bad |= !(pk > 0.0);
-    const double rowk = ((lane == k) ? 1.0 : m[k]) / pk;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i != k) m[i] = ((lane == k) ? 0.0 : m[i]) - f[i] * rowk;
-    m[k] = rowk;
-  }
-  if (bad && lane == 0) atomicOr(flags, FLAG_PIVOT);
-  if (lane < N) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < N) DinvT[lane * N + i] = m[i];
-  }
-}
-
-__global__ void __launch_bounds__(128) k_block_inverse(Geo g, const double* __restrict__ blocks,
-                                                      double* __restrict__ DinvT, int* flags) {
-  const int lane = threadIdx.x & 31;
-  const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (E >= g.n_s) return;
-  block_inverse(blocks + (size_t)E * (1 + g.dim) * g.N * g.N, DinvT + (size_t)E * g.N * g.N, g.N, lane, flags);
-}
-
-template <int W>
-__device__ __forceinline__ void cta_partial(double v, double* red, double* partials, int slot) {
-  // v is warp-uniform; sum warps in order
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < W; ++w) s += red[w];
-    partials[slot * gridDim.x + blockIdx.x] = s;
-  }
-}
-__device__ __forceinline__ double grid_total(const double* partials, int slot) {
-  const int lane = threadIdx.x & 31, G = gridDim.x;
-  double s = 0.0;
-  for (int b = lane; b < G; b += 32) s += partials[slot * G + b];
-  return warp_sum(s);
-}
-
-// z_E = DinvT^T r_E + zc_E e_E,  e_E = sum_F Binv[E][F] wc[F]; returns lane's z and r.z partial
-__device__ __forceinline__ double precond_apply(const PcgArgs& A, int E, int lane, double rk, double& zk) {
-  const int N = A.g.N;
-  const double* Di = A.DinvT + (size_t)E * N * N;
-  double acc = 0.0;
-  for (int j = 0; j < N; ++j) {
-    const double rj = __shfl_sync(FULL, rk, j);
-    if (lane < N) acc += Di[j * N + lane] * rj;
-  }
-  if (A.use_coarse) {
-    const double* row = A.Binv + (size_t)E * A.n_pad;
-    double e = 0.0;
-    for (int F = lane; F < A.g.n_s; F += 32) e += row[F] * A.wc[F];
-    e = warp_sum(e);
-    if (lane < N) acc += A.zc[E * N + lane] * e;
-  }
-  zk = lane < N ? acc : 0.0;
-  return warp_sum(zk * rk);
-}
-
-template <int W>
-__global__ void __launch_bounds__(32 * W, 1) k_pcg(PcgArgs A) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double red[W];
-  const Geo& g = A.g;
-  const int N = g.N;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int TW = gridDim.x * W, gw = blockIdx.x * W + warp;
-  const bool act = lane < N;
-
-  // setup: block-Jacobi inverses, r = b - B x, ||b||^2, ||r||^2, coarse residual
-  double pbb = 0.0, prr = 0.0;
-  for (int E = gw; E < g.n_s; E += TW) {
-    const double bx = spmv_warp(g, A.blocks, A.x, E, lane);
-    const double bk = act ? A.rhs[E * N + lane] : 0.0;
-    const double rk = act ? bk - bx : 0.0;
-    if (act) A.r[E * N + lane] = rk;
-    pbb += warp_sum(bk * bk);
-    prr += warp_sum(rk * rk);
-    const double w = warp_sum(act ? A.zc[E * N + lane] * rk : 0.0);
-    if (lane == 0) A.wc[E] = w;
-  }
-  cta_partial<W>(pbb, red, A.partials, 0);
-  cta_partial<W>(prr, red, A.partials, 1);
-  grid.sync();
-  const double bb = grid_total(A.partials, 0);
-  double rr = grid_total(A.partials, 1);
-  const double tol2 = A.rtol * A.rtol * bb;
-  double prz = 0.0;
-  for (int E = gw; E < g.n_s; E += TW) {
-    const double rk = act ? A.r[E * N + lane] : 0.0;
-    double zk;
-    prz += precond_apply(A, E, lane, rk, zk);
-    if (act) { A.z[E * N + lane] = zk; A.p[E * N + lane] = zk; }
-  }
-  cta_partial<W>(prz, red, A.partials, 2);
-  grid.sync();
-  double rz = grid_total(A.partials, 2);
-  int it = 0;
-  if (!(rr <= tol2) && bb > 0.0) {
-    for (it = 1; it <= A.max_iters; ++it) {
-      // q = B p, p.q
-      double ppq = 0.0;
-      for (int E = gw; E < g.n_s; E += TW) {
-        const double qk = spmv_warp(g, A.blocks, A.p, E, lane);
-        const double pk = act ? A.p[E * N + lane] : 0.0;
-        if (act) A.q[E * N + lane] = qk;
-        ppq += warp_sum(act ? pk * qk : 0.0);
-      }
-      cta_partial<W>(ppq, red, A.partials, 3);
-      grid.sync();
-      const double pq = grid_total(A.partials, 3);
-      if (!(pq > 0.0)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
-        break;
-      }
-      const double alpha = rz / pq;
-      prr = 0.0;
-      for (int E = gw; E < g.n_s; E += TW) {
-        double rk = 0.0;
-        if (act) {
-          A.x[E * N + lane] += alpha * A.p[E * N + lane];
-          rk = A.r[E * N + lane] - alpha * A.q[E * N + lane];
-          A.r[E * N + lane] = rk;
-        }
-        prr += warp_sum(rk * rk);
-        const double w = warp_sum(act ? A.zc[E * N + lane] * rk : 0.0);
-        if (lane == 0) A.wc[E] = w;
-      }
-      cta_partial<W>(prr, red, A.partials, 1);
-      grid.sync();
-      rr = grid_total(A.partials, 1);
-      if (rr <= tol2) break;
-      prz = 0.0;
-      for (int E = gw; E < g.n_s; E += TW) {
-        const double rk = act ? A.r[E * N + lane] : 0.0;
-        double zk;
-        prz += precond_apply(A, E, lane, rk, zk);
-        if (act) A.z[E * N + lane] = zk;
-      }
-      cta_partial<W>(prz, red, A.partials, 2);
-      grid.sync();
-      const double rz_new = grid_total(A.partials, 2);
-      const double beta = rz_new / rz;
-      rz = rz_new;
-      for (int E = gw; E < g.n_s; E += TW)
-        if (act) A.p[E * N + lane] = A.z[E * N + lane] + beta * A.p[E * N + lane];
-      grid.sync();
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    A.iters[0] = it;
-    A.iters[1] += min(it, A.max_iters);
-    if (it > A.max_iters) atomicOr(A.flags, FLAG_NOCONV);
-    if (!(rr == rr)) atomicOr(A.flags, FLAG_NAN);
   }
 }
 
@@ -797,10 +422,10 @@ struct lrbms_ctx {
   lrbms_solver_opts opts{1e-14, 5000, 10, 1};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
-  int proj_CH = 8, proj_nfmax = 1;
+  ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
-  Buf K, phiV, s0, s1, p, Phi, zc, blocks, rhs, c, r, z, pv, q, DinvT, wc, Binv, partials, scal, flags,
+  Buf K, phiV, s0, s1, p, Phi, zc, blocks, rhs, c, r, z, pv, pv2, q, T, DinvT, wc, Binv, Binv32, partials, scal, flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
   char* ws = nullptr;
@@ -1006,19 +631,30 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
-  int W = 1;
-  while (W < 16 && sms * W < g.n_s) W *= 2;
+  int W = std::max(1, std::min(16, cdiv(g.n_s, sms)));
   c->pcg_W = W;
   c->pcg_G = std::min(cdiv(g.n_s, W), sms);   // refined at bind (occupancy)
   c->n_pad = cdiv(g.n_s, 32) * 32;
   c->gj_G = sms;
-  int nfmax = 1;
-  for (int a = 0; a < g.dim; ++a) nfmax = std::max(nfmax, g.nface[a]);
-  c->proj_nfmax = nfmax;
-  c->proj_CH = std::min(g.N, 8);
-  c->proj_smem = sizeof(double) * ((size_t)g.N * g.n_loc + (size_t)c->proj_CH * g.n_loc + 5 * (size_t)g.n_loc +
-                                   3 * (size_t)nfmax + (size_t)g.N * nfmax);
-  if (c->proj_smem > 227 * 1024) return bad("subdomain too large for the shared-memory projection (N * n_loc too big)");
+  {
+    auto up = [](int v, int m) { return (v + m - 1) / m * m; };
+    auto pad4 = [](int v) { while (v % 16 != 4) ++v; return v; };
+    ProjArgs& P = c->proj;
+    P.nlp = up(g.n_loc, 4);
+    P.LD = pad4(P.nlp);
+    P.NP = up(g.N, 8);
+    P.KC = std::min(64, P.nlp);
+    P.LDY = pad4(P.KC);
+    int nfmax = 1;
+    for (int a = 0; a < g.dim; ++a) nfmax = std::max(nfmax, g.nface[a]);
+    P.nfmax = nfmax;
+    P.nfp = up(nfmax, 4);
+    P.LDN = pad4(P.nfp);
+    P.ybuf = up(std::max(std::max(P.NP * P.LDY, P.NP * P.LDN), 8 * 64), 2);
+    c->proj_smem = 8 * ((size_t)P.NP * P.LD + P.ybuf + 6 * (size_t)g.n_loc + 3 * (size_t)nfmax) + 4 * (size_t)nfmax;
+    if (c->proj_smem > 227 * 1024)
+      return bad("subdomain too large for the shared-memory projection (N * n_loc too big)");
+  }
   // workspace layout
   size_t off = 0;
   auto alloc = [&](Buf& b, size_t bytes) {
@@ -1033,10 +669,12 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->zc, R * 8);
   alloc(c->blocks, (size_t)g.n_s * (1 + g.dim) * g.N * g.N * 8);
   alloc(c->rhs, R * 8); alloc(c->c, R * 8); alloc(c->r, R * 8); alloc(c->z, R * 8); alloc(c->pv, R * 8);
-  alloc(c->q, R * 8);
-  alloc(c->DinvT, (size_t)g.n_s * g.N * g.N * 8);
+  alloc(c->pv2, R * 8); alloc(c->q, R * 8);
+  alloc(c->T, R * 3 * 8);
+  alloc(c->DinvT, (size_t)g.n_s * g.N * g.N * 4);
   alloc(c->wc, (size_t)c->n_pad * 8);
   alloc(c->Binv, (size_t)c->n_pad * c->n_pad * 8);
+  alloc(c->Binv32, (size_t)c->n_pad * c->n_pad * 4);
   alloc(c->partials, 8 * (size_t)4 * 4096);
   alloc(c->scal, 8 * 16);
   alloc(c->flags, 4 * 16);
@@ -1064,9 +702,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   CUDA_TRY(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int occ = 0;
   const int W = c->pcg_W;
-  const void* kp = W == 1 ? (const void*)k_pcg<1> : W == 2 ? (const void*)k_pcg<2> : W == 4 ? (const void*)k_pcg<4>
-                 : W == 8 ? (const void*)k_pcg<8> : (const void*)k_pcg<16>;
-  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kp, 32 * W, 0));
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_pcg, 32 * W, 0));
   if (occ < 1) return fail(c, LRBMS_E_CUDA, "PCG kernel cannot be resident");
   c->pcg_G = std::max(1, std::min(cdiv(c->g.n_s, W), sms * occ));
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_coarse_gj, 256, 0));
@@ -1191,11 +827,10 @@ static lrbms_status ready(lrbms_ctx* c) {
 
 static lrbms_status launch_project(lrbms_ctx* c) {
   StageScope sc_(c, 0);
-  ProjArgs A;
+  ProjArgs A = c->proj;
   A.g = c->g; A.f = c->f; A.L = links_of(c);
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs);
-  A.CH = c->proj_CH; A.nfmax = c->proj_nfmax;
   k_project<<<c->g.n_s, 256, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
   c->have_blocks = true;
@@ -1214,6 +849,8 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
   void* args[] = {&Bc, &n, &fl};
   CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj, dim3(c->gj_G), dim3(256), args, 0, c->stream));
   c->launches++;
+  k_to_f32<<<592, 256, 0, c->stream>>>(Bc, c->at<float>(c->Binv32), (size_t)c->n_pad * c->n_pad);
+  LAUNCH_CHECK(c);
   c->rebuilds++;
   c->last_rebuild_step = c->steps;
   return LRBMS_OK;
@@ -1228,7 +865,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   }
   {
     StageScope sc_(c, 2);
-    k_block_inverse<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->DinvT),
+    k_block_inverse<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<float>(c->DinvT),
                                                             c->at<int>(c->flags));
     LAUNCH_CHECK(c);
   }
@@ -1236,16 +873,14 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   PcgArgs A;
   A.g = g;
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs); A.zc = c->at<double>(c->zc);
-  A.Binv = c->at<double>(c->Binv);
-  A.x = c->at<double>(c->c); A.r = c->at<double>(c->r); A.z = c->at<double>(c->z); A.p = c->at<double>(c->pv);
-  A.q = c->at<double>(c->q); A.DinvT = c->at<double>(c->DinvT); A.wc = c->at<double>(c->wc);
+  A.Binv = c->at<float>(c->Binv32); A.DinvT = c->at<float>(c->DinvT);
+  A.x = c->at<double>(c->c); A.r = c->at<double>(c->r); A.z = c->at<double>(c->z);
+  A.pb0 = c->at<double>(c->pv); A.pb1 = c->at<double>(c->pv2);
+  A.qp = c->at<double>(c->q); A.T = c->at<double>(c->T); A.wc = c->at<double>(c->wc);
   A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
   A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
   void* args[] = {&A};
-  const int W = c->pcg_W;
-  const void* kp = W == 1 ? (const void*)k_pcg<1> : W == 2 ? (const void*)k_pcg<2> : W == 4 ? (const void*)k_pcg<4>
-                 : W == 8 ? (const void*)k_pcg<8> : (const void*)k_pcg<16>;
-  CUDA_TRY(c, cudaLaunchCooperativeKernel(kp, dim3(c->pcg_G), dim3(32 * W), args, 0, c->stream));
+  CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, 0, c->stream));
   c->launches++;
   return LRBMS_OK;
 }
