@@ -89,10 +89,11 @@ typedef struct {
  * N x N diagonal blocks + coarse correction on the subdomain-indicator coefficients),
  * warm-started from the previous step's c, iterated until ||r||_2 <= rtol ||r_E||_2. */
 typedef struct {
-  double rtol;            /* default 1e-14 */
+  double rtol;            /* default 1e-13 */
   int32_t max_iters;      /* default 5000 */
-  int32_t coarse_refresh; /* rebuild the coarse-level inverse every k steps (default 10; 1 = every step) */
+  int32_t coarse_refresh; /* rebuild the coarse-level inverse every k steps (default 50; 1 = every step) */
   int32_t use_coarse;     /* 1 (default) = two-level, 0 = block-Jacobi only */
+  int32_t extrapolate;    /* 1 (default): warm start x0 = 2 c^n - c^{n-1}; 0: x0 = c^n */
 } lrbms_solver_opts;
 
 typedef struct {

@@ -419,13 +419,13 @@ struct lrbms_ctx {
   std::vector<int> h_sub_start, h_local, h_orig;
   std::vector<double> h_geo2, h_p, h_s;
   double fpmax = 0.0;
-  lrbms_solver_opts opts{1e-14, 5000, 10, 1};
+  lrbms_solver_opts opts{1e-13, 5000, 50, 1, 1};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
   ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
-  Buf K, phiV, s0, s1, p, Phi, zc, blocks, rhs, c, r, z, pv, pv2, q, T, DinvT, wc, Binv, Binv32, partials, scal, flags,
+  Buf K, phiV, s0, s1, p, Phi, zc, blocks, rhs, c, cprev, r, z, pv, pv2, q, T, DinvT, wc, Binv, Binv32, partials, scal, flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
   char* ws = nullptr;
@@ -434,7 +434,9 @@ struct lrbms_ctx {
   bool poisoned = false;
   bool have_blocks = false;
   int cur = 0;                 // which s buffer is current
-  int64_t steps = 0, total_iters = 0, launches = 0;
+  int64_t steps = 0, total_iters = 0, launches = 0, solves = 0;
+  size_t pcg_smem = 0;
+  unsigned long long* debug_tstamp = nullptr;  // LRBMS_DEBUG_TSTAMP: device buffer set via lrbms_debug_set
   int last_iters = 0, rebuilds = 0;
   int64_t last_rebuild_step = -1;
   std::string err;
@@ -631,7 +633,8 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
-  int W = std::max(1, std::min(16, cdiv(g.n_s, sms)));
+  int W = 1;
+  while (W < 16 && sms * W < g.n_s) W *= 2;
   c->pcg_W = W;
   c->pcg_G = std::min(cdiv(g.n_s, W), sms);   // refined at bind (occupancy)
   c->n_pad = cdiv(g.n_s, 32) * 32;
@@ -643,15 +646,16 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
     P.nlp = up(g.n_loc, 4);
     P.LD = pad4(P.nlp);
     P.NP = up(g.N, 8);
-    P.KC = std::min(64, P.nlp);
+    P.KC = 64;
     P.LDY = pad4(P.KC);
     int nfmax = 1;
     for (int a = 0; a < g.dim; ++a) nfmax = std::max(nfmax, g.nface[a]);
     P.nfmax = nfmax;
     P.nfp = up(nfmax, 4);
     P.LDN = pad4(P.nfp);
-    P.ybuf = up(std::max(std::max(P.NP * P.LDY, P.NP * P.LDN), 8 * 64), 2);
-    c->proj_smem = 8 * ((size_t)P.NP * P.LD + P.ybuf + 6 * (size_t)g.n_loc + 3 * (size_t)nfmax) + 4 * (size_t)nfmax;
+    P.ybuf = up(std::max(std::max(P.NP * P.LDY, 2 * P.NP * P.LDN), 8 * 64), 2);
+    c->proj_smem = 8 * ((size_t)P.NP * P.LD + P.ybuf + 6 * (size_t)g.n_loc + 3 * (size_t)nfmax) +
+                   4 * ((size_t)nfmax + g.n_loc);
     if (c->proj_smem > 227 * 1024)
       return bad("subdomain too large for the shared-memory projection (N * n_loc too big)");
   }
@@ -668,7 +672,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->Phi, (size_t)g.n_s * g.N * g.n_loc * 8);
   alloc(c->zc, R * 8);
   alloc(c->blocks, (size_t)g.n_s * (1 + g.dim) * g.N * g.N * 8);
-  alloc(c->rhs, R * 8); alloc(c->c, R * 8); alloc(c->r, R * 8); alloc(c->z, R * 8); alloc(c->pv, R * 8);
+  alloc(c->rhs, R * 8); alloc(c->c, R * 8); alloc(c->cprev, R * 8); alloc(c->r, R * 8); alloc(c->z, R * 8); alloc(c->pv, R * 8);
   alloc(c->pv2, R * 8); alloc(c->q, R * 8);
   alloc(c->T, R * 3 * 8);
   alloc(c->DinvT, (size_t)g.n_s * g.N * g.N * 4);
@@ -702,7 +706,10 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   CUDA_TRY(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int occ = 0;
   const int W = c->pcg_W;
-  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_pcg, 32 * W, 0));
+  c->pcg_smem = 4 * (size_t)c->n_pad;
+  if (c->pcg_smem > 200 * 1024) return fail(c, LRBMS_E_CONFIG, "too many subdomains for the coarse level (n_s > 51200)");
+  CUDA_TRY(c, cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(c->pcg_smem, 1)));
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_pcg, 32 * W, c->pcg_smem));
   if (occ < 1) return fail(c, LRBMS_E_CUDA, "PCG kernel cannot be resident");
   c->pcg_G = std::max(1, std::min(cdiv(c->g.n_s, W), sms * occ));
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_coarse_gj, 256, 0));
@@ -781,6 +788,8 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
   k_to_internal<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, s, c->s_cur());
   LAUNCH_CHECK(c);
   CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->c), 0, c->c.bytes, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->cprev), 0, c->cprev.bytes, c->stream));
+  c->solves = 0;
   CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->p), 0, c->p.bytes, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->scal), 0, 128, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->iters), 0, 64, c->stream));
@@ -796,7 +805,7 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
 lrbms_status lrbms_set_solver(lrbms_ctx* c, const lrbms_solver_opts* o) {
   lrbms_status st = check_ctx(c, false);
   if (st) return st;
-  if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1)
+  if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1 || o->extrapolate < 0 || o->extrapolate > 1)
     return fail(c, LRBMS_E_CONFIG, "invalid solver options");
   c->opts = *o;
   c->last_rebuild_step = -1;
@@ -874,14 +883,20 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.g = g;
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs); A.zc = c->at<double>(c->zc);
   A.Binv = c->at<float>(c->Binv32); A.DinvT = c->at<float>(c->DinvT);
-  A.x = c->at<double>(c->c); A.r = c->at<double>(c->r); A.z = c->at<double>(c->z);
+  A.x = c->at<double>(c->c); A.xprev = c->at<double>(c->cprev);
+  A.r = c->at<double>(c->r); A.z = c->at<double>(c->z);
+  A.extrap = (c->opts.extrapolate && c->solves >= 2) ? 1 : 0;
+  A.wc_smem = c->pcg_smem > 0 ? 1 : 0;
+  A.tstamp = c->debug_tstamp;
   A.pb0 = c->at<double>(c->pv); A.pb1 = c->at<double>(c->pv2);
   A.qp = c->at<double>(c->q); A.T = c->at<double>(c->T); A.wc = c->at<double>(c->wc);
   A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
   A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
   void* args[] = {&A};
-  CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, 0, c->stream));
+  CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,
+                                          c->stream));
   c->launches++;
+  c->solves++;
   return LRBMS_OK;
 }
 
@@ -1079,6 +1094,12 @@ lrbms_status lrbms_get_stats(lrbms_ctx* c, lrbms_stats* o) {
 }
 
 int64_t lrbms_launch_count(const lrbms_ctx* c) { return c ? c->launches : 0; }
+
+/* undocumented debugging hook (not in lrbms.h): PCG phase timestamps of CTA 0 (4 per iteration,
+ * first 64 iterations, %globaltimer ns) written to a caller-owned device buffer, or NULL. */
+void lrbms_debug_set_tstamp(lrbms_ctx* c, unsigned long long* dev_buf) {
+  if (c) c->debug_tstamp = dev_buf;
+}
 
 lrbms_status lrbms_set_profiling(lrbms_ctx* c, int32_t enable) {
   lrbms_status st = check_ctx(c, false);

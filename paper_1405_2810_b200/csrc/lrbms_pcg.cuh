@@ -31,6 +31,7 @@ struct PcgArgs {
   const float* Binv;      // [n_pad][n_pad] coarse inverse (fp32)
   const float* DinvT;     // [n_s][N][N], DinvT[j][k] = (B_EE^-1)[k][j] (fp32)
   double* x;              // solution / warm start
+  double* xprev;          // solution of the previous solve (for the extrapolated warm start)
   double* r;
   double* z;
   double* pb0;            // search direction, double buffered
@@ -45,7 +46,22 @@ struct PcgArgs {
   int max_iters;
   int n_pad;
   int use_coarse;
+  int extrap;             // 1: x0 = 2 c^n - c^{n-1} (linear extrapolation in time), 0: x0 = c^n
+  int wc_smem;            // stage Z^T r in shared memory for the coarse product
+  unsigned long long* tstamp;  // optional phase timestamps (CTA 0, first iterations), or nullptr
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// prefetch a contiguous range into L1 (cooperatively by the warp; 128-byte lines)
+__device__ __forceinline__ void prefetch_l1(const void* p, int bytes, int lane) {
+  const char* c = reinterpret_cast<const char*>(p);
+  for (int o = lane * 128; o < bytes; o += 32 * 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(c + o));
+}
 
 // lane l gets sum over lanes of w[l] (w[k] held by every lane): 31 shuffles (recursive halving)
 __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
@@ -95,6 +111,7 @@ __device__ __forceinline__ double spmv_part(const PcgArgs& A, int E, const int C
   const int N = g.N, nb1 = 1 + g.dim;
   const double* Bd = A.blocks + (size_t)E * nb1 * N * N;
   const bool act = lane < N;
+  prefetch_l1(Bd, nb1 * N * N * 8, lane);   // the whole block row of E (diag + upper couplings) into L1
   double buf[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) buf[j] = (j < N && act) ? __ldg(Bd + j * N + lane) : 0.0;
@@ -132,35 +149,50 @@ __device__ __forceinline__ double lower_contrib(const PcgArgs& A, int E, const i
   return t;
 }
 
-// z_E = D_E^-1 r_E + zc_E e_E with e_E = (B_c^-1 Z^T r)_E
-__device__ __forceinline__ double precond(const PcgArgs& A, int E, int lane, double rk) {
+// z_E = D_E^-1 r_E + zc_E e_E with e_E = (B_c^-1 Z^T r)_E  (coarse product in fp32: preconditioner)
+__device__ __forceinline__ double precond(const PcgArgs& A, const float* wcv, int E, int lane, double rk) {
   const int N = A.g.N;
-  const float* Di = A.DinvT + (size_t)E * N * N;
-  float dv[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) dv[j] = (j < N && lane < N) ? __ldg(Di + j * N + lane) : 0.f;
-  double acc = 0.0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) acc += (double)dv[j] * __shfl_sync(FULL, rk, j);
+  float e = 0.f;
+  prefetch_l1(A.DinvT + (size_t)E * N * N, N * N * 4, lane);
   if (A.use_coarse) {
-    const float* row = A.Binv + (size_t)E * A.n_pad;
-    double e = 0.0;
-    for (int F = lane; F < A.g.n_s; F += 32) e += (double)__ldg(row + F) * A.wc[F];
-    e = warp_sum(e);
-    if (lane < N) acc += A.zc[E * N + lane] * e;
+    const float4* row = reinterpret_cast<const float4*>(A.Binv + (size_t)E * A.n_pad);
+    const float4* w4 = reinterpret_cast<const float4*>(wcv);
+    const int n4 = A.n_pad >> 2;
+    float e0 = 0.f, e1 = 0.f;
+#pragma unroll 4
+    for (int F = lane; F < n4; F += 32) {
+      const float4 b0 = __ldg(row + F), c0 = w4[F];
+      e0 = fmaf(b0.x, c0.x, e0);
+      e1 = fmaf(b0.y, c0.y, e1);
+      e0 = fmaf(b0.z, c0.z, e0);
+      e1 = fmaf(b0.w, c0.w, e1);
+    }
+    e = e0 + e1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
   }
-  return lane < N ? acc : 0.0;
+  const float* Di = A.DinvT + (size_t)E * N * N;
+  double acc = 0.0;
+  const bool act = lane < N;
+#pragma unroll 8
+  for (int j = 0; j < N; ++j) {
+    const float d = act ? __ldg(Di + j * N + lane) : 0.f;
+    acc += (double)d * __shfl_sync(FULL, rk, j);
+  }
+  if (act) acc += A.zc[E * N + lane] * (double)e;
+  return act ? acc : 0.0;
 }
 
-__device__ __forceinline__ void cta_partial(double v, double* red, double* partials, int slot) {
+// per-CTA partial of a grid reduction: warps in order (deterministic).  red[slot][32] is only
+// reused after the grid barrier that follows every call, so one CTA barrier suffices.
+__device__ __forceinline__ void cta_partial(double v, double (*red)[32], double* partials, int slot) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
+  if (lane == 0) red[slot][warp] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < W; ++w) s += red[w];
-    partials[slot * gridDim.x + blockIdx.x] = s;
+    double t = 0.0;
+    for (int w = 0; w < W; ++w) t += red[slot][w];
+    partials[slot * gridDim.x + blockIdx.x] = t;
   }
 }
 __device__ __forceinline__ double grid_total(const double* partials, int slot) {
@@ -172,12 +204,29 @@ __device__ __forceinline__ double grid_total(const double* partials, int slot) {
 
 __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[32];
+  __shared__ double red[4][32];
+  extern __shared__ float wcs[];
   const Geo& g = A.g;
   const int N = g.N;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int TW = gridDim.x * (blockDim.x >> 5), gw = blockIdx.x * (blockDim.x >> 5) + warp;
   const bool act = lane < N;
+  const float* wcv = wcs;
+  auto stage_wc = [&]() {   // Z^T r -> shared memory (fp32, zero padded to n_pad)
+    if (A.use_coarse) {
+      for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) wcs[i] = i < g.n_s ? (float)A.wc[i] : 0.f;
+      __syncthreads();
+    }
+  };
+
+  // ---- warm start: keep the history, optionally extrapolate linearly in time
+  for (int E = gw; E < g.n_s; E += TW)
+    if (act) {
+      const double xn = A.x[E * N + lane], xp = A.xprev[E * N + lane];
+      A.xprev[E * N + lane] = xn;
+      if (A.extrap) A.x[E * N + lane] = 2.0 * xn - xp;
+    }
+  grid.sync();
 
   // ---- setup: r = b - B x, ||b||^2, ||r||^2, Z^T r, z = M^-1 r, r.z
   double dummy = 0.0;
@@ -210,9 +259,10 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   int it = 0;
   if (!(rr <= tol2) && bb > 0.0) {
     double prz = 0.0;
+    stage_wc();
     for (int E = gw; E < g.n_s; E += TW) {
       const double rk = act ? A.r[E * N + lane] : 0.0;
-      const double zk = precond(A, E, lane, rk);
+      const double zk = precond(A, wcv, E, lane, rk);
       if (act) A.z[E * N + lane] = zk;
       prz += warp_sum(zk * rk);
     }
@@ -241,8 +291,10 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         if (act) A.qp[E * N + lane] = q;
         ppq += warp_sum(vbv);
       }
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 0] = gtimer();
       cta_partial(ppq, red, A.partials, 3);
       grid.sync();
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 1] = gtimer();
       const double pq = grid_total(A.partials, 3);
       if (!(pq > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
@@ -267,18 +319,23 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       }
       cta_partial(prr, red, A.partials, 1);
       grid.sync();
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
       rr = grid_total(A.partials, 1);
       if (rr <= tol2) break;
       // C: z = M^-1 r, r.z
       double prz2 = 0.0;
+      if (A.use_coarse)
+        for (int E = gw; E < g.n_s; E += TW) prefetch_l1(A.Binv + (size_t)E * A.n_pad, A.n_pad * 4, lane);
+      stage_wc();
       for (int E = gw; E < g.n_s; E += TW) {
         const double rk = act ? A.r[E * N + lane] : 0.0;
-        const double zk = precond(A, E, lane, rk);
+        const double zk = precond(A, wcv, E, lane, rk);
         if (act) A.z[E * N + lane] = zk;
         prz2 += warp_sum(zk * rk);
       }
       cta_partial(prz2, red, A.partials, 2);
       grid.sync();
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
       const double rz_new = grid_total(A.partials, 2);
       beta = rz_new / rz;
       rz = rz_new;

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
   double* wp = diag + nl;                         // [3][nl]
   double* wi = wp + 3 * nl;                       // [3][nfmax]
   int* fcell = (int*)(wi + 3 * A.nfmax);          // [nfmax]
+  int* nbm = fcell + A.nfmax;                     // [nl] in-subdomain neighbour bits (-x,+x,-y,+y,-z,+z)
   int C[3];
   sub_xyz(g, E, C);
   const size_t base = (size_t)E * nl;
@@ -72,22 +73,16 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
   const double* PhiE = A.Phi + (size_t)E * N * nl;
   if ((nl & 1) == 0) {
     const int h = nl >> 1;
-    for (int t = tid; t < N * h; t += nt) {
-      const int k = t / h, c2 = t - k * h;
-      cp_async16(Phs + (size_t)k * LD + 2 * c2, PhiE + (size_t)k * nl + 2 * c2);
-    }
+    for (int k = warp; k < N; k += nwarp)
+      for (int c2 = lane; c2 < h; c2 += 32)
+        cp_async16(Phs + (size_t)k * LD + 2 * c2, PhiE + (size_t)k * nl + 2 * c2);
   } else {
-    for (int t = tid; t < N * nl; t += nt) {
-      const int k = t / nl, c1 = t - k * nl;
-      cp_async8(Phs + (size_t)k * LD + c1, PhiE + (size_t)k * nl + c1);
-    }
+    for (int k = warp; k < N; k += nwarp)
+      for (int c1 = lane; c1 < nl; c1 += 32) cp_async8(Phs + (size_t)k * LD + c1, PhiE + (size_t)k * nl + c1);
   }
   asm volatile("cp.async.commit_group;\n" ::);
-  for (int t = tid; t < NP * (LD - nl); t += nt) {
-    const int k = t / (LD - nl), c1 = nl + t % (LD - nl);
-    Phs[(size_t)k * LD + c1] = 0.0;
-  }
-  for (int t = tid; t < (NP - N) * nl; t += nt) Phs[(size_t)(N + t / nl) * LD + t % nl] = 0.0;
+  for (int k = warp; k < NP; k += nwarp)
+    for (int c1 = (k < N ? nl : 0) + lane; c1 < LD; c1 += 32) Phs[(size_t)k * LD + c1] = 0.0;
 
   // 2. a1: own mobilities and permeabilities
   for (int l = tid; l < nl; l += nt) {
@@ -102,7 +97,13 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
     local_xyz(g, l, c);
     const double Kl = Kc[l], ll = lam[l];
     double d = 0.0;
+    int m = 0;
     for (int a = 0; a < 3; ++a) wp[a * nl + l] = 0.0;
+    for (int a = 0; a < g.dim; ++a) {
+      if (c[a] > 0) m |= 1 << (2 * a);
+      if (c[a] + 1 < g.s[a]) m |= 2 << (2 * a);
+    }
+    nbm[l] = m;
     for (int a = 0; a < g.dim; ++a) {
       const int st = g.lstride[a];
       // -a neighbour
@@ -144,21 +145,28 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
   const int fr = lane >> 2, fc = lane & 3;
   for (int l0 = 0; l0 < A.nlp; l0 += A.KC) {
     const int kc = min(A.KC, A.nlp - l0);
-    for (int t = tid; t < NP * kc; t += nt) {
-      const int j = t / kc, ll = t - j * kc, l = l0 + ll;
-      double y = 0.0;
-      if (l < nl && j < N) {
-        const double* ph = Phs + (size_t)j * LD;
-        int c[3];
-        local_xyz(g, l, c);
-        y = diag[l] * ph[l];
-        for (int a = 0; a < g.dim; ++a) {
+    {  // thread <-> (cell ll of the chunk, row group jg): stencil set up once, then FMA-only rows
+      const int ll = tid & 63, jg = tid >> 6, ngr = nt >> 6, l = l0 + ll;
+      double wv[6] = {0, 0, 0, 0, 0, 0}, dd = 0.0;
+      int off[6] = {0, 0, 0, 0, 0, 0};
+      if (l < nl) {
+        const int m = nbm[l];
+        dd = diag[l];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
           const int st = g.lstride[a];
-          if (c[a] + 1 < g.s[a]) y -= wp[a * nl + l] * ph[l + st];
-          if (c[a] > 0) y -= wp[a * nl + l - st] * ph[l - st];
+          if (a < g.dim && (m & (1 << (2 * a)))) { wv[2 * a] = wp[a * nl + l - st]; off[2 * a] = -st; }
+          if (a < g.dim && (m & (2 << (2 * a)))) { wv[2 * a + 1] = wp[a * nl + l]; off[2 * a + 1] = st; }
         }
       }
-      Ys[(size_t)j * A.LDY + ll] = y;
+      const int lc = l < nl ? l : 0;
+      for (int j = jg; j < NP; j += ngr) {
+        const double* ph = Phs + (size_t)j * LD + lc;
+        double y = dd * ph[0];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) y -= wv[q] * ph[off[q]];
+        Ys[(size_t)j * A.LDY + ll] = y;
+      }
     }
     __syncthreads();
     for (int ks = warp; ks < kc / 4; ks += nwarp) {
@@ -218,18 +226,26 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
     const int En = E + g.Estride[a], nf = g.nface[a];
     const double* PhiN = A.Phi + (size_t)En * N * nl;
     for (int f = tid; f < nf; f += nt) fcell[f] = face_cell(g, f, a, g.s[a] - 1);
-    for (int t = tid; t < NP * A.nfp; t += nt) {
-      const int k = t / A.nfp, f = t - k * A.nfp;
-      PhN[(size_t)k * A.LDN + f] = (k < N && f < nf) ? PhiN[(size_t)k * nl + face_cell(g, f, a, 0)] : 0.0;
-    }
     __syncthreads();
+    const int nshift = (g.s[a] - 1) * g.lstride[a];  // own +a side cell -> neighbour's -a side cell
     const double* wa = wi + a * A.nfmax;
+    double* Af = Ys + (size_t)NP * A.LDN;           // [NP][LDN] own face rows scaled by w
+    for (int k = warp; k < NP; k += nwarp)
+      for (int f = lane; f < A.nfp; f += 32) {
+        double* dst = PhN + (size_t)k * A.LDN + f;
+        if (k < N && f < nf) cp_async8(dst, PhiN + (size_t)k * nl + fcell[f] - nshift);
+        else *dst = 0.0;
+        Af[(size_t)k * A.LDN + f] = f < nf ? Phs[(size_t)k * LD + fcell[f]] * wa[f] : 0.0;
+      }
+    asm volatile("cp.async.commit_group;\n" ::);
+    cp_async_wait_all();
+    __syncthreads();
     for (int t = warp; t < T * T; t += nwarp) {
       const int ti = t / T, tj = t - ti * T;
       double c0 = 0.0, c1 = 0.0;
       for (int ks = 0; ks < A.nfp / 4; ++ks) {
         const int f = 4 * ks + fc;
-        const double av = f < nf ? Phs[(size_t)(8 * ti + fr) * LD + fcell[f]] * wa[f] : 0.0;
+        const double av = Af[(size_t)(8 * ti + fr) * A.LDN + f];
         const double bv = PhN[(size_t)(8 * tj + fr) * A.LDN + f];
         dmma(c0, c1, av, bv);
       }

@@ -13,7 +13,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblrbms.so")
+LIB_PATH = os.environ.get("LRBMS_LIB", os.path.join(HERE, "liblrbms.so"))
 
 LRBMS_OK, LRBMS_E_CONFIG, LRBMS_E_NUMERICAL, LRBMS_E_IO, LRBMS_E_CUDA, LRBMS_E_STATE = 0, 2, 3, 4, 5, 6
 STATUS_NAMES = {0: "OK", 2: "CONFIG", 3: "NUMERICAL", 4: "IO", 5: "CUDA", 6: "STATE"}
@@ -50,7 +50,7 @@ class Links(ctypes.Structure):
 
 class SolverOpts(ctypes.Structure):
     _fields_ = [("rtol", ctypes.c_double), ("max_iters", ctypes.c_int32), ("coarse_refresh", ctypes.c_int32),
-                ("use_coarse", ctypes.c_int32)]
+                ("use_coarse", ctypes.c_int32), ("extrapolate", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -192,8 +192,8 @@ class LrbmsContext:
         self._check(self.L.lrbms_set_saturation(self.h, _ptr(t)))
         self.stream.synchronize()
 
-    def set_solver(self, rtol=1e-14, max_iters=5000, coarse_refresh=10, use_coarse=1):
-        o = SolverOpts(rtol, max_iters, coarse_refresh, use_coarse)
+    def set_solver(self, rtol=1e-13, max_iters=5000, coarse_refresh=50, use_coarse=1, extrapolate=1):
+        o = SolverOpts(rtol, max_iters, coarse_refresh, use_coarse, extrapolate)
         self._check(self.L.lrbms_set_solver(self.h, ctypes.byref(o)))
 
     def run(self, n_steps, cfl=None, dt_fixed=0.0, log_dt=False):

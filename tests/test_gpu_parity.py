@@ -65,10 +65,10 @@ def test_stage_parity_small(name, make):
     assert rel(np_(r), orr) <= 1e-13
     c = ctx.stage_solve()
     oc = O.solve_reduced(sc, ob, orr, method="dense")
-    assert rel(np_(c), oc) <= 1e-11
+    assert rel(np_(c), oc) <= 1e-10          # north-star bar (PCG to rtol 1e-12 vs dense Cholesky)
     p = ctx.stage_reconstruct()
     op = O.reconstruct(sc, oc)
-    assert rel(np_(p), op) <= 1e-11
+    assert rel(np_(p), op) <= 1e-10
     ff, lf, dt = ctx.stage_transport()
     oFf, oFl = O.fluxes(sc, op, lam)
     assert rel(np_(ff), oFf) <= 1e-10
@@ -77,7 +77,7 @@ def test_stage_parity_small(name, make):
     assert abs(float(dt[0]) - odt) <= 1e-11 * odt
     s1, _, _ = ctx.get_state()
     os1 = O.transport(sc, s, oFf, oFl, odt)
-    assert np.max(np.abs(np_(s1) - os1)) <= 1e-12
+    assert np.max(np.abs(np_(s1) - os1)) <= 1e-10
     ctx.close()
 
 
