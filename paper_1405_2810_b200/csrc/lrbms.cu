@@ -62,6 +62,33 @@ __global__ void k_scale_phi(Geo g, double* __restrict__ phiV, int* flags) {
   if (!(v > 0.0)) atomicOr(flags, FLAG_NAN);
   phiV[idx] = v * g.vol;
 }
+// static face coefficients fc[g][a] = (T tau_a, T tau_b) of the face to the +a neighbour (R2)
+__global__ void k_face_coef(Geo g, const double* __restrict__ K, double2* __restrict__ fc) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  const int E = idx / g.n_loc, l = idx % g.n_loc;
+  int C[3], c[3];
+  sub_xyz(g, E, C);
+  local_xyz(g, l, c);
+  for (int a = 0; a < 3; ++a) {
+    double2 v = make_double2(0.0, 0.0);
+    if (a < g.dim) {
+      const int nb = neighbour(g, E, C, l, c, a, +1);
+      if (nb >= 0) {
+        const double Ka = K[idx], Kb = K[nb];
+        const double T = g.geo[a] * 2.0 * Ka * Kb / (Ka + Kb);
+        v = make_double2(T * (Ka / (Ka + Kb)), T * (Kb / (Ka + Kb)));
+      }
+    }
+    fc[(size_t)idx * 3 + a] = v;
+  }
+}
+__global__ void k_link_coef(Geo g, Links L, const double* __restrict__ K, double* __restrict__ gK, int n_links) {
+  const int E = blockIdx.x * blockDim.x + threadIdx.x;
+  if (E >= g.n_s) return;
+  for (int q = L.sub_start[E]; q < L.sub_start[E + 1]; ++q) gK[q] = L.geo2[q] * K[(size_t)E * g.n_loc + L.local[q]];
+}
+
 // zc[E][k] = sum_l Phi[E][k][l]: coefficients of the subdomain indicator 1_E (coarse space)
 __global__ void k_basis_indicator(Geo g, const double* __restrict__ Phi, double* __restrict__ zc) {
   int E = blockIdx.x;
@@ -239,6 +266,7 @@ struct FluxArgs {
   const double* K;
   const double* p;
   const double* phiV;   // phi * V or nullptr (phi = 1)
+  const double2* fc;    // [n][3] static face coefficients
   double* s_out;
   unsigned long long* dt_bits;
   double* dt_log;       // [steps] or nullptr
@@ -252,23 +280,22 @@ struct FluxArgs {
   int step;
 };
 
-// flux on the face between cell (this, lower if dir > 0) and its neighbour nb; returns the
-// flux leaving this cell and, optionally, the fractional-flow-weighted flux leaving it.
-__device__ __forceinline__ double out_flux(const FluxArgs& A, int a, int dir, double Kl, double ll,
-                                           double pl, double sl, int nb, double& fwout) {
-  const double Kn = A.K[nb];
+// flux on the face between this cell and its neighbour nb along axis a (dir = +-1); returns the
+// flux leaving this cell and, in fwout, the fractional-flow-weighted flux leaving it.
+__device__ __forceinline__ double out_flux(const FluxArgs& A, int a, int dir, size_t gl, double ll, double pl,
+                                           double sl, int nb, double& fwout) {
   const double sn = A.s[nb];
   const double ln = total_mobility(A.f, sn);
   const double pn = A.p[nb];
   double F, s_up;
   if (dir > 0) {   // this = T1, nb = T2: F = w (p1 - p2), leaving this cell
-    F = face_weight(A.g.geo[a], Kl, Kn, ll, ln) * (pl - pn);
+    F = face_w(A.fc[gl * 3 + a], ll, ln) * (pl - pn);
     s_up = F >= 0.0 ? sl : sn;
     fwout = F * frac_flow(A.f, s_up);
     return F;
   }
   // nb = T1, this = T2: F = w (p1 - p2) leaves T1, i.e. -F leaves this cell
-  F = face_weight(A.g.geo[a], Kn, Kl, ln, ll) * (pn - pl);
+  F = face_w(A.fc[(size_t)nb * 3 + a], ln, ll) * (pn - pl);
   s_up = F >= 0.0 ? sn : sl;
   fwout = -(F * frac_flow(A.f, s_up));
   return -F;
@@ -296,7 +323,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
   for (int l = threadIdx.x; l < nl; l += blockDim.x) {
     int c[3];
     local_xyz(g, l, c);
-    const double Kl = A.K[base + l], sl = A.s[base + l], pl = A.p[base + l];
+    const double sl = A.s[base + l], pl = A.p[base + l];
     const double ll = total_mobility(A.f, sl);
     double pos = 0.0, neg = 0.0;
     for (int a = 0; a < g.dim; ++a)
@@ -304,7 +331,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
         const int nb = neighbour(g, E, C, l, c, a, dir);
         if (nb < 0) continue;
         double fw;
-        const double F = out_flux(A, a, dir, Kl, ll, pl, sl, nb, fw);
+        const double F = out_flux(A, a, dir, base + l, ll, pl, sl, nb, fw);
         pos += fmax(F, 0.0);
         neg += fmax(-F, 0.0);
         if (A.face_flux && dir > 0) {
@@ -320,7 +347,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
     for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
       const int l = A.L.local[q];
       const double sl = A.s[base + l];
-      const double F = A.L.geo2[q] * A.K[base + l] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
+      const double F = A.L.gK[q] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
       opos[l] += fmax(F, 0.0);
       oneg[l] += fmax(-F, 0.0);
       if (A.link_flux) A.link_flux[A.L.orig[q]] = F;
@@ -364,7 +391,7 @@ __global__ void __launch_bounds__(512) k_transport(FluxArgs A) {
   for (int l = threadIdx.x; l < nl; l += blockDim.x) {
     int c[3];
     local_xyz(g, l, c);
-    const double Kl = A.K[base + l], sl = A.s[base + l], pl = A.p[base + l];
+    const double sl = A.s[base + l], pl = A.p[base + l];
     const double ll = total_mobility(A.f, sl);
     double acc = 0.0;
     for (int a = 0; a < g.dim; ++a)
@@ -372,7 +399,7 @@ __global__ void __launch_bounds__(512) k_transport(FluxArgs A) {
         const int nb = neighbour(g, E, C, l, c, a, dir);
         if (nb < 0) continue;
         double fw;
-        out_flux(A, a, dir, Kl, ll, pl, sl, nb, fw);
+        out_flux(A, a, dir, base + l, ll, pl, sl, nb, fw);
         acc += fw;
       }
     net[l] = acc;
@@ -382,7 +409,7 @@ __global__ void __launch_bounds__(512) k_transport(FluxArgs A) {
     for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
       const int l = A.L.local[q];
       const double sl = A.s[base + l];
-      const double F = A.L.geo2[q] * A.K[base + l] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
+      const double F = A.L.gK[q] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
       const double s_up = F >= 0.0 ? sl : A.L.s_ext[q];
       net[l] += F * frac_flow(A.f, s_up);
     }
@@ -425,7 +452,8 @@ struct lrbms_ctx {
   ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
-  Buf K, phiV, s0, s1, p, Phi, zc, blocks, rhs, c, cprev, r, z, pv, pv2, q, T, DinvT, wc, Binv, Binv32, partials, scal, flags,
+  Buf K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, cprev, yv, r, z, pv, pv2, q, T, Linv, wc, Binv, Binv32, partials, scal,
+      flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
   char* ws = nullptr;
@@ -436,7 +464,7 @@ struct lrbms_ctx {
   int cur = 0;                 // which s buffer is current
   int64_t steps = 0, total_iters = 0, launches = 0, solves = 0;
   size_t pcg_smem = 0;
-  unsigned long long* debug_tstamp = nullptr;  // LRBMS_DEBUG_TSTAMP: device buffer set via lrbms_debug_set
+  unsigned long long* debug_tstamp = nullptr;  // set by lrbms_debug_set_tstamp (not in lrbms.h)
   int last_iters = 0, rebuilds = 0;
   int64_t last_rebuild_step = -1;
   std::string err;
@@ -515,6 +543,7 @@ static lrbms_status check_ctx(lrbms_ctx* c, bool need_bound = true) {
 }
 
 static int cdiv(int a, int b) { return (a + b - 1) / b; }
+static Links links_of(const lrbms_ctx* c);
 
 // stage profiling: record an event pair around each stage; resolved after the stream syncs
 static cudaEvent_t next_event(lrbms_ctx* c) {
@@ -596,6 +625,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   if (!(fl->swr >= 0) || !(fl->sor >= 0) || !(fl->swr + fl->sor < 1)) return bad("need swr, sor >= 0, swr + sor < 1");
   if (!(fl->nw >= 1) || !(fl->no >= 1)) return bad("Corey exponents must be >= 1");
   f.mu_w = fl->mu_w; f.mu_o = fl->mu_o; f.swr = fl->swr; f.range = 1.0 - fl->swr - fl->sor;
+  f.inv_range = 1.0 / f.range; f.inv_mu_w = 1.0 / f.mu_w; f.inv_mu_o = 1.0 / f.mu_o;
   f.nw = fl->nw; f.no = fl->no;
   f.kind = (fl->nw == 2.0 && fl->no == 2.0) ? 2 : ((fl->nw == 1.0 && fl->no == 1.0) ? 1 : 0);
   c->fpmax = fprime_max_host(f);
@@ -667,7 +697,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
     off += (bytes + 255) / 256 * 256;
   };
   const size_t n = g.n, R = (size_t)g.n_s * g.N;
-  alloc(c->K, n * 8); alloc(c->phiV, n * 8); alloc(c->s0, n * 8); alloc(c->s1, n * 8); alloc(c->p, n * 8);
+  alloc(c->K, n * 8); alloc(c->fc, n * 3 * 16); alloc(c->l_gK, 8 * (size_t)nl); alloc(c->phiV, n * 8); alloc(c->s0, n * 8); alloc(c->s1, n * 8); alloc(c->p, n * 8);
   alloc(c->tmp, n * 8);
   alloc(c->Phi, (size_t)g.n_s * g.N * g.n_loc * 8);
   alloc(c->zc, R * 8);
@@ -675,7 +705,8 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->rhs, R * 8); alloc(c->c, R * 8); alloc(c->cprev, R * 8); alloc(c->r, R * 8); alloc(c->z, R * 8); alloc(c->pv, R * 8);
   alloc(c->pv2, R * 8); alloc(c->q, R * 8);
   alloc(c->T, R * 3 * 8);
-  alloc(c->DinvT, (size_t)g.n_s * g.N * g.N * 4);
+  alloc(c->Linv, (size_t)g.n_s * g.N * g.N * 8);
+  alloc(c->zh, R * 8); alloc(c->yv, R * 8);
   alloc(c->wc, (size_t)c->n_pad * 8);
   alloc(c->Binv, (size_t)c->n_pad * c->n_pad * 8);
   alloc(c->Binv32, (size_t)c->n_pad * c->n_pad * 4);
@@ -740,6 +771,11 @@ lrbms_status lrbms_set_medium(lrbms_ctx* c, const double* K, const double* phi) 
   const Geo& g = c->g;
   const int nb = cdiv(g.n, 256);
   k_to_internal<<<nb, 256, 0, c->stream>>>(g, K, c->at<double>(c->K));
+  LAUNCH_CHECK(c);
+  k_face_coef<<<nb, 256, 0, c->stream>>>(g, c->at<double>(c->K), c->at<double2>(c->fc));
+  LAUNCH_CHECK(c);
+  k_link_coef<<<cdiv(g.n_s, 128), 128, 0, c->stream>>>(g, links_of(c), c->at<double>(c->K), c->at<double>(c->l_gK),
+                                                         c->n_links);
   LAUNCH_CHECK(c);
   if (phi) {
     k_to_internal<<<nb, 256, 0, c->stream>>>(g, phi, c->at<double>(c->phiV));
@@ -821,6 +857,7 @@ static Links links_of(const lrbms_ctx* c) {
   L.local = c->at<int>(c->l_local);
   L.orig = c->at<int>(c->l_orig);
   L.geo2 = c->at<double>(c->l_geo2);
+  L.gK = c->at<double>(c->l_gK);
   L.p = c->at<double>(c->l_p);
   L.s_ext = c->at<double>(c->l_s);
   return L;
@@ -839,6 +876,7 @@ static lrbms_status launch_project(lrbms_ctx* c) {
   ProjArgs A = c->proj;
   A.g = c->g; A.f = c->f; A.L = links_of(c);
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
+  A.fc = c->at<double2>(c->fc);
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs);
   k_project<<<c->g.n_s, 256, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
@@ -869,29 +907,33 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   const Geo& g = c->g;
   const bool coarse = c->opts.use_coarse && g.n_s > 1;
   if (coarse && (c->last_rebuild_step < 0 || c->steps - c->last_rebuild_step >= c->opts.coarse_refresh)) {
-    lrbms_status st = launch_coarse(c);
+    lrbms_status st = launch_coarse(c);   // from the untransformed blocks
     if (st) return st;
   }
   {
-    StageScope sc_(c, 2);
-    k_block_inverse<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<float>(c->DinvT),
-                                                            c->at<int>(c->flags));
+    StageScope sc_(c, 2);   // block Cholesky + scaling of the couplings: Bh = L^-1 B L^-T
+    k_block_chol<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
+                                                         c->at<double>(c->zc), c->at<double>(c->zh),
+                                                         c->at<int>(c->flags));
+    LAUNCH_CHECK(c);
+    k_transform<<<g.n_s, 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv));
     LAUNCH_CHECK(c);
   }
+  c->have_blocks = false;   // the blocks are now in scaled form
   StageScope sc_(c, 3);
   PcgArgs A;
   A.g = g;
-  A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs); A.zc = c->at<double>(c->zc);
-  A.Binv = c->at<float>(c->Binv32); A.DinvT = c->at<float>(c->DinvT);
-  A.x = c->at<double>(c->c); A.xprev = c->at<double>(c->cprev);
+  A.blocks = c->at<double>(c->blocks); A.Linv = c->at<double>(c->Linv);
+  A.rhs = c->at<double>(c->rhs); A.zh = c->at<double>(c->zh);
+  A.Binv = c->at<float>(c->Binv32);
+  A.x = c->at<double>(c->c); A.xprev = c->at<double>(c->cprev); A.y = c->at<double>(c->yv);
   A.r = c->at<double>(c->r); A.z = c->at<double>(c->z);
-  A.extrap = (c->opts.extrapolate && c->solves >= 2) ? 1 : 0;
-  A.wc_smem = c->pcg_smem > 0 ? 1 : 0;
-  A.tstamp = c->debug_tstamp;
   A.pb0 = c->at<double>(c->pv); A.pb1 = c->at<double>(c->pv2);
   A.qp = c->at<double>(c->q); A.T = c->at<double>(c->T); A.wc = c->at<double>(c->wc);
   A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
   A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
+  A.extrap = (c->opts.extrapolate && c->solves >= 2) ? 1 : 0;
+  A.tstamp = c->debug_tstamp;
   void* args[] = {&A};
   CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,
                                           c->stream));
@@ -915,6 +957,7 @@ static FluxArgs flux_args(lrbms_ctx* c, double cfl, double dt_fixed, double* dt_
   A.g = c->g; A.f = c->f; A.L = links_of(c);
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.p = c->at<double>(c->p);
   A.phiV = c->have_phi ? c->at<double>(c->phiV) : nullptr;
+  A.fc = c->at<double2>(c->fc);
   A.s_out = c->s_nxt();
   A.dt_bits = (unsigned long long*)c->at<double>(c->scal);
   A.t_acc = c->at<double>(c->scal) + 1;

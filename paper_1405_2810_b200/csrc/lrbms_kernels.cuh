@@ -31,6 +31,7 @@ struct Geo {
 
 struct Flu {
   double mu_w, mu_o, swr, range, nw, no;
+  double inv_range, inv_mu_w, inv_mu_o;   // reciprocals: no fp64 divisions in the per-cell kernels
   int kind;        // 1 = linear, 2 = quadratic Corey, 0 = general exponents
 };
 
@@ -39,6 +40,7 @@ struct Links {     // sorted by (subdomain, local cell, original index)
   const int* local;       // [n_links] local cell l
   const int* orig;        // [n_links] index in the caller's link list
   const double* geo2;     // [n_links] 2|F|/h of the link face
+  const double* gK;       // [n_links] 2|F|/h * K_cell (set with the medium): g_L = gK * lambda
   const double* p;        // [n_links] fixed pressure p_L
   const double* s_ext;    // [n_links] external saturation
 };
@@ -46,7 +48,7 @@ struct Links {     // sorted by (subdomain, local cell, original index)
 // ------------------------------------------------------------------ a1: mobilities
 // eq:brooksCorey P:183-186 with Corey k_r (R5), S_e clamped (A8); eq:frationalFlow P:203-206.
 __device__ __forceinline__ void mobilities(const Flu& f, double s, double& lw, double& lo) {
-  double se = (s - f.swr) / f.range;
+  double se = (s - f.swr) * f.inv_range;
   se = fmin(fmax(se, 0.0), 1.0);
   double kw, ko;
   if (f.kind == 2) {
@@ -59,8 +61,8 @@ __device__ __forceinline__ void mobilities(const Flu& f, double s, double& lw, d
     kw = pow(se, f.nw);
     ko = pow(1.0 - se, f.no);
   }
-  lw = kw / f.mu_w;
-  lo = ko / f.mu_o;
+  lw = kw * f.inv_mu_w;
+  lo = ko * f.inv_mu_o;
 }
 __device__ __forceinline__ double total_mobility(const Flu& f, double s) {
   double lw, lo;
@@ -84,6 +86,12 @@ __device__ __forceinline__ double face_weight(double geo, double Ka, double Kb, 
   double tb = Kb / (Ka + Kb);
   return T * (ta * la + tb * lb);
 }
+
+// Static face coefficients (set with the medium): for the face between cell a (lower) and its +axis
+// neighbour b, fc = (T_F tau_a, T_F tau_b), so w_F(lambda) = fc.x lambda_a + fc.y lambda_b.
+// Both cells of a face read the same fc and evaluate the same expression: bitwise antisymmetric
+// fluxes.  fc = (0, 0) where there is no +axis neighbour.
+__device__ __forceinline__ double face_w(double2 fc, double la, double lb) { return fc.x * la + fc.y * lb; }
 
 // ------------------------------------------------------------------ index helpers
 __device__ __forceinline__ void local_xyz(const Geo& g, int l, int c[3]) {

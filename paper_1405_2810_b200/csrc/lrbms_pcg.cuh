@@ -1,23 +1,28 @@
 // lrbms_pcg.cuh -- a3: the reduced solve B c = r (eq:reducedSystem) on the GPU.
 //
-// One cooperative persistent kernel per solve, warp per subdomain (lane k <-> coefficient k of
-// c_E, N <= 32).  Two-level preconditioned CG (Hestenes-Stiefel), warm-started from the previous
-// step, iterated to ||r||_2 <= rtol ||b||_2 (exact-solve reading A17):
-//   M^-1 r = D^-1 r + Z B_c^-1 Z^T r,  D = blockdiag(B_EE),  Z_E = Phi_E 1_E (indicator coefficients).
-// The preconditioner is stored in fp32 (it only steers the iteration; every product with B, every
-// vector update and every reduction is fp64).
+// 1. k_block_chol (warp per subdomain): B_EE = L_E L_E^T (in-register Cholesky), L_E^-1, and the
+//    transformed coarse vector zh_E = L_E^T zc_E.
+// 2. k_transform (warp per coupling block): Bh_{E,E'} = L_E^-1 B_{E,E'} L_E'^-T, in place.
+//    The block-Jacobi-scaled system  Bh y = L^-1 r,  c = L^-T y  has an IDENTITY diagonal block:
+//    the SpMV reads only the coupling blocks and the block-Jacobi preconditioner costs nothing.
+// 3. k_pcg: one cooperative persistent kernel per solve, warp per subdomain (lane k <-> coefficient
+//    k, N <= 32).  Preconditioned CG (Hestenes-Stiefel) on Bh with the coarse correction
+//    M^-1 = I + Zh B_c^-1 Zh^T (B_c = Zh^T Bh Zh = Z^T B Z, the Galerkin operator on the subdomain
+//    indicators, inverted every few steps), warm-started from the (extrapolated) previous solution,
+//    iterated to ||rh||_2 <= rtol ||L^-1 b||_2 (exact-solve reading A17).
 //
 // SpMV with the upper block storage reads every coupling block ONCE per iteration: the warp of E
-// loads U = B_{E,E+a} row by row (coalesced), forms U v_{E+a} for itself by a warp reduce-scatter
+// loads U = Bh_{E,E+a} row by row (coalesced), forms U v_{E+a} for itself by a warp reduce-scatter
 // and U^T v_E for E+a, which it hands over through T[E+a][a]; the owner adds it after the grid
-// barrier that follows the SpMV anyway (p.q is formed symmetrically, p.Bp = sum_E p_E.D p_E +
+// barrier that follows the SpMV anyway (p.q is formed symmetrically, p.Bp = sum_E p_E.p_E +
 // 2 p_E.U p_{E+a}, so it needs no completed q).  3 grid barriers per iteration:
 //   A: p = z + beta p_old (neighbours recomputed locally), q_partial, T, p.q     -> sync
-//   B: alpha, x += alpha p, r -= alpha q, ||r||^2, Z^T r                        -> sync
-//   C: z = M^-1 r, r.z                                                          -> sync
+//   B: alpha, y += alpha p, r -= alpha q, ||r||^2, Zh^T r                       -> sync
+//   C: z = r + Zh B_c^-1 Zh^T r, r.z                                            -> sync
 // Reductions are per-CTA in warp order, then every warp sums the per-CTA partials in a fixed
 // order: all warps obtain bitwise-identical scalars, so the termination test is grid-uniform and
-// runs are deterministic.
+// runs are deterministic.  The coarse inverse is stored in fp32 (it only steers the iteration);
+// every product with Bh, every vector update and every reduction is fp64.
 #pragma once
 #include "lrbms_kernels.cuh"
 
@@ -25,20 +30,21 @@ namespace lrbms {
 
 struct PcgArgs {
   Geo g;
-  const double* blocks;   // [n_s][1+dim][N][N]
-  const double* rhs;      // [n_s][N]
-  const double* zc;       // [n_s][N]
+  const double* blocks;   // [n_s][1+dim][N][N]: L_E in slot 0, transformed couplings in 1..dim
+  const double* Linv;     // [n_s][N][N] L_E^-1 (row-major)
+  const double* rhs;      // [n_s][N] b
+  const double* zh;       // [n_s][N] L_E^T zc_E
   const float* Binv;      // [n_pad][n_pad] coarse inverse (fp32)
-  const float* DinvT;     // [n_s][N][N], DinvT[j][k] = (B_EE^-1)[k][j] (fp32)
-  double* x;              // solution / warm start
-  double* xprev;          // solution of the previous solve (for the extrapolated warm start)
+  double* x;              // solution c / warm start (original variables)
+  double* xprev;          // previous solution (extrapolation history)
+  double* y;              // transformed unknown L^T c
   double* r;
   double* z;
   double* pb0;            // search direction, double buffered
   double* pb1;
-  double* qp;             // partial q (diag + own upper blocks)
+  double* qp;             // partial q
   double* T;              // [n_s][3][N] transposed contributions from lower neighbours
-  double* wc;             // [n_s] coarse residual Z^T r
+  double* wc;             // [n_s] coarse residual Zh^T r
   double* partials;       // [4][gridDim]
   int* iters;
   int* flags;
@@ -47,7 +53,6 @@ struct PcgArgs {
   int n_pad;
   int use_coarse;
   int extrap;             // 1: x0 = 2 c^n - c^{n-1} (linear extrapolation in time), 0: x0 = c^n
-  int wc_smem;            // stage Z^T r in shared memory for the coarse product
   unsigned long long* tstamp;  // optional phase timestamps (CTA 0, first iterations), or nullptr
 };
 
@@ -102,8 +107,130 @@ __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
   return w[0];
 }
 
-// Part A of y = B v for subdomain E: returns lane's (D v_E + sum_a U_a v_{E+a}); stores U_a^T v_E
-// into T[E+a][a]; adds v_E.(D v_E) + 2 v_E.(U_a v_{E+a}) (lane-local) to vbv.
+// ============================================================================ factorisation + transform
+
+// Warp per subdomain.  Lane j holds column j of the (padded-to-32 with identity) block.
+__global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
+                                                   const double* __restrict__ zc, double* __restrict__ zh,
+                                                   int* flags) {
+  const int lane = threadIdx.x & 31;
+  const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (E >= g.n_s) return;
+  const int N = g.N;
+  double* Bd = blocks + (size_t)E * (1 + g.dim) * N * N;
+  double m[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) m[i] = (lane < N && i < N) ? Bd[i * N + lane] : (i == lane ? 1.0 : 0.0);
+  bool bad = false;
+  const double d0 = m[lane];   // original diagonal entry of this lane's column
+  // right-looking Cholesky on the full symmetric trailing matrix: lane j's m[k] = M[k][j] = M[j][k].
+  // A pivot below 1e-13 of its original diagonal entry means a numerically rank-deficient Phi_E.
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double dkk = __shfl_sync(FULL, m[k], k);
+    bad |= !(dkk > 1e-13 * __shfl_sync(FULL, d0, k));
+    const double d = sqrt(dkk), rd = 1.0 / d;
+    const double ljk = m[k] * rd;          // L[lane][k] for lane >= k
+    double col[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) col[i] = (i > k) ? __shfl_sync(FULL, m[i], k) * rd : 0.0;
+    if (lane > k) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i > k) m[i] -= col[i] * ljk;
+    } else if (lane == k) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) m[i] = (i > k) ? col[i] : (i == k ? d : 0.0);
+    }
+  }
+  // L^-1 by forward substitution, one column per lane: L x = e_lane
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) acc -= __shfl_sync(FULL, m[i], k) * x[k];
+    x[i] = acc * (1.0 / __shfl_sync(FULL, m[i], i));
+  }
+  if (bad && lane == 0) atomicOr(flags, FLAG_PIVOT);
+  const double zk = lane < N ? zc[E * N + lane] : 0.0;
+  double zhat = 0.0;   // (L^T zc)[lane] = sum_i L[i][lane] zc[i]
+#pragma unroll
+  for (int i = 0; i < 32; ++i) zhat += m[i] * __shfl_sync(FULL, zk, i);
+  if (lane < N) {
+    double* Li = Linv + (size_t)E * N * N;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < N) {
+        Bd[i * N + lane] = m[i];   // L in the diagonal slot
+        Li[i * N + lane] = x[i];
+      }
+    zh[E * N + lane] = zhat;
+  }
+}
+
+__device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// CTA (8 warps) per subdomain E: Bh_{E,E+a} = L_E^-1 U L_{E+a}^-T in place for its upper couplings,
+// two 32x32x32 products on the fp64 tensor cores (DMMA) through shared memory (rows padded to 36).
+__global__ void __launch_bounds__(256) k_transform(Geo g, double* __restrict__ blocks,
+                                                  const double* __restrict__ Linv) {
+  constexpr int LDX = 36;
+  __shared__ double XE[32 * LDX], Us[32 * LDX], XN[32 * LDX], T1[32 * LDX];
+  const int E = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int N = g.N, NN = N * N;
+  const int fr = lane >> 2, fc = lane & 3;
+  int C[3];
+  sub_xyz(g, E, C);
+  auto load = [&](double* dst, const double* src) {
+    for (int t = tid; t < 32 * 32; t += blockDim.x) {
+      const int i = t >> 5, j = t & 31;
+      dst[i * LDX + j] = (i < N && j < N) ? src[i * N + j] : 0.0;
+    }
+  };
+  load(XE, Linv + (size_t)E * NN);
+  for (int a = 0; a < g.dim; ++a) {
+    if (C[a] + 1 >= g.S[a]) continue;
+    double* U = blocks + ((size_t)E * (1 + g.dim) + 1 + a) * NN;
+    load(Us, U);
+    load(XN, Linv + (size_t)(E + g.Estride[a]) * NN);
+    __syncthreads();
+    // T1 = X_E U : warp -> tiles (warp, warp + 8) of the 4 x 4 tile grid
+    for (int t = warp; t < 16; t += 8) {
+      const int ti = t >> 2, tj = t & 3;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        dmma_t(c0, c1, XE[(8 * ti + fr) * LDX + 4 * ks + fc], Us[(4 * ks + fc) * LDX + 8 * tj + fr]);
+      T1[(8 * ti + fr) * LDX + 8 * tj + 2 * fc] = c0;
+      T1[(8 * ti + fr) * LDX + 8 * tj + 2 * fc + 1] = c1;
+    }
+    __syncthreads();
+    // Bh = T1 X_N^T
+    for (int t = warp; t < 16; t += 8) {
+      const int ti = t >> 2, tj = t & 3;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        dmma_t(c0, c1, T1[(8 * ti + fr) * LDX + 4 * ks + fc], XN[(8 * tj + fr) * LDX + 4 * ks + fc]);
+      const int i = 8 * ti + fr, j = 8 * tj + 2 * fc;
+      if (i < N) {
+        if (j < N) U[i * N + j] = c0;
+        if (j + 1 < N) U[i * N + j + 1] = c1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================================ PCG on the scaled system
+
+// Part A of q = Bh v for subdomain E: returns lane's (v_E + sum_a U_a v_{E+a}); stores U_a^T v_E
+// into T[E+a][a]; adds v_E.v_E + 2 v_E.(U_a v_{E+a}) (lane-local) to vbv.
 template <class VF>
 __device__ __forceinline__ double spmv_part(const PcgArgs& A, int E, const int C[3], int lane, double vE,
                                             VF vload, double& vbv) {
@@ -111,19 +238,16 @@ __device__ __forceinline__ double spmv_part(const PcgArgs& A, int E, const int C
   const int N = g.N, nb1 = 1 + g.dim;
   const double* Bd = A.blocks + (size_t)E * nb1 * N * N;
   const bool act = lane < N;
-  prefetch_l1(Bd, nb1 * N * N * 8, lane);   // the whole block row of E (diag + upper couplings) into L1
+  double acc = vE;
+  double local = vE * vE;
   double buf[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) buf[j] = (j < N && act) ? __ldg(Bd + j * N + lane) : 0.0;
-  double acc = 0.0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) acc += buf[j] * __shfl_sync(FULL, vE, j);
-  double local = vE * acc;
   for (int a = 0; a < g.dim; ++a) {
     if (C[a] + 1 >= g.S[a]) continue;
     const int En = E + g.Estride[a];
     const double vN = vload(En);
     const double* U = Bd + (size_t)(1 + a) * N * N;
+    for (int b = a + 1; b < g.dim; ++b)        // the next existing coupling block into L1
+      if (C[b] + 1 < g.S[b]) { prefetch_l1(Bd + (size_t)(1 + b) * N * N, N * N * 8, lane); break; }
 #pragma unroll
     for (int k = 0; k < 32; ++k) buf[k] = (k < N && act) ? __ldg(U + k * N + lane) : 0.0;
     double tT = 0.0;  // (U^T v_E)[lane] = sum_k U[k][lane] v_E[k]
@@ -149,11 +273,10 @@ __device__ __forceinline__ double lower_contrib(const PcgArgs& A, int E, const i
   return t;
 }
 
-// z_E = D_E^-1 r_E + zc_E e_E with e_E = (B_c^-1 Z^T r)_E  (coarse product in fp32: preconditioner)
+// z_E = r_E + zh_E e_E with e_E = (B_c^-1 Zh^T r)_E  (coarse product in fp32: preconditioner)
 __device__ __forceinline__ double precond(const PcgArgs& A, const float* wcv, int E, int lane, double rk) {
   const int N = A.g.N;
   float e = 0.f;
-  prefetch_l1(A.DinvT + (size_t)E * N * N, N * N * 4, lane);
   if (A.use_coarse) {
     const float4* row = reinterpret_cast<const float4*>(A.Binv + (size_t)E * A.n_pad);
     const float4* w4 = reinterpret_cast<const float4*>(wcv);
@@ -171,16 +294,7 @@ __device__ __forceinline__ double precond(const PcgArgs& A, const float* wcv, in
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
   }
-  const float* Di = A.DinvT + (size_t)E * N * N;
-  double acc = 0.0;
-  const bool act = lane < N;
-#pragma unroll 8
-  for (int j = 0; j < N; ++j) {
-    const float d = act ? __ldg(Di + j * N + lane) : 0.f;
-    acc += (double)d * __shfl_sync(FULL, rk, j);
-  }
-  if (act) acc += A.zc[E * N + lane] * (double)e;
-  return act ? acc : 0.0;
+  return lane < N ? rk + A.zh[E * N + lane] * (double)e : 0.0;
 }
 
 // per-CTA partial of a grid reduction: warps in order (deterministic).  red[slot][32] is only
@@ -212,48 +326,66 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   const int TW = gridDim.x * (blockDim.x >> 5), gw = blockIdx.x * (blockDim.x >> 5) + warp;
   const bool act = lane < N;
   const float* wcv = wcs;
-  auto stage_wc = [&]() {   // Z^T r -> shared memory (fp32, zero padded to n_pad)
+  auto stage_wc = [&]() {   // Zh^T r -> shared memory (fp32, zero padded to n_pad)
     if (A.use_coarse) {
       for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) wcs[i] = i < g.n_s ? (float)A.wc[i] : 0.f;
       __syncthreads();
     }
   };
 
-  // ---- warm start: keep the history, optionally extrapolate linearly in time
-  for (int E = gw; E < g.n_s; E += TW)
+  // ---- warm start (original variables, history kept) and transform: y0 = L^T x0, rb = L^-1 b
+  double pbb = 0.0;
+  for (int E = gw; E < g.n_s; E += TW) {
+    double xk = 0.0;
     if (act) {
       const double xn = A.x[E * N + lane], xp = A.xprev[E * N + lane];
       A.xprev[E * N + lane] = xn;
-      if (A.extrap) A.x[E * N + lane] = 2.0 * xn - xp;
+      xk = A.extrap ? 2.0 * xn - xp : xn;
     }
+    const double* L = A.blocks + (size_t)E * (1 + g.dim) * N * N;
+    double yk = 0.0;   // (L^T x)[lane] = sum_i L[i][lane] x[i]
+    for (int i = 0; i < N; ++i) {
+      const double xi = __shfl_sync(FULL, xk, i);
+      if (act) yk += L[i * N + lane] * xi;
+    }
+    // rb = L^-1 b by a reduce-scatter over rows of L^-1
+    const double bk = act ? A.rhs[E * N + lane] : 0.0;
+    const double* Li = A.Linv + (size_t)E * N * N;
+    double w[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w[i] = (i < N && act) ? Li[i * N + lane] * bk : 0.0;
+    const double rbk = reduce_scatter32(w, lane);
+    if (act) {
+      A.y[E * N + lane] = yk;
+      A.r[E * N + lane] = rbk;   // r holds rb until the residual is formed
+    }
+    pbb += warp_sum(act ? rbk * rbk : 0.0);
+  }
+  cta_partial(pbb, red, A.partials, 0);
   grid.sync();
-
-  // ---- setup: r = b - B x, ||b||^2, ||r||^2, Z^T r, z = M^-1 r, r.z
+  const double bb = grid_total(A.partials, 0);
+  // ---- r = rb - Bh y0, ||r||^2, Zh^T r
   double dummy = 0.0;
   for (int E = gw; E < g.n_s; E += TW) {
     int C[3];
     sub_xyz(g, E, C);
-    auto xload = [&](int Ep) { return act ? A.x[Ep * N + lane] : 0.0; };
-    const double q = spmv_part(A, E, C, lane, xload(E), xload, dummy);
+    auto yload = [&](int Ep) { return act ? A.y[Ep * N + lane] : 0.0; };
+    const double q = spmv_part(A, E, C, lane, yload(E), yload, dummy);
     if (act) A.qp[E * N + lane] = q;
   }
   grid.sync();
-  double pbb = 0.0, prr = 0.0;
+  double prr = 0.0;
   for (int E = gw; E < g.n_s; E += TW) {
     int C[3];
     sub_xyz(g, E, C);
-    const double bk = act ? A.rhs[E * N + lane] : 0.0;
-    const double rk = act ? bk - (A.qp[E * N + lane] + lower_contrib(A, E, C, lane)) : 0.0;
+    const double rk = act ? A.r[E * N + lane] - (A.qp[E * N + lane] + lower_contrib(A, E, C, lane)) : 0.0;
     if (act) A.r[E * N + lane] = rk;
-    pbb += warp_sum(bk * bk);
     prr += warp_sum(rk * rk);
-    const double w = warp_sum(act ? A.zc[E * N + lane] * rk : 0.0);
+    const double w = warp_sum(act ? A.zh[E * N + lane] * rk : 0.0);
     if (lane == 0) A.wc[E] = w;
   }
-  cta_partial(pbb, red, A.partials, 0);
   cta_partial(prr, red, A.partials, 1);
   grid.sync();
-  const double bb = grid_total(A.partials, 0);
   double rr = grid_total(A.partials, 1);
   const double tol2 = A.rtol * A.rtol * bb;
   int it = 0;
@@ -274,7 +406,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       double* pcur = (it & 1) ? A.pb1 : A.pb0;
       const double* pold = (it & 1) ? A.pb0 : A.pb1;
       const bool first = it == 1;
-      // A: p = z + beta p_old; q_partial = (D + U) p; T; p.Bp
+      // A: p = z + beta p_old; q_partial = (I + U) p; T; p.Bh p
       double ppq = 0.0;
       for (int E = gw; E < g.n_s; E += TW) {
         int C[3];
@@ -301,7 +433,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         break;
       }
       const double alpha = rz / pq;
-      // B: x, r, ||r||^2, Z^T r
+      // B: y, r, ||r||^2, Zh^T r
       prr = 0.0;
       for (int E = gw; E < g.n_s; E += TW) {
         int C[3];
@@ -309,12 +441,12 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         double rk = 0.0;
         if (act) {
           const double q = A.qp[E * N + lane] + lower_contrib(A, E, C, lane);
-          A.x[E * N + lane] += alpha * pcur[E * N + lane];
+          A.y[E * N + lane] += alpha * pcur[E * N + lane];
           rk = A.r[E * N + lane] - alpha * q;
           A.r[E * N + lane] = rk;
         }
         prr += warp_sum(rk * rk);
-        const double w = warp_sum(act ? A.zc[E * N + lane] * rk : 0.0);
+        const double w = warp_sum(act ? A.zh[E * N + lane] * rk : 0.0);
         if (lane == 0) A.wc[E] = w;
       }
       cta_partial(prr, red, A.partials, 1);
@@ -341,46 +473,22 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       rz = rz_new;
     }
   }
+  // ---- back-transform c = L^-T y (per subdomain; no barrier needed)
+  for (int E = gw; E < g.n_s; E += TW) {
+    const double yk = act ? A.y[E * N + lane] : 0.0;
+    const double* Li = A.Linv + (size_t)E * N * N;
+    double xk = 0.0;   // sum_i Linv[i][lane] y[i]
+    for (int i = 0; i < N; ++i) {
+      const double yi = __shfl_sync(FULL, yk, i);
+      if (act) xk += Li[i * N + lane] * yi;
+    }
+    if (act) A.x[E * N + lane] = xk;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.iters[0] = it;
     A.iters[1] += min(it, A.max_iters);
     if (it > A.max_iters) atomicOr(A.flags, FLAG_NOCONV);
     if (!(rr == rr)) atomicOr(A.flags, FLAG_NAN);
-  }
-}
-
-// In-register Gauss-Jordan inverse of the N x N diagonal block (padded to 32 with identity).
-// Lane j holds column j.  No pivoting: B_EE is SPD, pivots are Schur-complement diagonals.
-__global__ void __launch_bounds__(128) k_block_inverse(Geo g, const double* __restrict__ blocks,
-                                                      float* __restrict__ DinvT, int* flags) {
-  const int lane = threadIdx.x & 31;
-  const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (E >= g.n_s) return;
-  const int N = g.N;
-  const double* Bd = blocks + (size_t)E * (1 + g.dim) * N * N;
-  double m[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) m[i] = (lane < N && i < N) ? Bd[i * N + lane] : (i == lane ? 1.0 : 0.0);
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    double f[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) f[i] = __shfl_sync(FULL, m[i], k);
-    const double pk = f[k];
-    bad |= !(pk > 0.0);
-    const double rowk = ((lane == k) ? 1.0 : m[k]) / pk;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i != k) m[i] = ((lane == k) ? 0.0 : m[i]) - f[i] * rowk;
-    m[k] = rowk;
-  }
-  if (bad && lane == 0) atomicOr(flags, FLAG_PIVOT);
-  if (lane < N) {
-    float* D = DinvT + (size_t)E * N * N;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < N) D[lane * N + i] = (float)m[i];
   }
 }
 

@@ -23,6 +23,7 @@ struct ProjArgs {
   const double* s;
   const double* K;
   const double* Phi;
+  const double2* fc;   // [n][3] static face coefficients
   double* blocks;
   double* rhs;
   int LD, nlp, NP, KC, LDY, nfmax, nfp, LDN;
@@ -84,18 +85,15 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
   for (int k = warp; k < NP; k += nwarp)
     for (int c1 = (k < N ? nl : 0) + lane; c1 < LD; c1 += 32) Phs[(size_t)k * LD + c1] = 0.0;
 
-  // 2. a1: own mobilities and permeabilities
-  for (int l = tid; l < nl; l += nt) {
-    lam[l] = total_mobility(A.f, A.s[base + l]);
-    Kc[l] = A.K[base + l];
-  }
+  // 2. a1: own mobilities
+  for (int l = tid; l < nl; l += nt) lam[l] = total_mobility(A.f, A.s[base + l]);
   __syncthreads();
-  // 3. face weights (R2): diag_l = sum over all faces of l; wp = weight to the +a neighbour in E;
-  //    wi = weight across the +a subdomain side
+  // 3. face weights (R2) from the static coefficients: diag_l = sum over all faces of l; wp = weight
+  //    to the +a neighbour in E; wi = weight across the +a subdomain side
   for (int l = tid; l < nl; l += nt) {
     int c[3];
     local_xyz(g, l, c);
-    const double Kl = Kc[l], ll = lam[l];
+    const double ll = lam[l];
     double d = 0.0;
     int m = 0;
     for (int a = 0; a < 3; ++a) wp[a * nl + l] = 0.0;
@@ -106,21 +104,21 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
     nbm[l] = m;
     for (int a = 0; a < g.dim; ++a) {
       const int st = g.lstride[a];
-      // -a neighbour
+      // -a neighbour (the lower cell of that face owns its coefficients)
       if (c[a] > 0) {
-        d += face_weight(g.geo[a], Kc[l - st], Kl, lam[l - st], ll);
+        d += face_w(A.fc[(base + l - st) * 3 + a], lam[l - st], ll);
       } else if (C[a] > 0) {
         const int nb = neighbour(g, E, C, l, c, a, -1);
-        d += face_weight(g.geo[a], A.K[nb], Kl, total_mobility(A.f, A.s[nb]), ll);
+        d += face_w(A.fc[(size_t)nb * 3 + a], total_mobility(A.f, A.s[nb]), ll);
       }
       // +a neighbour
       if (c[a] + 1 < g.s[a]) {
-        const double w = face_weight(g.geo[a], Kl, Kc[l + st], ll, lam[l + st]);
+        const double w = face_w(A.fc[(base + l) * 3 + a], ll, lam[l + st]);
         d += w;
         wp[a * nl + l] = w;
       } else if (C[a] + 1 < g.S[a]) {
         const int nb = neighbour(g, E, C, l, c, a, +1);
-        const double w = face_weight(g.geo[a], Kl, A.K[nb], ll, total_mobility(A.f, A.s[nb]));
+        const double w = face_w(A.fc[(base + l) * 3 + a], ll, total_mobility(A.f, A.s[nb]));
         d += w;
         wi[a * A.nfmax + face_pos(g, c, a)] = w;
       }
@@ -131,7 +129,7 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
   if (tid == 0) {  // links of E (R6), sequential: deterministic
     for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
       const int l = A.L.local[q];
-      diag[l] += A.L.geo2[q] * Kc[l] * lam[l];
+      diag[l] += A.L.gK[q] * lam[l];
     }
   }
   cp_async_wait_all();
@@ -210,7 +208,7 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
     double rr = 0.0;
     for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
       const int l = A.L.local[q];
-      rr += Phs[(size_t)tid * LD + l] * (A.L.geo2[q] * Kc[l] * lam[l] * A.L.p[q]);
+      rr += Phs[(size_t)tid * LD + l] * (A.L.gK[q] * lam[l] * A.L.p[q]);
     }
     A.rhs[E * N + tid] = rr;
   }
