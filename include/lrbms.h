@@ -85,15 +85,16 @@ typedef struct {
   const double *s_ext;
 } lrbms_links;
 
-/* Reduced-solve options (a3).  The solve is preconditioned CG (block-Jacobi on the
- * N x N diagonal blocks + coarse correction on the subdomain-indicator coefficients),
- * warm-started from the previous step's c, iterated until ||r||_2 <= rtol ||r_E||_2. */
+/* Reduced-solve options (a3).  The solve is preconditioned CG on the block-Jacobi-scaled system
+ * L^-1 B L^-T y = L^-1 r (B_EE = L_E L_E^T) with a coarse correction on the subdomain-indicator
+ * coefficients, started from the B-optimal combination of the last `history` solutions (Galerkin
+ * projection onto their span), iterated until ||L^-1 (r - B c)||_2 <= rtol ||L^-1 r||_2. */
 typedef struct {
   double rtol;            /* default 1e-13 */
   int32_t max_iters;      /* default 5000 */
   int32_t coarse_refresh; /* rebuild the coarse-level inverse every k steps (default 50; 1 = every step) */
   int32_t use_coarse;     /* 1 (default) = two-level, 0 = block-Jacobi only */
-  int32_t extrapolate;    /* 1 (default): warm start x0 = 2 c^n - c^{n-1}; 0: x0 = c^n */
+  int32_t history;        /* previous solutions in the initial-guess projection, 0..8 (default 8) */
 } lrbms_solver_opts;
 
 typedef struct {

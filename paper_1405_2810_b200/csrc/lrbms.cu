@@ -433,6 +433,8 @@ __global__ void __launch_bounds__(512) k_transport(FluxArgs A) {
 
 namespace {
 
+constexpr int KHIST = 8;   // previous solutions kept for the Galerkin initial guess
+
 struct Buf {
   size_t off = 0, bytes = 0;
 };
@@ -446,13 +448,14 @@ struct lrbms_ctx {
   std::vector<int> h_sub_start, h_local, h_orig;
   std::vector<double> h_geo2, h_p, h_s;
   double fpmax = 0.0;
-  lrbms_solver_opts opts{1e-13, 5000, 50, 1, 1};
+  lrbms_solver_opts opts{1e-13, 5000, 50, 1, 8};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
   ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
-  Buf K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, cprev, yv, r, z, pv, pv2, q, T, Linv, wc, Binv, Binv32, partials, scal,
+  Buf K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
+      Binv32, partials, scal,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
@@ -463,6 +466,7 @@ struct lrbms_ctx {
   bool have_blocks = false;
   int cur = 0;                 // which s buffer is current
   int64_t steps = 0, total_iters = 0, launches = 0, solves = 0;
+  int hist_count = 0, hist_head = KHIST - 1;   // ring buffer of previous solutions (initial guess)
   size_t pcg_smem = 0;
   unsigned long long* debug_tstamp = nullptr;  // set by lrbms_debug_set_tstamp (not in lrbms.h)
   int last_iters = 0, rebuilds = 0;
@@ -683,7 +687,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
     P.nfmax = nfmax;
     P.nfp = up(nfmax, 4);
     P.LDN = pad4(P.nfp);
-    P.ybuf = up(std::max(std::max(P.NP * P.LDY, 2 * P.NP * P.LDN), 8 * 64), 2);
+    P.ybuf = up(std::max(std::max(P.NP * P.LDY, 2 * P.NP * P.LDN), 16 * 64), 2);
     c->proj_smem = 8 * ((size_t)P.NP * P.LD + P.ybuf + 6 * (size_t)g.n_loc + 3 * (size_t)nfmax) +
                    4 * ((size_t)nfmax + g.n_loc);
     if (c->proj_smem > 227 * 1024)
@@ -702,7 +706,11 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->Phi, (size_t)g.n_s * g.N * g.n_loc * 8);
   alloc(c->zc, R * 8);
   alloc(c->blocks, (size_t)g.n_s * (1 + g.dim) * g.N * g.N * 8);
-  alloc(c->rhs, R * 8); alloc(c->c, R * 8); alloc(c->cprev, R * 8); alloc(c->r, R * 8); alloc(c->z, R * 8); alloc(c->pv, R * 8);
+  alloc(c->rhs, R * 8); alloc(c->c, R * 8); alloc(c->r, R * 8);
+  alloc(c->hist, KHIST * R * 8); alloc(c->Wh, KHIST * R * 8); alloc(c->Vh, KHIST * R * 8);
+  alloc(c->TH, KHIST * 3 * R * 8);
+  alloc(c->rbv, R * 8);
+  alloc(c->gpart, 8 * 44 * (size_t)cdiv(g.n_s, 8)); alloc(c->z, R * 8); alloc(c->pv, R * 8);
   alloc(c->pv2, R * 8); alloc(c->q, R * 8);
   alloc(c->T, R * 3 * 8);
   alloc(c->Linv, (size_t)g.n_s * g.N * g.N * 8);
@@ -710,7 +718,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->wc, (size_t)c->n_pad * 8);
   alloc(c->Binv, (size_t)c->n_pad * c->n_pad * 8);
   alloc(c->Binv32, (size_t)c->n_pad * c->n_pad * 4);
-  alloc(c->partials, 8 * (size_t)4 * 4096);
+  alloc(c->partials, 8 * (size_t)48 * 4096);
   alloc(c->scal, 8 * 16);
   alloc(c->flags, 4 * 16);
   alloc(c->iters, 4 * 16);
@@ -824,8 +832,9 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
   k_to_internal<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, s, c->s_cur());
   LAUNCH_CHECK(c);
   CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->c), 0, c->c.bytes, c->stream));
-  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->cprev), 0, c->cprev.bytes, c->stream));
   c->solves = 0;
+  c->hist_count = 0;
+  c->hist_head = KHIST - 1;
   CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->p), 0, c->p.bytes, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->scal), 0, 128, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->iters), 0, 64, c->stream));
@@ -841,7 +850,7 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
 lrbms_status lrbms_set_solver(lrbms_ctx* c, const lrbms_solver_opts* o) {
   lrbms_status st = check_ctx(c, false);
   if (st) return st;
-  if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1 || o->extrapolate < 0 || o->extrapolate > 1)
+  if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1 || o->history < 0 || o->history > KHIST)
     return fail(c, LRBMS_E_CONFIG, "invalid solver options");
   c->opts = *o;
   c->last_rebuild_step = -1;
@@ -878,7 +887,7 @@ static lrbms_status launch_project(lrbms_ctx* c) {
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
   A.fc = c->at<double2>(c->fc);
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs);
-  k_project<<<c->g.n_s, 256, c->proj_smem, c->stream>>>(A);
+  k_project<<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
   c->have_blocks = true;
   return LRBMS_OK;
@@ -926,19 +935,45 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.blocks = c->at<double>(c->blocks); A.Linv = c->at<double>(c->Linv);
   A.rhs = c->at<double>(c->rhs); A.zh = c->at<double>(c->zh);
   A.Binv = c->at<float>(c->Binv32);
-  A.x = c->at<double>(c->c); A.xprev = c->at<double>(c->cprev); A.y = c->at<double>(c->yv);
+  A.x = c->at<double>(c->c); A.y = c->at<double>(c->yv);
+  const size_t R = (size_t)g.n_s * g.N;
+  A.nh = std::min(c->hist_count, c->opts.history);
+  const int out_slot = (c->hist_head + 1) % KHIST;
+  A.hist_out = c->at<double>(c->hist) + (size_t)out_slot * R;
+  A.W = c->at<double>(c->Wh); A.V = c->at<double>(c->Vh); A.rb = c->at<double>(c->rbv);
+  {
+    HistArgs H;
+    H.g = g;
+    H.blocks = c->at<double>(c->blocks); H.Linv = c->at<double>(c->Linv); H.rhs = c->at<double>(c->rhs);
+    H.hist = c->at<double>(c->hist); H.W = c->at<double>(c->Wh); H.V = c->at<double>(c->Vh);
+    H.TH = c->at<double>(c->TH); H.rb = c->at<double>(c->rbv); H.gpart = c->at<double>(c->gpart);
+    H.nh = A.nh;
+    for (int j = 0; j < 8; ++j) H.hslot[j] = ((c->hist_head - j) % KHIST + KHIST) % KHIST;
+    const int nb = cdiv(g.n_s, 8);
+    k_hist_transform<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
+    LAUNCH_CHECK(c);
+    if (H.nh > 0) {
+      k_hist_spmv<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
+      LAUNCH_CHECK(c);
+      k_hist_gram<<<nb, 256, 0, c->stream>>>(H);
+      LAUNCH_CHECK(c);
+    }
+    A.gpart = H.gpart;
+    A.ngram = nb;
+  }
   A.r = c->at<double>(c->r); A.z = c->at<double>(c->z);
   A.pb0 = c->at<double>(c->pv); A.pb1 = c->at<double>(c->pv2);
   A.qp = c->at<double>(c->q); A.T = c->at<double>(c->T); A.wc = c->at<double>(c->wc);
   A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
   A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
-  A.extrap = (c->opts.extrapolate && c->solves >= 2) ? 1 : 0;
   A.tstamp = c->debug_tstamp;
   void* args[] = {&A};
   CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,
                                           c->stream));
   c->launches++;
   c->solves++;
+  c->hist_head = out_slot;
+  c->hist_count = std::min(c->hist_count + 1, KHIST);
   return LRBMS_OK;
 }
 

@@ -35,8 +35,13 @@ struct PcgArgs {
   const double* rhs;      // [n_s][N] b
   const double* zh;       // [n_s][N] L_E^T zc_E
   const float* Binv;      // [n_pad][n_pad] coarse inverse (fp32)
-  double* x;              // solution c / warm start (original variables)
-  double* xprev;          // previous solution (extrapolation history)
+  double* x;              // solution c (original variables)
+  double* hist_out;       // slot receiving this solve's solution (history ring buffer)
+  const double* W;        // [KH][n_s][N] transformed history L^T c^{n-j}
+  const double* V;        // [KH][n_s][N] Bh W
+  const double* rb;       // [n_s][N] L^-1 b
+  const double* gpart;    // [44][ngram] Gram / rhs partials from k_hist_gram
+  int ngram;
   double* y;              // transformed unknown L^T c
   double* r;
   double* z;
@@ -52,7 +57,7 @@ struct PcgArgs {
   int max_iters;
   int n_pad;
   int use_coarse;
-  int extrap;             // 1: x0 = 2 c^n - c^{n-1} (linear extrapolation in time), 0: x0 = c^n
+  int nh;                 // number of history vectors (0..KH)
   unsigned long long* tstamp;  // optional phase timestamps (CTA 0, first iterations), or nullptr
 };
 
@@ -309,11 +314,271 @@ __device__ __forceinline__ void cta_partial(double v, double (*red)[32], double*
     partials[slot * gridDim.x + blockIdx.x] = t;
   }
 }
+// like cta_partial, for the 44 Gram-matrix slots (own shared buffer, one barrier per slot)
+__device__ __forceinline__ void cta_partial_n(double v, double (*red)[32], double* partials, int slot) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+  if (lane == 0) red[slot - 4][warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < W; ++w) t += red[slot - 4][w];
+    partials[slot * gridDim.x + blockIdx.x] = t;
+  }
+}
 __device__ __forceinline__ double grid_total(const double* partials, int slot) {
   const int lane = threadIdx.x & 31, G = gridDim.x;
   double s = 0.0;
   for (int b = lane; b < G; b += 32) s += partials[slot * G + b];
   return warp_sum(s);
+}
+
+// ============================================================================ initial guess (history)
+// Galerkin projection of the new solution onto the span of the last nh solutions, in the scaled
+// variables W_j = L^T c^{n-j}: minimise ||y - y*||_Bh over y0 = W alpha, (W^T Bh W) alpha = W^T rb.
+// Three small kernels (W and rb; V = Bh W with one read of every coupling block; Gram partials)
+// precede k_pcg, which solves the nh x nh system redundantly in every thread.
+
+struct HistArgs {
+  Geo g;
+  const double* blocks;   // L in slot 0, scaled couplings
+  const double* Linv;
+  const double* rhs;
+  const double* hist;     // [KH][R] ring buffer
+  double* W;              // [KH][R]
+  double* V;              // [KH][R]
+  double* TH;             // [KH][n_s][3][N]
+  double* rb;             // [R]  L^-1 b
+  double* gpart;          // [44][gridDim] Gram / rhs partials
+  int nh;
+  int hslot[8];
+};
+
+// warp per subdomain; each warp stages 32x32 blocks in its own padded shared tile
+__global__ void __launch_bounds__(128) k_hist_transform(HistArgs A) {
+  __shared__ double tile[4][32 * 33];
+  const Geo& g = A.g;
+  const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int E = blockIdx.x * 4 + warp;
+  if (E >= g.n_s) return;
+  const bool act = lane < N;
+  const size_t R = (size_t)g.n_s * N;
+  double* ts = tile[warp];
+  const double* L = A.blocks + (size_t)E * (1 + g.dim) * N * N;
+  for (int k = 0; k < N; ++k)
+    if (act) ts[k * 33 + lane] = L[k * N + lane];
+  double xk[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) xk[j] = (j < A.nh && act) ? A.hist[(size_t)A.hslot[j] * R + E * N + lane] : 0.0;
+  __syncwarp();
+  double wk[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) wk[j] = 0.0;
+  for (int i = 0; i < N; ++i) {   // W_j[lane] = sum_i L[i][lane] x_j[i]
+    const double lil = act ? ts[i * 33 + lane] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) wk[j] += lil * __shfl_sync(FULL, xk[j], i);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < A.nh && act) A.W[j * R + E * N + lane] = wk[j];
+  __syncwarp();
+  const double* Li = A.Linv + (size_t)E * N * N;
+  for (int k = 0; k < N; ++k)
+    if (act) ts[k * 33 + lane] = Li[k * N + lane];
+  const double bk = act ? A.rhs[E * N + lane] : 0.0;
+  __syncwarp();
+  double rbk = 0.0;   // (L^-1 b)[lane] = sum_k Linv[lane][k] b[k]
+  for (int k = 0; k < N; ++k) {
+    const double bkk = __shfl_sync(FULL, bk, k);
+    if (act) rbk += ts[lane * 33 + k] * bkk;
+  }
+  if (act) A.rb[E * N + lane] = rbk;
+}
+
+// warp per subdomain: V_j = W_j + sum_a U_a W_{E+a,j} (own part); U_a^T W_{E,j} -> TH[j][E+a][a]
+__global__ void __launch_bounds__(128) k_hist_spmv(HistArgs A) {
+  __shared__ double tile[4][32 * 33];
+  const Geo& g = A.g;
+  const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int E = blockIdx.x * 4 + warp;
+  if (E >= g.n_s) return;
+  const bool act = lane < N;
+  const size_t R = (size_t)g.n_s * N;
+  double* ts = tile[warp];
+  int C[3];
+  sub_xyz(g, E, C);
+  const double* Bd = A.blocks + (size_t)E * (1 + g.dim) * N * N;
+  double wE[8], v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    wE[j] = (j < A.nh && act) ? A.W[j * R + E * N + lane] : 0.0;
+    v[j] = wE[j];
+  }
+  for (int a = 0; a < g.dim; ++a) {
+    if (C[a] + 1 >= g.S[a]) continue;
+    const int En = E + g.Estride[a];
+    const double* U = Bd + (size_t)(1 + a) * N * N;
+    __syncwarp();
+    for (int k = 0; k < N; ++k)
+      if (act) ts[k * 33 + lane] = U[k * N + lane];
+    double wN[8], tT[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      wN[j] = (j < A.nh && act) ? A.W[j * R + En * N + lane] : 0.0;
+      tT[j] = 0.0;
+    }
+    __syncwarp();
+    for (int k = 0; k < N; ++k) {
+      const double col = act ? ts[k * 33 + lane] : 0.0;   // U[k][lane]
+      const double row = act ? ts[lane * 33 + k] : 0.0;   // U[lane][k]
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        tT[j] += col * __shfl_sync(FULL, wE[j], k);
+        v[j] += row * __shfl_sync(FULL, wN[j], k);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < A.nh && act) A.TH[((size_t)j * g.n_s * 3 + (size_t)En * 3 + a) * N + lane] = tT[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < A.nh && act) A.V[j * R + E * N + lane] = v[j];
+}
+
+// complete V (lower hand-overs), Gram partials G_ij = W_i.V_j (i <= j) and g_i = W_i.rb per CTA
+__global__ void __launch_bounds__(256) k_hist_gram(HistArgs A) {
+  __shared__ double red[44][8];
+  const Geo& g = A.g;
+  const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int E = blockIdx.x * 8 + warp;
+  const bool act = lane < N;
+  const size_t R = (size_t)g.n_s * N;
+  double gp[44];
+#pragma unroll
+  for (int q = 0; q < 44; ++q) gp[q] = 0.0;
+  if (E < g.n_s) {
+    int C[3];
+    sub_xyz(g, E, C);
+    double wv[8], vv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      wv[j] = 0.0; vv[j] = 0.0;
+      if (j < A.nh && act) {
+        wv[j] = A.W[j * R + E * N + lane];
+        double v = A.V[j * R + E * N + lane];
+        for (int a = 0; a < g.dim; ++a)
+          if (C[a] > 0) v += A.TH[((size_t)j * g.n_s * 3 + (size_t)E * 3 + a) * N + lane];
+        vv[j] = v;
+        A.V[j * R + E * N + lane] = v;
+      }
+    }
+    const double rbk = act ? A.rb[E * N + lane] : 0.0;
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = i; j < 8; ++j) {
+        if (j < A.nh) gp[q] = warp_sum(wv[i] * vv[j]);
+        ++q;
+      }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < A.nh) gp[36 + i] = warp_sum(wv[i] * rbk);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 44; ++q) red[q][warp] = gp[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < 44) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+    A.gpart[threadIdx.x * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// Solve of one PCG run's setup (out of line: its register pressure stays out of the iteration
+// loop): alpha from the Gram partials, y0 = W alpha, r0 = rb - V alpha, ||rb||^2, ||r0||^2, Zh^T r0.
+__device__ __noinline__ void pcg_initial_guess(const PcgArgs& A, cg::grid_group& grid, double (*red)[32],
+                                               double& bb_out, double& rr_out) {
+  const Geo& g = A.g;
+  const int N = g.N;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int TW = gridDim.x * W, gw = blockIdx.x * W + warp;
+  const bool act = lane < N;
+  const int nh = A.nh;
+  const size_t R = (size_t)g.n_s * N;
+  double alpha_h[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) alpha_h[j] = 0.0;
+  if (nh > 0) {
+    auto gsum = [&](int q) {   // fixed-order sum of the k_hist_gram partials (same in every warp)
+      double s = 0.0;
+      for (int b = lane; b < A.ngram; b += 32) s += A.gpart[q * A.ngram + b];
+      return warp_sum(s);
+    };
+    double G[8][8], rhs8[8];
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = i; j < 8; ++j) {
+        const double v = (j < nh) ? gsum(q) : 0.0;
+        G[i][j] = v; G[j][i] = v;
+        ++q;
+      }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) rhs8[i] = i < nh ? gsum(36 + i) : 0.0;
+    bool keep[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      keep[k] = k < nh && G[k][k] > 1e-12 * fabs(G[0][0]) && G[k][k] > 0.0;
+      if (keep[k]) {
+        const double piv = G[k][k];
+#pragma unroll
+        for (int i = k + 1; i < 8; ++i) {
+          const double f = G[i][k] / piv;
+#pragma unroll
+          for (int j = k; j < 8; ++j) G[i][j] -= f * G[k][j];
+          rhs8[i] -= f * rhs8[k];
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 7; k >= 0; --k) {
+      if (k < nh && keep[k]) {
+        double v = rhs8[k];
+#pragma unroll
+        for (int j = k + 1; j < 8; ++j) v -= G[k][j] * alpha_h[j];
+        alpha_h[k] = v / G[k][k];
+      }
+    }
+  }
+  double pbb = 0.0, prr = 0.0;
+  for (int E = gw; E < g.n_s; E += TW) {
+    const double rbk = act ? A.rb[E * N + lane] : 0.0;
+    double yk = 0.0, rk = rbk;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nh && act) {
+        yk += alpha_h[j] * A.W[j * R + E * N + lane];
+        rk -= alpha_h[j] * A.V[j * R + E * N + lane];
+      }
+    if (act) {
+      A.y[E * N + lane] = yk;
+      A.r[E * N + lane] = rk;
+    }
+    pbb += warp_sum(rbk * rbk);
+    prr += warp_sum(rk * rk);
+    const double w = warp_sum(act ? A.zh[E * N + lane] * rk : 0.0);
+    if (lane == 0) A.wc[E] = w;
+  }
+  cta_partial(pbb, red, A.partials, 0);
+  cta_partial(prr, red, A.partials, 1);
+  grid.sync();
+  bb_out = grid_total(A.partials, 0);
+  rr_out = grid_total(A.partials, 1);
 }
 
 __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
@@ -333,60 +598,8 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
     }
   };
 
-  // ---- warm start (original variables, history kept) and transform: y0 = L^T x0, rb = L^-1 b
-  double pbb = 0.0;
-  for (int E = gw; E < g.n_s; E += TW) {
-    double xk = 0.0;
-    if (act) {
-      const double xn = A.x[E * N + lane], xp = A.xprev[E * N + lane];
-      A.xprev[E * N + lane] = xn;
-      xk = A.extrap ? 2.0 * xn - xp : xn;
-    }
-    const double* L = A.blocks + (size_t)E * (1 + g.dim) * N * N;
-    double yk = 0.0;   // (L^T x)[lane] = sum_i L[i][lane] x[i]
-    for (int i = 0; i < N; ++i) {
-      const double xi = __shfl_sync(FULL, xk, i);
-      if (act) yk += L[i * N + lane] * xi;
-    }
-    // rb = L^-1 b by a reduce-scatter over rows of L^-1
-    const double bk = act ? A.rhs[E * N + lane] : 0.0;
-    const double* Li = A.Linv + (size_t)E * N * N;
-    double w[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) w[i] = (i < N && act) ? Li[i * N + lane] * bk : 0.0;
-    const double rbk = reduce_scatter32(w, lane);
-    if (act) {
-      A.y[E * N + lane] = yk;
-      A.r[E * N + lane] = rbk;   // r holds rb until the residual is formed
-    }
-    pbb += warp_sum(act ? rbk * rbk : 0.0);
-  }
-  cta_partial(pbb, red, A.partials, 0);
-  grid.sync();
-  const double bb = grid_total(A.partials, 0);
-  // ---- r = rb - Bh y0, ||r||^2, Zh^T r
-  double dummy = 0.0;
-  for (int E = gw; E < g.n_s; E += TW) {
-    int C[3];
-    sub_xyz(g, E, C);
-    auto yload = [&](int Ep) { return act ? A.y[Ep * N + lane] : 0.0; };
-    const double q = spmv_part(A, E, C, lane, yload(E), yload, dummy);
-    if (act) A.qp[E * N + lane] = q;
-  }
-  grid.sync();
-  double prr = 0.0;
-  for (int E = gw; E < g.n_s; E += TW) {
-    int C[3];
-    sub_xyz(g, E, C);
-    const double rk = act ? A.r[E * N + lane] - (A.qp[E * N + lane] + lower_contrib(A, E, C, lane)) : 0.0;
-    if (act) A.r[E * N + lane] = rk;
-    prr += warp_sum(rk * rk);
-    const double w = warp_sum(act ? A.zh[E * N + lane] * rk : 0.0);
-    if (lane == 0) A.wc[E] = w;
-  }
-  cta_partial(prr, red, A.partials, 1);
-  grid.sync();
-  double rr = grid_total(A.partials, 1);
+  double bb, rr;
+  pcg_initial_guess(A, grid, red, bb, rr);
   const double tol2 = A.rtol * A.rtol * bb;
   int it = 0;
   if (!(rr <= tol2) && bb > 0.0) {
@@ -434,7 +647,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       }
       const double alpha = rz / pq;
       // B: y, r, ||r||^2, Zh^T r
-      prr = 0.0;
+      double prr = 0.0;
       for (int E = gw; E < g.n_s; E += TW) {
         int C[3];
         sub_xyz(g, E, C);
@@ -482,7 +695,10 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       const double yi = __shfl_sync(FULL, yk, i);
       if (act) xk += Li[i * N + lane] * yi;
     }
-    if (act) A.x[E * N + lane] = xk;
+    if (act) {
+      A.x[E * N + lane] = xk;
+      A.hist_out[E * N + lane] = xk;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.iters[0] = it;

@@ -51,7 +51,7 @@ __device__ __forceinline__ int pair_tj(int p) {
   return p < 4 ? p : p < 7 ? p - 3 : p < 9 ? p - 5 : 3;
 }
 
-__global__ void __launch_bounds__(256) k_project(ProjArgs A) {
+__global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   extern __shared__ __align__(16) double sm[];
   const Geo& g = A.g;
   const int N = g.N, nl = g.n_loc, E = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) k_project(ProjArgs A) {
   }
   // deterministic cross-warp reduction, one tile pair at a time; mirror for exact symmetry
   double* BEE = A.blocks + (size_t)E * nb1 * N * N;
-  double* red = Ys;  // [8][64]
+  double* red = Ys;  // [nwarp][64]
 #pragma unroll
   for (int p = 0; p < 10; ++p) {
     if (pair_tj(p) >= T) continue;

@@ -1,5 +1,5 @@
 """Solver-accuracy / cost sweep on one GPU (self-consistency; no oracle):
-run a config for its step count with several (rtol, extrapolate, coarse_refresh) settings and report
+run a config for its step count with several (rtol, history, coarse_refresh) settings and report
 PCG iterations per step, ms per step and max |s - s_ref|, ||c - c_ref||/||c_ref|| against the
 tightest setting."""
 import json
@@ -16,11 +16,9 @@ from paper_1405_2810_b200.lrbms import LrbmsContext  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else None
 settings = json.loads(sys.argv[3]) if len(sys.argv) > 3 else [
-    {"rtol": 1e-15, "extrapolate": 0, "coarse_refresh": 1},
-    {"rtol": 1e-14, "extrapolate": 0}, {"rtol": 1e-14, "extrapolate": 1},
-    {"rtol": 1e-13, "extrapolate": 1}, {"rtol": 1e-12, "extrapolate": 1},
-    {"rtol": 1e-11, "extrapolate": 1}, {"rtol": 1e-10, "extrapolate": 1},
-    {"rtol": 1e-12, "extrapolate": 1, "coarse_refresh": 50}, {"rtol": 1e-12, "extrapolate": 1, "coarse_refresh": 1},
+    {"rtol": 1e-15, "history": 0, "coarse_refresh": 1},
+    {"rtol": 1e-13, "history": 1}, {"rtol": 1e-13, "history": 2}, {"rtol": 1e-13, "history": 4},
+    {"rtol": 1e-13, "history": 8}, {"rtol": 1e-12, "history": 8}, {"rtol": 1e-11, "history": 8},
 ]
 sc = inputs.make_scenario(cfg)
 steps = steps or sc.n_steps
