@@ -88,9 +88,10 @@ typedef struct {
 /* Reduced-solve options (a3).  The solve is preconditioned CG on the block-Jacobi-scaled system
  * L^-1 B L^-T y = L^-1 r (B_EE = L_E L_E^T) with a coarse correction on the subdomain-indicator
  * coefficients, started from the B-optimal combination of the last `history` solutions (Galerkin
- * projection onto their span), iterated until ||L^-1 (r - B c)||_2 <= rtol ||L^-1 r||_2. */
+ * projection onto their span), iterated until the preconditioned residual sqrt(rh.M^-1 rh) of the
+ * scaled system is <= rtol ||L^-1 r||_2 (rh = L^-1 (r - B c); an energy-norm error proxy). */
 typedef struct {
-  double rtol;            /* default 1e-13 */
+  double rtol;            /* default 1e-12, on sqrt(r.M^-1 r) relative to ||L^-1 b|| */
   int32_t max_iters;      /* default 5000 */
   int32_t coarse_refresh; /* rebuild the coarse-level inverse every k steps (default 50; 1 = every step) */
   int32_t use_coarse;     /* 1 (default) = two-level, 0 = block-Jacobi only */

@@ -268,6 +268,7 @@ struct FluxArgs {
   const double* phiV;   // phi * V or nullptr (phi = 1)
   const double2* fc;    // [n][3] static face coefficients
   double* s_out;
+  double* netw;         // [n] outward fractional-flow flux sum_F F f(chi(s)) per cell (a6 input)
   unsigned long long* dt_bits;
   double* dt_log;       // [steps] or nullptr
   double* t_acc;        // simulated time
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
   const int E = blockIdx.x, nl = g.n_loc;
   double* opos = sm;
   double* oneg = sm + nl;
+  double* netw = sm + 2 * nl;
   __shared__ double redmin[32];
   int C[3];
   sub_xyz(g, E, C);
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
     local_xyz(g, l, c);
     const double sl = A.s[base + l], pl = A.p[base + l];
     const double ll = total_mobility(A.f, sl);
-    double pos = 0.0, neg = 0.0;
+    double pos = 0.0, neg = 0.0, acc = 0.0;
     for (int a = 0; a < g.dim; ++a)
       for (int dir = -1; dir <= 1; dir += 2) {
         const int nb = neighbour(g, E, C, l, c, a, dir);
@@ -334,6 +336,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
         const double F = out_flux(A, a, dir, base + l, ll, pl, sl, nb, fw);
         pos += fmax(F, 0.0);
         neg += fmax(-F, 0.0);
+        acc += fw;
         if (A.face_flux && dir > 0) {
           const int i = C[0] * g.s[0] + c[0], j = C[1] * g.s[1] + c[1], k = C[2] * g.s[2] + c[2];
           A.face_flux[face_index(g, i, j, k, a)] = F;
@@ -341,6 +344,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
       }
     opos[l] = pos;
     oneg[l] = neg;
+    netw[l] = acc;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -350,12 +354,15 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
       const double F = A.L.gK[q] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
       opos[l] += fmax(F, 0.0);
       oneg[l] += fmax(-F, 0.0);
+      const double s_up = F >= 0.0 ? sl : A.L.s_ext[q];
+      netw[l] += F * frac_flow(A.f, s_up);
       if (A.link_flux) A.link_flux[A.L.orig[q]] = F;
     }
   }
   __syncthreads();
   double mn = INFINITY;
   for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    A.netw[base + l] = netw[l];
     const double Q = fmax(opos[l], oneg[l]);
     if (Q > 0.0) {
       const double pv = A.phiV ? A.phiV[base + l] : g.vol;
@@ -374,54 +381,23 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
   }
 }
 
-// a6: s^{n+1}_i = s^n_i - dt/(phi_i V) sum_F F_F^{out} f(chi(s^n))  (eq:saturationDG at k = 0, A5)
-__global__ void __launch_bounds__(512) k_transport(FluxArgs A) {
-  extern __shared__ double sm[];
+// a6: s^{n+1}_i = s^n_i - dt/(phi_i V) sum_F F_F^{out} f(chi(s^n))  (eq:saturationDG at k = 0, A5);
+// the flux sums were formed by k_flux_cfl (one flux evaluation per face side per step)
+__global__ void __launch_bounds__(256) k_transport(FluxArgs A) {
   const Geo& g = A.g;
-  const int E = blockIdx.x, nl = g.n_loc;
-  double* net = sm;
-  int C[3];
-  sub_xyz(g, E, C);
-  const size_t base = (size_t)E * nl;
   double dt = A.dt_fixed;
   if (!(dt > 0.0)) {
     const unsigned long long bits = *((volatile unsigned long long*)A.dt_bits);
     dt = __longlong_as_double((long long)bits);
   }
-  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-    int c[3];
-    local_xyz(g, l, c);
-    const double sl = A.s[base + l], pl = A.p[base + l];
-    const double ll = total_mobility(A.f, sl);
-    double acc = 0.0;
-    for (int a = 0; a < g.dim; ++a)
-      for (int dir = -1; dir <= 1; dir += 2) {
-        const int nb = neighbour(g, E, C, l, c, a, dir);
-        if (nb < 0) continue;
-        double fw;
-        out_flux(A, a, dir, base + l, ll, pl, sl, nb, fw);
-        acc += fw;
-      }
-    net[l] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
-      const int l = A.L.local[q];
-      const double sl = A.s[base + l];
-      const double F = A.L.gK[q] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
-      const double s_up = F >= 0.0 ? sl : A.L.s_ext[q];
-      net[l] += F * frac_flow(A.f, s_up);
-    }
-  }
-  __syncthreads();
-  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-    const double pv = A.phiV ? A.phiV[base + l] : g.vol;
-    const double sn = A.s[base + l] - dt / pv * net[l];
-    A.s_out[base + l] = sn;
+  const size_t n = g.n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double pv = A.phiV ? A.phiV[i] : g.vol;
+    const double sn = A.s[i] - dt / pv * A.netw[i];
+    A.s_out[i] = sn;
     if (!(sn == sn)) atomicOr(A.flags, FLAG_NAN);
   }
-  if (E == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (!(dt < INFINITY)) atomicOr(A.flags, FLAG_NOFLOW);
     *A.t_acc += dt;
     A.t_acc[1] = dt;
@@ -448,13 +424,13 @@ struct lrbms_ctx {
   std::vector<int> h_sub_start, h_local, h_orig;
   std::vector<double> h_geo2, h_p, h_s;
   double fpmax = 0.0;
-  lrbms_solver_opts opts{1e-13, 5000, 50, 1, 8};
+  lrbms_solver_opts opts{1e-12, 5000, 50, 1, 8};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
   ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
-  Buf K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
+  Buf netw, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
       Binv32, partials, scal,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
@@ -703,6 +679,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   const size_t n = g.n, R = (size_t)g.n_s * g.N;
   alloc(c->K, n * 8); alloc(c->fc, n * 3 * 16); alloc(c->l_gK, 8 * (size_t)nl); alloc(c->phiV, n * 8); alloc(c->s0, n * 8); alloc(c->s1, n * 8); alloc(c->p, n * 8);
   alloc(c->tmp, n * 8);
+  alloc(c->netw, n * 8);
   alloc(c->Phi, (size_t)g.n_s * g.N * g.n_loc * 8);
   alloc(c->zc, R * 8);
   alloc(c->blocks, (size_t)g.n_s * (1 + g.dim) * g.N * g.N * 8);
@@ -755,8 +732,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   if (occ < 1) return fail(c, LRBMS_E_CUDA, "GJ kernel cannot be resident");
   c->gj_G = sms * std::min(occ, 2);
   CUDA_TRY(c, cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
-  CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * c->g.n_loc));
-  CUDA_TRY(c, cudaFuncSetAttribute(k_transport, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * c->g.n_loc));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
   // link tables
   const Geo& g = c->g;
   CUDA_TRY(c, cudaMemcpyAsync(c->at<int>(c->l_start), c->h_sub_start.data(), 4 * (g.n_s + 1), cudaMemcpyHostToDevice, c->stream));
@@ -994,6 +970,7 @@ static FluxArgs flux_args(lrbms_ctx* c, double cfl, double dt_fixed, double* dt_
   A.phiV = c->have_phi ? c->at<double>(c->phiV) : nullptr;
   A.fc = c->at<double2>(c->fc);
   A.s_out = c->s_nxt();
+  A.netw = c->at<double>(c->netw);
   A.dt_bits = (unsigned long long*)c->at<double>(c->scal);
   A.t_acc = c->at<double>(c->scal) + 1;
   A.dt_log = dt_log;
@@ -1012,12 +989,12 @@ static lrbms_status launch_transport(lrbms_ctx* c, double cfl, double dt_fixed, 
   A.link_flux = link_flux;
   {
     StageScope sc_(c, 5);
-    k_flux_cfl<<<g.n_s, nt, 2 * 8 * g.n_loc, c->stream>>>(A);
+    k_flux_cfl<<<g.n_s, nt, 3 * 8 * g.n_loc, c->stream>>>(A);
     LAUNCH_CHECK(c);
   }
   {
     StageScope sc_(c, 6);
-    k_transport<<<g.n_s, nt, 8 * g.n_loc, c->stream>>>(A);
+    k_transport<<<std::min(cdiv(g.n, 256), 148 * 8), 256, 0, c->stream>>>(A);
     LAUNCH_CHECK(c);
   }
   c->cur ^= 1;

@@ -600,9 +600,11 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
 
   double bb, rr;
   pcg_initial_guess(A, grid, red, bb, rr);
+  // stopping test on the preconditioned residual r.M^-1 r (an energy-norm error proxy that weights
+  // the smooth, coarse-level residual components), relative to ||L^-1 b||^2 <= b.M^-1 b
   const double tol2 = A.rtol * A.rtol * bb;
   int it = 0;
-  if (!(rr <= tol2) && bb > 0.0) {
+  if (!(rr <= 0.0) && bb > 0.0) {
     double prz = 0.0;
     stage_wc();
     for (int E = gw; E < g.n_s; E += TW) {
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
     grid.sync();
     double rz = grid_total(A.partials, 2);
     double beta = 0.0;
-    for (it = 1; it <= A.max_iters; ++it) {
+    for (it = (rz <= tol2) ? A.max_iters + 2 : 1; it <= A.max_iters; ++it) {
       double* pcur = (it & 1) ? A.pb1 : A.pb0;
       const double* pold = (it & 1) ? A.pb0 : A.pb1;
       const bool first = it == 1;
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       grid.sync();
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
       rr = grid_total(A.partials, 1);
-      if (rr <= tol2) break;
+      if (!(rr > 0.0)) break;   // exact solution (or NaN, flagged below)
       // C: z = M^-1 r, r.z
       double prz2 = 0.0;
       if (A.use_coarse)
@@ -682,9 +684,11 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       grid.sync();
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
       const double rz_new = grid_total(A.partials, 2);
+      if (rz_new <= tol2) break;
       beta = rz_new / rz;
       rz = rz_new;
     }
+    if (it == A.max_iters + 2) it = 0;   // converged at the initial guess
   }
   // ---- back-transform c = L^-T y (per subdomain; no barrier needed)
   for (int E = gw; E < g.n_s; E += TW) {
