@@ -89,6 +89,16 @@ __global__ void k_link_coef(Geo g, Links L, const double* __restrict__ K, double
   for (int q = L.sub_start[E]; q < L.sub_start[E + 1]; ++q) gK[q] = L.geo2[q] * K[(size_t)E * g.n_loc + L.local[q]];
 }
 
+// a1 for a saturation written outside the step (set_saturation, run_host input)
+__global__ void k_mobility(Geo g, Flu f, const double* __restrict__ s, double* __restrict__ lam, double* __restrict__ fw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  double lw, lo;
+  mobilities(f, s[i], lw, lo);
+  lam[i] = lw + lo;
+  fw[i] = lw / (lw + lo);
+}
+
 // zc[E][k] = sum_l Phi[E][k][l]: coefficients of the subdomain indicator 1_E (coarse space)
 __global__ void k_basis_indicator(Geo g, const double* __restrict__ Phi, double* __restrict__ zc) {
   int E = blockIdx.x;
@@ -269,6 +279,10 @@ struct FluxArgs {
   const double2* fc;    // [n][3] static face coefficients
   double* s_out;
   double* netw;         // [n] outward fractional-flow flux sum_F F f(chi(s)) per cell (a6 input)
+  const double* lam;    // [n] lambda_t(s^n) (a1, formed once per step by the previous transport)
+  const double* fw;     // [n] f_w(s^n)
+  double* lam_out;      // [n] lambda_t(s^{n+1}) written by the transport
+  double* fw_out;
   unsigned long long* dt_bits;
   double* dt_log;       // [steps] or nullptr
   double* t_acc;        // simulated time
@@ -284,21 +298,18 @@ struct FluxArgs {
 // flux on the face between this cell and its neighbour nb along axis a (dir = +-1); returns the
 // flux leaving this cell and, in fwout, the fractional-flow-weighted flux leaving it.
 __device__ __forceinline__ double out_flux(const FluxArgs& A, int a, int dir, size_t gl, double ll, double pl,
-                                           double sl, int nb, double& fwout) {
-  const double sn = A.s[nb];
-  const double ln = total_mobility(A.f, sn);
+                                           double fl, int nb, double& fwout) {
+  const double ln = A.lam[nb];
   const double pn = A.p[nb];
-  double F, s_up;
-  if (dir > 0) {   // this = T1, nb = T2: F = w (p1 - p2), leaving this cell
+  double F;
+  if (dir > 0) {   // this = T1, nb = T2: F = w (p1 - p2), leaving this cell; upwind chi (eq:upwind)
     F = face_w(A.fc[gl * 3 + a], ll, ln) * (pl - pn);
-    s_up = F >= 0.0 ? sl : sn;
-    fwout = F * frac_flow(A.f, s_up);
+    fwout = F * (F >= 0.0 ? fl : A.fw[nb]);
     return F;
   }
   // nb = T1, this = T2: F = w (p1 - p2) leaves T1, i.e. -F leaves this cell
   F = face_w(A.fc[(size_t)nb * 3 + a], ln, ll) * (pn - pl);
-  s_up = F >= 0.0 ? sn : sl;
-  fwout = -(F * frac_flow(A.f, s_up));
+  fwout = -(F * (F >= 0.0 ? A.fw[nb] : fl));
   return -F;
 }
 
@@ -325,15 +336,14 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
   for (int l = threadIdx.x; l < nl; l += blockDim.x) {
     int c[3];
     local_xyz(g, l, c);
-    const double sl = A.s[base + l], pl = A.p[base + l];
-    const double ll = total_mobility(A.f, sl);
+    const double pl = A.p[base + l], ll = A.lam[base + l], fl = A.fw[base + l];
     double pos = 0.0, neg = 0.0, acc = 0.0;
     for (int a = 0; a < g.dim; ++a)
       for (int dir = -1; dir <= 1; dir += 2) {
         const int nb = neighbour(g, E, C, l, c, a, dir);
         if (nb < 0) continue;
         double fw;
-        const double F = out_flux(A, a, dir, base + l, ll, pl, sl, nb, fw);
+        const double F = out_flux(A, a, dir, base + l, ll, pl, fl, nb, fw);
         pos += fmax(F, 0.0);
         neg += fmax(-F, 0.0);
         acc += fw;
@@ -351,11 +361,10 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
     for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
       const int l = A.L.local[q];
       const double sl = A.s[base + l];
-      const double F = A.L.gK[q] * total_mobility(A.f, sl) * (A.p[base + l] - A.L.p[q]);
+      const double F = A.L.gK[q] * A.lam[base + l] * (A.p[base + l] - A.L.p[q]);
       opos[l] += fmax(F, 0.0);
       oneg[l] += fmax(-F, 0.0);
-      const double s_up = F >= 0.0 ? sl : A.L.s_ext[q];
-      netw[l] += F * frac_flow(A.f, s_up);
+      netw[l] += F * (F >= 0.0 ? A.fw[base + l] : frac_flow(A.f, A.L.s_ext[q]));
       if (A.link_flux) A.link_flux[A.L.orig[q]] = F;
     }
   }
@@ -395,6 +404,10 @@ __global__ void __launch_bounds__(256) k_transport(FluxArgs A) {
     const double pv = A.phiV ? A.phiV[i] : g.vol;
     const double sn = A.s[i] - dt / pv * A.netw[i];
     A.s_out[i] = sn;
+    double lw, lo;
+    mobilities(A.f, sn, lw, lo);   // a1 of the next step, formed once
+    A.lam_out[i] = lw + lo;
+    A.fw_out[i] = lw / (lw + lo);
     if (!(sn == sn)) atomicOr(A.flags, FLAG_NAN);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -430,7 +443,7 @@ struct lrbms_ctx {
   ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
-  Buf netw, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
+  Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
       Binv32, partials, scal,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
@@ -460,6 +473,10 @@ struct lrbms_ctx {
   T* at(const Buf& b) const { return reinterpret_cast<T*>(ws + b.off); }
   double* s_cur() const { return at<double>(cur ? s1 : s0); }
   double* s_nxt() const { return at<double>(cur ? s0 : s1); }
+  double* lam_cur() const { return at<double>(cur ? lam1 : lam0); }
+  double* lam_nxt() const { return at<double>(cur ? lam0 : lam1); }
+  double* fw_cur() const { return at<double>(cur ? fw1 : fw0); }
+  double* fw_nxt() const { return at<double>(cur ? fw0 : fw1); }
 };
 
 static lrbms_status fail(lrbms_ctx* c, lrbms_status st, const char* fmt, ...) {
@@ -680,6 +697,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->K, n * 8); alloc(c->fc, n * 3 * 16); alloc(c->l_gK, 8 * (size_t)nl); alloc(c->phiV, n * 8); alloc(c->s0, n * 8); alloc(c->s1, n * 8); alloc(c->p, n * 8);
   alloc(c->tmp, n * 8);
   alloc(c->netw, n * 8);
+  alloc(c->lam0, n * 8); alloc(c->lam1, n * 8); alloc(c->fw0, n * 8); alloc(c->fw1, n * 8);
   alloc(c->Phi, (size_t)g.n_s * g.N * g.n_loc * 8);
   alloc(c->zc, R * 8);
   alloc(c->blocks, (size_t)g.n_s * (1 + g.dim) * g.N * g.N * 8);
@@ -807,6 +825,8 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
   c->cur = 0;
   k_to_internal<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, s, c->s_cur());
   LAUNCH_CHECK(c);
+  k_mobility<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, c->f, c->s_cur(), c->lam_cur(), c->fw_cur());
+  LAUNCH_CHECK(c);
   CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->c), 0, c->c.bytes, c->stream));
   c->solves = 0;
   c->hist_count = 0;
@@ -861,7 +881,7 @@ static lrbms_status launch_project(lrbms_ctx* c) {
   ProjArgs A = c->proj;
   A.g = c->g; A.f = c->f; A.L = links_of(c);
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
-  A.fc = c->at<double2>(c->fc);
+  A.fc = c->at<double2>(c->fc); A.lam = c->lam_cur();
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs);
   k_project<<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
@@ -971,6 +991,7 @@ static FluxArgs flux_args(lrbms_ctx* c, double cfl, double dt_fixed, double* dt_
   A.fc = c->at<double2>(c->fc);
   A.s_out = c->s_nxt();
   A.netw = c->at<double>(c->netw);
+  A.lam = c->lam_cur(); A.fw = c->fw_cur(); A.lam_out = c->lam_nxt(); A.fw_out = c->fw_nxt();
   A.dt_bits = (unsigned long long*)c->at<double>(c->scal);
   A.t_acc = c->at<double>(c->scal) + 1;
   A.dt_log = dt_log;
@@ -1054,6 +1075,8 @@ lrbms_status lrbms_run_host(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
   if (s_in) {
     CUDA_TRY(c, cudaMemcpyAsync(tmp, s_in, 8 * (size_t)g.n, cudaMemcpyHostToDevice, c->stream));
     k_to_internal<<<nb, 256, 0, c->stream>>>(g, tmp, c->s_cur());
+    LAUNCH_CHECK(c);
+    k_mobility<<<nb, 256, 0, c->stream>>>(g, c->f, c->s_cur(), c->lam_cur(), c->fw_cur());
     LAUNCH_CHECK(c);
   }
   st = lrbms_run(c, n_steps, cfl, dt_fixed, nullptr);

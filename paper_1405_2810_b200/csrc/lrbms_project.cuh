@@ -24,6 +24,7 @@ struct ProjArgs {
   const double* K;
   const double* Phi;
   const double2* fc;   // [n][3] static face coefficients
+  const double* lam;   // [n] lambda_t(s^n)
   double* blocks;
   double* rhs;
   int LD, nlp, NP, KC, LDY, nfmax, nfp, LDN;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
     for (int c1 = (k < N ? nl : 0) + lane; c1 < LD; c1 += 32) Phs[(size_t)k * LD + c1] = 0.0;
 
   // 2. a1: own mobilities
-  for (int l = tid; l < nl; l += nt) lam[l] = total_mobility(A.f, A.s[base + l]);
+  for (int l = tid; l < nl; l += nt) lam[l] = A.lam[base + l];
   __syncthreads();
   // 3. face weights (R2) from the static coefficients: diag_l = sum over all faces of l; wp = weight
   //    to the +a neighbour in E; wi = weight across the +a subdomain side
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
         d += face_w(A.fc[(base + l - st) * 3 + a], lam[l - st], ll);
       } else if (C[a] > 0) {
         const int nb = neighbour(g, E, C, l, c, a, -1);
-        d += face_w(A.fc[(size_t)nb * 3 + a], total_mobility(A.f, A.s[nb]), ll);
+        d += face_w(A.fc[(size_t)nb * 3 + a], A.lam[nb], ll);
       }
       // +a neighbour
       if (c[a] + 1 < g.s[a]) {
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
         wp[a * nl + l] = w;
       } else if (C[a] + 1 < g.S[a]) {
         const int nb = neighbour(g, E, C, l, c, a, +1);
-        const double w = face_w(A.fc[(base + l) * 3 + a], ll, total_mobility(A.f, A.s[nb]));
+        const double w = face_w(A.fc[(base + l) * 3 + a], ll, A.lam[nb]);
         d += w;
         wi[a * A.nfmax + face_pos(g, c, a)] = w;
       }
