@@ -360,7 +360,6 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
   if (threadIdx.x == 0) {
     for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
       const int l = A.L.local[q];
-      const double sl = A.s[base + l];
       const double F = A.L.gK[q] * A.lam[base + l] * (A.p[base + l] - A.L.p[q]);
       opos[l] += fmax(F, 0.0);
       oneg[l] += fmax(-F, 0.0);

@@ -32,10 +32,3 @@ r = np.median(np.array(rows), axis=0) / 1e3
 print(f"iters {it}: median us  A-work {r[0]:.2f}  A-sync {r[1]:.2f}  B(work+sync) {r[2]:.2f}  C(work+sync) {r[3]:.2f}"
       f"  total {r.sum():.2f}")
 
-fr = []
-for i in range(2, min(it, 60)):
-    # 6: before pload, 0: spmv start, 1: after diag, 2..4: before coupling a, 5: spmv end; prev C sync end t[i-1,3]
-    fr.append((f[i, 6] - t[i - 1, 3], f[i, 0] - f[i, 6], f[i, 1] - f[i, 0], f[i, 3] - f[i, 2], f[i, 4] - f[i, 3],
-               f[i, 5] - f[i, 4], t[i, 0] - f[i, 5]))
-r = np.median(np.array(fr), axis=0) / 1e3
-print("warp0 of CTA0 (us): sync->loop %.2f  pload %.2f  diag %.2f  cpl0 %.2f  cpl1 %.2f  cpl2 %.2f  after-spmv->A-end %.2f" % tuple(r))
