@@ -158,9 +158,10 @@ lrbms_status lrbms_stage_transport(lrbms_ctx *ctx, double cfl, double dt_fixed,
 lrbms_status lrbms_get_stats(lrbms_ctx *ctx, lrbms_stats *out);
 
 /* Per-stage device timing with CUDA events on the bound stream (off by default).
- * Stages: 0 project (a1+a2), 1 coarse-level rebuild, 2 block-Jacobi inverses, 3 PCG (a3),
- * 4 reconstruction (a4), 5 flux + CFL (a5), 6 transport (a6).  Enabling resets the sums. */
-#define LRBMS_N_STAGES 7
+ * Stages: 0 project (a1+a2), 1 coarse-level rebuild, 2 block Cholesky + scaling of the couplings,
+ * 3 initial guess from the solution history, 4 PCG (a3), 5 reconstruction (a4), 6 flux + CFL (a5),
+ * 7 transport (a6).  Enabling resets the sums. */
+#define LRBMS_N_STAGES 8
 lrbms_status lrbms_set_profiling(lrbms_ctx *ctx, int32_t enable);
 /* ms[i] = accumulated device milliseconds, launches[i] = kernel launches of stage i, i < n. */
 lrbms_status lrbms_get_stage_times(lrbms_ctx *ctx, double *ms, int64_t *launches, int32_t n);

@@ -924,7 +924,6 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     LAUNCH_CHECK(c);
   }
   c->have_blocks = false;   // the blocks are now in scaled form
-  StageScope sc_(c, 3);
   PcgArgs A;
   A.g = g;
   A.blocks = c->at<double>(c->blocks); A.Linv = c->at<double>(c->Linv);
@@ -937,6 +936,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.hist_out = c->at<double>(c->hist) + (size_t)out_slot * R;
   A.W = c->at<double>(c->Wh); A.V = c->at<double>(c->Vh); A.rb = c->at<double>(c->rbv);
   {
+    StageScope sh_(c, 3);
     HistArgs H;
     H.g = g;
     H.blocks = c->at<double>(c->blocks); H.Linv = c->at<double>(c->Linv); H.rhs = c->at<double>(c->rhs);
@@ -962,6 +962,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
   A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
   A.tstamp = c->debug_tstamp;
+  StageScope sc_(c, 4);
   void* args[] = {&A};
   CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,
                                           c->stream));
@@ -973,7 +974,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
 }
 
 static lrbms_status launch_recon(lrbms_ctx* c) {
-  StageScope sc_(c, 4);
+  StageScope sc_(c, 5);
   const Geo& g = c->g;
   const int nt = std::min(1024, cdiv(g.n_loc, 32) * 32);
   k_recon<<<g.n_s, nt, 0, c->stream>>>(g, c->at<double>(c->Phi), c->at<double>(c->c), c->at<double>(c->p),
@@ -1008,12 +1009,12 @@ static lrbms_status launch_transport(lrbms_ctx* c, double cfl, double dt_fixed, 
   A.face_flux = face_flux;
   A.link_flux = link_flux;
   {
-    StageScope sc_(c, 5);
+    StageScope sc_(c, 6);
     k_flux_cfl<<<g.n_s, nt, 3 * 8 * g.n_loc, c->stream>>>(A);
     LAUNCH_CHECK(c);
   }
   {
-    StageScope sc_(c, 6);
+    StageScope sc_(c, 7);
     k_transport<<<std::min(cdiv(g.n, 256), 148 * 8), 256, 0, c->stream>>>(A);
     LAUNCH_CHECK(c);
   }

@@ -264,7 +264,7 @@ class LrbmsContext:
         self._check(self.L.lrbms_get_stats(self.h, ctypes.byref(st)))
         return {k: getattr(st, k) for k, _ in Stats._fields_}
 
-    STAGES = ["project", "coarse", "block_inverse", "pcg", "recon", "flux_cfl", "transport"]
+    STAGES = ["project", "coarse", "scale", "guess", "pcg", "recon", "flux_cfl", "transport"]
 
     def set_profiling(self, on: bool):
         self._check(self.L.lrbms_set_profiling(self.h, 1 if on else 0))

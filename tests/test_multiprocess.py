@@ -1,6 +1,7 @@
 """The N > 1 host path of bench.py (replicas, max-over-ranks timing) on CPU with gloo, world size 2."""
 import json
 import os
+import re
 import socket
 import subprocess
 import sys
@@ -41,7 +42,7 @@ def test_max_over_ranks_gloo(tmp_path):
            "--master-addr=127.0.0.1", f"--master-port={port}", str(script)]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
-    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    lines = [json.loads(m) for m in re.findall(r"\{[^{}]*\}", out.stdout)]   # ranks may share a line
     assert len(lines) == 2
     assert all(l["world"] == 2 and l["max"] == 2.0 for l in lines)
 
