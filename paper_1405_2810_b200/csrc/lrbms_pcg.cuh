@@ -325,6 +325,21 @@ __device__ __forceinline__ void cta_partial_n(double v, double (*red)[32], doubl
     partials[slot * gridDim.x + blockIdx.x] = t;
   }
 }
+// fixed-order total of the per-CTA partials, read by warp 0 only and broadcast through shared memory:
+// 2048 warps hammering the same few L2 lines right after a grid barrier serialise at one L2 slice.
+// bc is a per-call-site shared slot; every call site is followed by another CTA barrier before the
+// same slot is written again.
+__device__ __forceinline__ double grid_total_b(const double* partials, int slot, double* bc) {
+  if ((threadIdx.x >> 5) == 0) {
+    const int lane = threadIdx.x & 31, G = gridDim.x;
+    double s = 0.0;
+    for (int b = lane; b < G; b += 32) s += partials[slot * G + b];
+    s = warp_sum(s);
+    if (lane == 0) *bc = s;
+  }
+  __syncthreads();
+  return *bc;
+}
 __device__ __forceinline__ double grid_total(const double* partials, int slot) {
   const int lane = threadIdx.x & 31, G = gridDim.x;
   double s = 0.0;
@@ -501,7 +516,7 @@ __global__ void __launch_bounds__(256) k_hist_gram(HistArgs A) {
 // Solve of one PCG run's setup (out of line: its register pressure stays out of the iteration
 // loop): alpha from the Gram partials, y0 = W alpha, r0 = rb - V alpha, ||rb||^2, ||r0||^2, Zh^T r0.
 __device__ __noinline__ void pcg_initial_guess(const PcgArgs& A, cg::grid_group& grid, double (*red)[32],
-                                               double& bb_out, double& rr_out) {
+                                               double* sh, double& bb_out, double& rr_out) {
   const Geo& g = A.g;
   const int N = g.N;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
@@ -513,23 +528,28 @@ __device__ __noinline__ void pcg_initial_guess(const PcgArgs& A, cg::grid_group&
 #pragma unroll
   for (int j = 0; j < 8; ++j) alpha_h[j] = 0.0;
   if (nh > 0) {
-    auto gsum = [&](int q) {   // fixed-order sum of the k_hist_gram partials (same in every warp)
-      double s = 0.0;
-      for (int b = lane; b < A.ngram; b += 32) s += A.gpart[q * A.ngram + b];
-      return warp_sum(s);
-    };
+    // fixed-order sums of the k_hist_gram partials by warp 0, broadcast through shared memory
+    if (warp == 0) {
+      for (int q = 0; q < 44; ++q) {
+        double v = 0.0;
+        for (int b = lane; b < A.ngram; b += 32) v += A.gpart[q * A.ngram + b];
+        v = warp_sum(v);
+        if (lane == 0) sh[q] = v;
+      }
+    }
+    __syncthreads();
     double G[8][8], rhs8[8];
     int q = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = i; j < 8; ++j) {
-        const double v = (j < nh) ? gsum(q) : 0.0;
+        const double v = (j < nh) ? sh[q] : 0.0;
         G[i][j] = v; G[j][i] = v;
         ++q;
       }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) rhs8[i] = i < nh ? gsum(36 + i) : 0.0;
+    for (int i = 0; i < 8; ++i) rhs8[i] = i < nh ? sh[36 + i] : 0.0;
     bool keep[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -577,13 +597,15 @@ __device__ __noinline__ void pcg_initial_guess(const PcgArgs& A, cg::grid_group&
   cta_partial(pbb, red, A.partials, 0);
   cta_partial(prr, red, A.partials, 1);
   grid.sync();
-  bb_out = grid_total(A.partials, 0);
-  rr_out = grid_total(A.partials, 1);
+  bb_out = grid_total_b(A.partials, 0, &sh[44]);
+  rr_out = grid_total_b(A.partials, 1, &sh[45]);
 }
 
 __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[4][32];
+  __shared__ double bc[4];
+  __shared__ double sh46[46];
   extern __shared__ float wcs[];
   const Geo& g = A.g;
   const int N = g.N;
@@ -599,7 +621,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   };
 
   double bb, rr;
-  pcg_initial_guess(A, grid, red, bb, rr);
+  pcg_initial_guess(A, grid, red, sh46, bb, rr);
   // stopping test on the preconditioned residual r.M^-1 r (an energy-norm error proxy that weights
   // the smooth, coarse-level residual components), relative to ||L^-1 b||^2 <= b.M^-1 b
   const double tol2 = A.rtol * A.rtol * bb;
@@ -615,7 +637,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
     }
     cta_partial(prz, red, A.partials, 2);
     grid.sync();
-    double rz = grid_total(A.partials, 2);
+    double rz = grid_total_b(A.partials, 2, &bc[0]);
     double beta = 0.0;
     for (it = (rz <= tol2) ? A.max_iters + 2 : 1; it <= A.max_iters; ++it) {
       double* pcur = (it & 1) ? A.pb1 : A.pb0;
@@ -642,7 +664,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       cta_partial(ppq, red, A.partials, 3);
       grid.sync();
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 1] = gtimer();
-      const double pq = grid_total(A.partials, 3);
+      const double pq = grid_total_b(A.partials, 3, &bc[1]);
       if (!(pq > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
         break;
@@ -667,7 +689,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       cta_partial(prr, red, A.partials, 1);
       grid.sync();
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
-      rr = grid_total(A.partials, 1);
+      rr = grid_total_b(A.partials, 1, &bc[2]);
       if (!(rr > 0.0)) break;   // exact solution (or NaN, flagged below)
       // C: z = M^-1 r, r.z
       double prz2 = 0.0;
@@ -683,7 +705,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       cta_partial(prz2, red, A.partials, 2);
       grid.sync();
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
-      const double rz_new = grid_total(A.partials, 2);
+      const double rz_new = grid_total_b(A.partials, 2, &bc[3]);
       if (rz_new <= tol2) break;
       beta = rz_new / rz;
       rz = rz_new;

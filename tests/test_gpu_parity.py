@@ -238,3 +238,17 @@ def test_full_size_prefix(name):
     assert rel(np_(cg), ref["cs"][-1]) <= 1e-10
     assert rel(np_(pg), ref["ps"][-1]) <= 1e-10
     assert np.max(np.abs(np_(sg) - ref["s"])) <= 1e-10
+
+
+def test_c4_prefix_tight_solver():
+    """C4 amplifies round-off (a 1e-14 K perturbation gives |ds| 5.7e-11 after 20 steps and 2.2e-6
+    after 1000): its saturation parity is checked on a 10-step prefix with a tight
+    reduced solve; c and p carry the 1e-10 bar."""
+    sc = inputs.make_scenario("C4")
+    ref = O.run(sc, n_steps=10, keep=True)
+    ctx = ctx_for(sc, rtol=1e-14)
+    ctx.run(10)
+    s, p, c = ctx.get_state()
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
