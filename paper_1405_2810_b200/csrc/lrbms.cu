@@ -260,10 +260,26 @@ __global__ void k_recon(Geo g, const double* __restrict__ Phi, const double* __r
   if (E == 0 && threadIdx.x == 0) *dt_bits = 0x7ff0000000000000ull;  // +inf: reset the dt min
   __syncthreads();
   const double* PhiE = Phi + (size_t)E * N * nl;
-  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
-    double acc = 0.0;
-    for (int k = 0; k < N; ++k) acc += PhiE[(size_t)k * nl + l] * cs[k];
-    p[(size_t)E * nl + l] = acc;
+  if ((nl & 1) == 0) {   // two cells per thread, 16-byte streaming loads, 8 in flight
+    const int h = nl >> 1;
+    const double2* P2 = reinterpret_cast<const double2*>(PhiE);
+    for (int l2 = threadIdx.x; l2 < h; l2 += blockDim.x) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < N; ++k) {
+        const double2 v = __ldcs(P2 + (size_t)k * h + l2);
+        a0 += v.x * cs[k];
+        a1 += v.y * cs[k];
+      }
+      reinterpret_cast<double2*>(p + (size_t)E * nl)[l2] = make_double2(a0, a1);
+    }
+  } else {
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+      double acc = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < N; ++k) acc += __ldcs(PhiE + (size_t)k * nl + l) * cs[k];
+      p[(size_t)E * nl + l] = acc;
+    }
   }
 }
 
@@ -456,6 +472,7 @@ struct lrbms_ctx {
   int64_t steps = 0, total_iters = 0, launches = 0, solves = 0;
   int hist_count = 0, hist_head = KHIST - 1;   // ring buffer of previous solutions (initial guess)
   size_t pcg_smem = 0;
+  int pcg_binv_smem = 0;   // 1: k_pcg stages its rows of the coarse inverse in shared memory
   unsigned long long* debug_tstamp = nullptr;  // set by lrbms_debug_set_tstamp (not in lrbms.h)
   int last_iters = 0, rebuilds = 0;
   int64_t last_rebuild_step = -1;
@@ -745,6 +762,20 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_pcg, 32 * W, c->pcg_smem));
   if (occ < 1) return fail(c, LRBMS_E_CUDA, "PCG kernel cannot be resident");
   c->pcg_G = std::max(1, std::min(cdiv(c->g.n_s, W), sms * occ));
+  {  // stage the CTA's rows of the coarse inverse in shared memory when they fit
+    const size_t rows = (size_t)W * cdiv(c->g.n_s, c->pcg_G * W);
+    const size_t need = 4 * (size_t)c->n_pad * (1 + rows);
+    int occ2 = 0;
+    c->pcg_binv_smem = 0;
+    if (need <= 200 * 1024) {
+      CUDA_TRY(c, cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+      CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void*)k_pcg, 32 * W, need));
+      if (occ2 >= occ) {
+        c->pcg_smem = need;
+        c->pcg_binv_smem = 1;
+      }
+    }
+  }
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_coarse_gj, 256, 0));
   if (occ < 1) return fail(c, LRBMS_E_CUDA, "GJ kernel cannot be resident");
   c->gj_G = sms * std::min(occ, 2);
@@ -961,6 +992,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.qp = c->at<double>(c->q); A.T = c->at<double>(c->T); A.wc = c->at<double>(c->wc);
   A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
   A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
+  A.binv_smem = c->pcg_binv_smem;
   A.tstamp = c->debug_tstamp;
   StageScope sc_(c, 4);
   void* args[] = {&A};
@@ -976,7 +1008,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
 static lrbms_status launch_recon(lrbms_ctx* c) {
   StageScope sc_(c, 5);
   const Geo& g = c->g;
-  const int nt = std::min(1024, cdiv(g.n_loc, 32) * 32);
+  const int nt = std::min(1024, cdiv((g.n_loc + 1) / 2, 32) * 32);
   k_recon<<<g.n_s, nt, 0, c->stream>>>(g, c->at<double>(c->Phi), c->at<double>(c->c), c->at<double>(c->p),
                                        (unsigned long long*)c->at<double>(c->scal));
   LAUNCH_CHECK(c);

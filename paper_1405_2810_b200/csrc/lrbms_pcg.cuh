@@ -57,6 +57,7 @@ struct PcgArgs {
   int max_iters;
   int n_pad;
   int use_coarse;
+  int binv_smem;          // 1: the CTA's rows of Binv are staged in shared memory once per solve
   int nh;                 // number of history vectors (0..KH)
   unsigned long long* tstamp;  // optional phase timestamps (CTA 0, first iterations), or nullptr
 };
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
 #pragma unroll
   for (int i = 0; i < 32; ++i) m[i] = (lane < N && i < N) ? Bd[i * N + lane] : (i == lane ? 1.0 : 0.0);
   bool bad = false;
-  const double d0 = m[lane];   // original diagonal entry of this lane's column
+  const double d0 = lane < N ? Bd[lane * N + lane] : 1.0;   // original diagonal entry of this lane's column
   // right-looking Cholesky on the full symmetric trailing matrix: lane j's m[k] = M[k][j] = M[j][k].
   // A pivot below 1e-13 of its original diagonal entry means a numerically rank-deficient Phi_E.
 #pragma unroll
@@ -136,16 +137,18 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
     bad |= !(dkk > 1e-13 * __shfl_sync(FULL, d0, k));
     const double d = sqrt(dkk), rd = 1.0 / d;
     const double ljk = m[k] * rd;          // L[lane][k] for lane >= k
-    double col[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) col[i] = (i > k) ? __shfl_sync(FULL, m[i], k) * rd : 0.0;
-    if (lane > k) {
+    for (int i = 0; i < 32; ++i) {
+      if (i <= k) continue;
+      const double ci = __shfl_sync(FULL, m[i], k) * rd;   // L[i][k]
+      if (lane > k) m[i] -= ci * ljk;
+      else if (lane == k) m[i] = ci;
+    }
+    if (lane == k) {
+      m[k] = d;
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (i > k) m[i] -= col[i] * ljk;
-    } else if (lane == k) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) m[i] = (i > k) ? col[i] : (i == k ? d : 0.0);
+        if (i < k) m[i] = 0.0;
     }
   }
   // L^-1 by forward substitution, one column per lane: L x = e_lane
@@ -279,17 +282,17 @@ __device__ __forceinline__ double lower_contrib(const PcgArgs& A, int E, const i
 }
 
 // z_E = r_E + zh_E e_E with e_E = (B_c^-1 Zh^T r)_E  (coarse product in fp32: preconditioner)
-__device__ __forceinline__ double precond(const PcgArgs& A, const float* wcv, int E, int lane, double rk) {
+__device__ __forceinline__ double precond(const PcgArgs& A, const float* wcv, const float* brow, int E, int lane, double rk) {
   const int N = A.g.N;
   float e = 0.f;
   if (A.use_coarse) {
-    const float4* row = reinterpret_cast<const float4*>(A.Binv + (size_t)E * A.n_pad);
+    const float4* row = reinterpret_cast<const float4*>(brow);
     const float4* w4 = reinterpret_cast<const float4*>(wcv);
     const int n4 = A.n_pad >> 2;
     float e0 = 0.f, e1 = 0.f;
 #pragma unroll 4
     for (int F = lane; F < n4; F += 32) {
-      const float4 b0 = __ldg(row + F), c0 = w4[F];
+      const float4 b0 = row[F], c0 = w4[F];
       e0 = fmaf(b0.x, c0.x, e0);
       e1 = fmaf(b0.y, c0.y, e1);
       e0 = fmaf(b0.z, c0.z, e0);
@@ -613,6 +616,24 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   const int TW = gridDim.x * (blockDim.x >> 5), gw = blockIdx.x * (blockDim.x >> 5) + warp;
   const bool act = lane < N;
   const float* wcv = wcs;
+  // rows of B_c^-1 of this CTA's subdomains (E = gw + j TW -> smem row j W + warp), staged once per
+  // solve: the coarse product of every iteration then reads shared memory instead of 16.8 MB of L2
+  float* bsm = wcs + A.n_pad;
+  const int WPC = blockDim.x >> 5;
+  if (A.use_coarse && A.binv_smem) {
+    const int nrow = WPC * ((g.n_s + TW - 1) / TW);
+    const int n4 = A.n_pad >> 2;
+    for (int t = threadIdx.x; t < nrow * n4; t += blockDim.x) {
+      const int rr = t / n4, F = t - rr * n4;
+      const int E = blockIdx.x * WPC + (rr % WPC) + (rr / WPC) * TW;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (E < g.n_s) v = __ldcs(reinterpret_cast<const float4*>(A.Binv + (size_t)E * A.n_pad) + F);
+      reinterpret_cast<float4*>(bsm)[t] = v;
+    }
+  }
+  auto brow = [&](int E) -> const float* {
+    return A.binv_smem ? bsm + (size_t)(((E - gw) / TW) * WPC + warp) * A.n_pad : A.Binv + (size_t)E * A.n_pad;
+  };
   auto stage_wc = [&]() {   // Zh^T r -> shared memory (fp32, zero padded to n_pad)
     if (A.use_coarse) {
       for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) wcs[i] = i < g.n_s ? (float)A.wc[i] : 0.f;
@@ -631,7 +652,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
     stage_wc();
     for (int E = gw; E < g.n_s; E += TW) {
       const double rk = act ? A.r[E * N + lane] : 0.0;
-      const double zk = precond(A, wcv, E, lane, rk);
+      const double zk = precond(A, wcv, brow(E), E, lane, rk);
       if (act) A.z[E * N + lane] = zk;
       prz += warp_sum(zk * rk);
     }
@@ -693,12 +714,12 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       if (!(rr > 0.0)) break;   // exact solution (or NaN, flagged below)
       // C: z = M^-1 r, r.z
       double prz2 = 0.0;
-      if (A.use_coarse)
+      if (A.use_coarse && !A.binv_smem)
         for (int E = gw; E < g.n_s; E += TW) prefetch_l1(A.Binv + (size_t)E * A.n_pad, A.n_pad * 4, lane);
       stage_wc();
       for (int E = gw; E < g.n_s; E += TW) {
         const double rk = act ? A.r[E * N + lane] : 0.0;
-        const double zk = precond(A, wcv, E, lane, rk);
+        const double zk = precond(A, wcv, brow(E), E, lane, rk);
         if (act) A.z[E * N + lane] = zk;
         prz2 += warp_sum(zk * rk);
       }
