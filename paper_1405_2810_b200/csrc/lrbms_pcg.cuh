@@ -239,35 +239,98 @@ __global__ void __launch_bounds__(256) k_transform(Geo g, double* __restrict__ b
 
 // Part A of q = Bh v for subdomain E: returns lane's (v_E + sum_a U_a v_{E+a}); stores U_a^T v_E
 // into T[E+a][a]; adds v_E.v_E + 2 v_E.(U_a v_{E+a}) (lane-local) to vbv.
+//
+// Register tiling of a 32 x 32 block: lane l = 4 a + b holds U[4a + i][b + 4j] (i < 4, j < 8): its
+// four rows R(a) = {4a..4a+3} and eight columns C(b) = {b, b+4, .., b+28}.  U v is then a 4-lane
+// reduce-scatter (rows) and U^T v an 8-lane one (columns), and both land on lane l = coefficient l:
+// 10 fp64 shuffles per block instead of 63 for the row-per-load layout.  Every load instruction
+// reads 8 rows x 32 contiguous bytes (full sectors).  sv is the warp's 2 x 32-double staging slot.
 template <class VF>
 __device__ __forceinline__ double spmv_part(const PcgArgs& A, int E, const int C[3], int lane, double vE,
-                                            VF vload, double& vbv) {
+                                            VF vload, double& vbv, double* sv) {
   const Geo& g = A.g;
   const int N = g.N, nb1 = 1 + g.dim;
   const double* Bd = A.blocks + (size_t)E * nb1 * N * N;
   const bool act = lane < N;
+  const int ra = (lane >> 2) * 4, cb = lane & 3;
   double acc = vE;
   double local = vE * vE;
-  double buf[32];
+  sv[lane] = vE;
+  __syncwarp();
+  double vr[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) vr[i] = sv[ra + i];
   for (int a = 0; a < g.dim; ++a) {
     if (C[a] + 1 >= g.S[a]) continue;
     const int En = E + g.Estride[a];
     const double vN = vload(En);
     const double* U = Bd + (size_t)(1 + a) * N * N;
-    for (int b = a + 1; b < g.dim; ++b)        // the next existing coupling block into L1
-      if (C[b] + 1 < g.S[b]) { prefetch_l1(Bd + (size_t)(1 + b) * N * N, N * N * 8, lane); break; }
+    double u[4][8];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) buf[k] = (k < N && act) ? __ldg(U + k * N + lane) : 0.0;
-    double tT = 0.0;  // (U^T v_E)[lane] = sum_k U[k][lane] v_E[k]
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int k = 0; k < 32; ++k) tT += buf[k] * __shfl_sync(FULL, vE, k);
+      for (int j = 0; j < 8; ++j) {
+        const int r = ra + i, c = cb + 4 * j;
+        u[i][j] = (r < N && c < N) ? __ldg(U + r * N + c) : 0.0;
+      }
+    __syncwarp();
+    sv[32 + lane] = vN;
+    __syncwarp();
+    double pu[4], pt[8];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) buf[k] *= vN;
-    const double tU = reduce_scatter32(buf, lane);   // (U v_{E+a})[lane]
+    for (int j = 0; j < 8; ++j) pt[j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pu[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double vc = sv[32 + cb + 4 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        pu[i] = fma(u[i][j], vc, pu[i]);
+        pt[j] = fma(u[i][j], vr[i], pt[j]);
+      }
+    }
+    // rows: reduce-scatter over lane bits 1, 0 -> lane keeps row ra + cb = lane
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const bool hi = lane & 2;
+      const double send = hi ? pu[i] : pu[i + 2];
+      const double keep = hi ? pu[i + 2] : pu[i];
+      pu[i] = keep + __shfl_xor_sync(FULL, send, 2);
+    }
+    {
+      const bool hi = lane & 1;
+      const double send = hi ? pu[0] : pu[1];
+      const double keep = hi ? pu[1] : pu[0];
+      pu[0] = keep + __shfl_xor_sync(FULL, send, 1);
+    }
+    // columns: reduce-scatter over lane bits 4, 3, 2 -> lane keeps column cb + 4 (lane >> 2) = lane
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool hi = lane & 16;
+      const double send = hi ? pt[j] : pt[j + 4];
+      const double keep = hi ? pt[j + 4] : pt[j];
+      pt[j] = keep + __shfl_xor_sync(FULL, send, 16);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const bool hi = lane & 8;
+      const double send = hi ? pt[j] : pt[j + 2];
+      const double keep = hi ? pt[j + 2] : pt[j];
+      pt[j] = keep + __shfl_xor_sync(FULL, send, 8);
+    }
+    {
+      const bool hi = lane & 4;
+      const double send = hi ? pt[0] : pt[1];
+      const double keep = hi ? pt[1] : pt[0];
+      pt[0] = keep + __shfl_xor_sync(FULL, send, 4);
+    }
+    const double tU = pu[0];   // (U v_{E+a})[lane]
     acc += tU;
     local += 2.0 * vE * tU;
-    if (act) A.T[((size_t)En * 3 + a) * N + lane] = tT;
+    if (act) A.T[((size_t)En * 3 + a) * N + lane] = pt[0];
   }
+  __syncwarp();
   vbv += local;
   return acc;
 }
@@ -609,6 +672,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   __shared__ double red[4][32];
   __shared__ double bc[4];
   __shared__ double sh46[46];
+  __shared__ double vsm[16][64];   // per-warp SpMV staging (<= 16 warps)
   extern __shared__ float wcs[];
   const Geo& g = A.g;
   const int N = g.N;
@@ -677,7 +741,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         const double pE = pload(E);
         if (act) pcur[E * N + lane] = pE;
         double vbv = 0.0;
-        const double q = spmv_part(A, E, C, lane, pE, pload, vbv);
+        const double q = spmv_part(A, E, C, lane, pE, pload, vbv, &vsm[warp][0]);
         if (act) A.qp[E * N + lane] = q;
         ppq += warp_sum(vbv);
       }
