@@ -459,7 +459,7 @@ struct lrbms_ctx {
   size_t proj_smem = 0;
   // workspace layout
   Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
-      Binv32, partials, scal,
+      Binv32, partials, scal, gbar,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
@@ -731,6 +731,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->Binv32, (size_t)c->n_pad * c->n_pad * 4);
   alloc(c->partials, 8 * (size_t)48 * 4096);
   alloc(c->scal, 8 * 16);
+  alloc(c->gbar, 256);
   alloc(c->flags, 4 * 16);
   alloc(c->iters, 4 * 16);
   alloc(c->l_start, 4 * (size_t)(g.n_s + 1));
@@ -994,7 +995,9 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
   A.binv_smem = c->pcg_binv_smem;
   A.tstamp = c->debug_tstamp;
+  A.gbar = c->at<unsigned>(c->gbar);
   StageScope sc_(c, 4);
+  CUDA_TRY(c, cudaMemsetAsync(A.gbar, 0, sizeof(unsigned), c->stream));
   void* args[] = {&A};
   CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,
                                           c->stream));

@@ -60,6 +60,7 @@ struct PcgArgs {
   int binv_smem;          // 1: the CTA's rows of Binv are staged in shared memory once per solve
   int nh;                 // number of history vectors (0..KH)
   unsigned long long* tstamp;  // optional phase timestamps (CTA 0, first iterations), or nullptr
+  unsigned* gbar;         // grid-barrier arrival counter (zeroed before the launch)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -406,6 +407,46 @@ __device__ __forceinline__ double grid_total_b(const double* partials, int slot,
   __syncthreads();
   return *bc;
 }
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Deterministic grid-wide sum fused with the grid barrier: per-CTA partial (warps in order) ->
+// arrival on a monotone counter -> warp 0 sums the per-CTA partials in a fixed order -> shared
+// broadcast.  Two CTA barriers per call instead of the four of cta_partial + grid.sync +
+// grid_total_b.  Partials rotate over 4 slots (a slot is rewritten only 4 barriers later, after
+// every CTA has read it); red16/bc are rewritten only after the first CTA barrier of the next call.
+__device__ __forceinline__ double grid_reduce(double v, double* red16, double* partials, unsigned* bar,
+                                              unsigned& epoch, double* bc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, G = gridDim.x;
+  if (lane == 0) red16[warp] = v;
+  __syncthreads();
+  ++epoch;
+  double* ps = partials + (size_t)(epoch & 3) * G;
+  if (warp == 0) {
+    if (lane == 0) {
+      double t = 0.0;
+      for (int w = 0; w < W; ++w) t += red16[w];
+      ps[blockIdx.x] = t;
+      __threadfence();
+      atomicAdd(bar, 1u);
+      const unsigned target = epoch * (unsigned)G;
+      while (ld_acquire_gpu(bar) < target) {
+      }
+      __threadfence();
+    }
+    __syncwarp();
+    double s = 0.0;
+    for (int b = lane; b < G; b += 32) s += __ldcg(ps + b);
+    s = warp_sum(s);
+    if (lane == 0) *bc = s;
+  }
+  __syncthreads();
+  return *bc;
+}
+
 __device__ __forceinline__ double grid_total(const double* partials, int slot) {
   const int lane = threadIdx.x & 31, G = gridDim.x;
   double s = 0.0;
@@ -707,6 +748,9 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
 
   double bb, rr;
   pcg_initial_guess(A, grid, red, sh46, bb, rr);
+  __shared__ double red16[16];
+  unsigned epoch = 0;
+  double* gparts = A.partials + 8 * (size_t)gridDim.x;   // slots 8..11 (the setup uses 0..1)
   // stopping test on the preconditioned residual r.M^-1 r (an energy-norm error proxy that weights
   // the smooth, coarse-level residual components), relative to ||L^-1 b||^2 <= b.M^-1 b
   const double tol2 = A.rtol * A.rtol * bb;
@@ -720,9 +764,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       if (act) A.z[E * N + lane] = zk;
       prz += warp_sum(zk * rk);
     }
-    cta_partial(prz, red, A.partials, 2);
-    grid.sync();
-    double rz = grid_total_b(A.partials, 2, &bc[0]);
+    double rz = grid_reduce(prz, red16, gparts, A.gbar, epoch, &bc[0]);
     double beta = 0.0;
     for (it = (rz <= tol2) ? A.max_iters + 2 : 1; it <= A.max_iters; ++it) {
       double* pcur = (it & 1) ? A.pb1 : A.pb0;
@@ -746,10 +788,8 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         ppq += warp_sum(vbv);
       }
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 0] = gtimer();
-      cta_partial(ppq, red, A.partials, 3);
-      grid.sync();
+      const double pq = grid_reduce(ppq, red16, gparts, A.gbar, epoch, &bc[0]);
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 1] = gtimer();
-      const double pq = grid_total_b(A.partials, 3, &bc[1]);
       if (!(pq > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
         break;
@@ -771,10 +811,8 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         const double w = warp_sum(act ? A.zh[E * N + lane] * rk : 0.0);
         if (lane == 0) A.wc[E] = w;
       }
-      cta_partial(prr, red, A.partials, 1);
-      grid.sync();
+      rr = grid_reduce(prr, red16, gparts, A.gbar, epoch, &bc[0]);
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
-      rr = grid_total_b(A.partials, 1, &bc[2]);
       if (!(rr > 0.0)) break;   // exact solution (or NaN, flagged below)
       // C: z = M^-1 r, r.z
       double prz2 = 0.0;
@@ -787,10 +825,8 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         if (act) A.z[E * N + lane] = zk;
         prz2 += warp_sum(zk * rk);
       }
-      cta_partial(prz2, red, A.partials, 2);
-      grid.sync();
+      const double rz_new = grid_reduce(prz2, red16, gparts, A.gbar, epoch, &bc[0]);
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
-      const double rz_new = grid_total_b(A.partials, 2, &bc[3]);
       if (rz_new <= tol2) break;
       beta = rz_new / rz;
       rz = rz_new;
