@@ -251,6 +251,129 @@ __global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* flags)
   }
 }
 
+// Row-distributed Gauss-Jordan inversion in fp32 (the coarse inverse only steers the PCG; it is
+// stored in fp32 anyway): every CTA keeps its R = ceil(n / G) rows of the matrix in shared memory for
+// the whole sweep, so the only traffic per 32-wide panel K is the panel's 32 (old) pivot rows, which
+// their owners publish in a double-buffered global slab.  With P = A_KK^-1 (formed redundantly by
+// warp 0 of every CTA) and Rk = the old rows K, every row i is updated as
+//   c_i = -A_iK P (i outside K) or P[i - 32K] (i inside K);  A_iK <- c_i;
+//   A_iJ <- A_iJ + c_i Rk_J (outside K) or c_i Rk_J (inside K),  J outside K,
+// which is the blocked sweep A_KK <- P, A_KJ <- P A_KJ, A_IJ -= A_IK P A_KJ, A_IK <- -A_IK P.
+// One grid barrier per panel.  A non-positive pivot (fp32 breakdown on an ill-conditioned coarse
+// matrix) zeroes the result: the PCG then runs without the coarse correction instead of failing.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& epoch) {
+  __syncthreads();
+  ++epoch;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    const unsigned target = epoch * gridDim.x;
+    while (ld_acquire_gpu(bar) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+constexpr int GJ_CH = 256;   // columns per staged chunk of the pivot rows
+__global__ void __launch_bounds__(512, 1) k_coarse_gj32(const double* __restrict__ Bc, float* __restrict__ out,
+                                                       float* __restrict__ Rk, int n, unsigned* bar, int* bad) {
+  extern __shared__ __align__(16) float smf[];
+  const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = (n + G - 1) / G;
+  const int r0 = blockIdx.x * R, r1 = min(n, r0 + R), nr = max(0, r1 - r0);
+  float* Ar = smf;                       // [R][n] own rows
+  float* Rs = Ar + (size_t)R * n;        // [32][GJ_CH] staged pivot-row chunk
+  float* Pm = Rs + 32 * GJ_CH;           // [32][33] P = A_KK^-1
+  float* Cf = Pm + 32 * 33;              // [R][32] coefficients c_i
+  __shared__ int sbad;
+  if (tid == 0) sbad = 0;
+  for (int t = tid; t < nr * n; t += blockDim.x) Ar[t] = (float)Bc[(size_t)r0 * n + t];
+  unsigned epoch = 0;
+  const int nb = n / 32;
+  for (int K = 0; K < nb; ++K) {
+    float* Rb = Rk + (size_t)(K & 1) * 32 * n;
+    const int k0 = 32 * K;
+    __syncthreads();
+    for (int i = max(r0, k0); i < min(r1, k0 + 32); ++i)
+      for (int j = tid; j < n; j += blockDim.x) Rb[(size_t)(i - k0) * n + j] = Ar[(size_t)(i - r0) * n + j];
+    grid_barrier(bar, epoch);
+    if (warp == 0) {   // P = A_KK^-1, in-register Gauss-Jordan (lane = column)
+      float m[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) m[i] = __ldcg(Rb + (size_t)i * n + k0 + lane);
+      bool bd = false;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float pk = __shfl_sync(FULL, m[k], k);
+        bd |= !(pk > 0.f);
+        const float pinv = 1.f / pk;
+        const float rk = lane == k ? pinv : m[k] * pinv;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i == k) continue;
+          const float f = __shfl_sync(FULL, m[i], k);
+          m[i] = lane == k ? -f * pinv : fmaf(-f, rk, m[i]);
+        }
+        m[k] = rk;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) Pm[i * 33 + lane] = m[i];
+      if (bd && lane == 0) sbad = 1;
+    }
+    __syncthreads();
+    for (int t = tid; t < nr * 32; t += blockDim.x) {
+      const int i = t >> 5, cc = t & 31, gi = r0 + i;
+      float v;
+      if (gi >= k0 && gi < k0 + 32) {
+        v = Pm[(gi - k0) * 33 + cc];
+      } else {
+        v = 0.f;
+        const float* a = Ar + (size_t)i * n + k0;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) v = fmaf(-a[k], Pm[k * 33 + cc], v);
+      }
+      Cf[t] = v;
+    }
+    __syncthreads();
+    for (int t = tid; t < nr * 32; t += blockDim.x) Ar[(size_t)(t >> 5) * n + k0 + (t & 31)] = Cf[t];
+    for (int c0 = 0; c0 < n; c0 += GJ_CH) {
+      __syncthreads();   // previous chunk consumed
+      for (int t = tid; t < 32 * (GJ_CH / 4); t += blockDim.x) {
+        const int k = t / (GJ_CH / 4), j4 = t % (GJ_CH / 4), j = c0 + 4 * j4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < n) v = __ldcg(reinterpret_cast<const float4*>(Rb + (size_t)k * n + j));
+        reinterpret_cast<float4*>(Rs)[t] = v;
+      }
+      __syncthreads();
+      const int jj = tid % GJ_CH, rg = tid / GJ_CH, ng = blockDim.x / GJ_CH, j = c0 + jj;
+      if (j < n && (j < k0 || j >= k0 + 32)) {
+        float rs[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) rs[k] = Rs[k * GJ_CH + jj];
+        for (int i = rg; i < nr; i += ng) {
+          const int gi = r0 + i;
+          float acc = (gi >= k0 && gi < k0 + 32) ? 0.f : Ar[(size_t)i * n + j];
+          const float4* cf = reinterpret_cast<const float4*>(Cf + i * 32);
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) {
+            const float4 c = cf[k4];
+            acc = fmaf(c.x, rs[4 * k4], acc);
+            acc = fmaf(c.y, rs[4 * k4 + 1], acc);
+            acc = fmaf(c.z, rs[4 * k4 + 2], acc);
+            acc = fmaf(c.w, rs[4 * k4 + 3], acc);
+          }
+          Ar[(size_t)i * n + j] = acc;
+        }
+      }
+    }
+  }
+  // breakdown anywhere -> zero inverse (no coarse correction)
+  if (tid == 0 && sbad) atomicOr(bad, 1);
+  grid_barrier(bar, epoch);
+  const bool zero = __ldcg(bad) != 0;
+  for (int t = tid; t < nr * n; t += blockDim.x) out[(size_t)r0 * n + t] = zero ? 0.f : Ar[t];
+}
+
 // ---------------------------------------------------------------------------- a4: reconstruction
 __global__ void k_recon(Geo g, const double* __restrict__ Phi, const double* __restrict__ c,
                         double* __restrict__ p, unsigned long long* dt_bits) {
@@ -455,11 +578,13 @@ struct lrbms_ctx {
   lrbms_solver_opts opts{1e-12, 5000, 50, 1, 8};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
+  int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
+  size_t gj32_smem = 0;
   ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
   Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
-      Binv32, partials, scal, gbar,
+      Binv32, partials, scal, gbar, gjrk, gjbar,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
@@ -732,6 +857,8 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->partials, 8 * (size_t)48 * 4096);
   alloc(c->scal, 8 * 16);
   alloc(c->gbar, 256);
+  alloc(c->gjrk, 2 * 32 * (size_t)c->n_pad * 4);
+  alloc(c->gjbar, 256);
   alloc(c->flags, 4 * 16);
   alloc(c->iters, 4 * 16);
   alloc(c->l_start, 4 * (size_t)(g.n_s + 1));
@@ -780,6 +907,21 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_coarse_gj, 256, 0));
   if (occ < 1) return fail(c, LRBMS_E_CUDA, "GJ kernel cannot be resident");
   c->gj_G = sms * std::min(occ, 2);
+  {  // fp32 row-resident inversion when the rows fit in shared memory
+    const int n = c->n_pad, G = std::min(sms, n);
+    const int R = cdiv(n, G);
+    const size_t need = 4 * ((size_t)R * n + 32 * GJ_CH + 32 * 33 + (size_t)R * 32);
+    c->gj32_G = 0;
+    if (need <= 200 * 1024) {
+      CUDA_TRY(c, cudaFuncSetAttribute(k_coarse_gj32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+      int occ3 = 0;
+      CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, (const void*)k_coarse_gj32, 512, need));
+      if (occ3 >= 1) {
+        c->gj32_G = G;
+        c->gj32_smem = need;
+      }
+    }
+  }
   CUDA_TRY(c, cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
   // link tables
@@ -928,12 +1070,25 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
   k_coarse_assemble<<<cdiv(c->n_pad, 8), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->zc), Bc, c->n_pad);
   LAUNCH_CHECK(c);
   int n = c->n_pad;
-  int* fl = c->at<int>(c->flags);
-  void* args[] = {&Bc, &n, &fl};
-  CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj, dim3(c->gj_G), dim3(256), args, 0, c->stream));
-  c->launches++;
-  k_to_f32<<<592, 256, 0, c->stream>>>(Bc, c->at<float>(c->Binv32), (size_t)c->n_pad * c->n_pad);
-  LAUNCH_CHECK(c);
+  if (c->gj32_G > 0) {
+    const double* Bcc = Bc;
+    float* out = c->at<float>(c->Binv32);
+    float* rk = c->at<float>(c->gjrk);
+    unsigned* bar = c->at<unsigned>(c->gjbar);
+    int* bad = reinterpret_cast<int*>(bar + 16);
+    CUDA_TRY(c, cudaMemsetAsync(bar, 0, 256, c->stream));
+    void* args[] = {&Bcc, &out, &rk, &n, &bar, &bad};
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), args,
+                                            c->gj32_smem, c->stream));
+    c->launches++;
+  } else {
+    int* fl = c->at<int>(c->flags);
+    void* args[] = {&Bc, &n, &fl};
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj, dim3(c->gj_G), dim3(256), args, 0, c->stream));
+    c->launches++;
+    k_to_f32<<<592, 256, 0, c->stream>>>(Bc, c->at<float>(c->Binv32), (size_t)c->n_pad * c->n_pad);
+    LAUNCH_CHECK(c);
+  }
   c->rebuilds++;
   c->last_rebuild_step = c->steps;
   return LRBMS_OK;
