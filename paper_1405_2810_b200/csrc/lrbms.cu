@@ -814,16 +814,15 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
     P.nlp = up(g.n_loc, 4);
     P.LD = pad4(P.nlp);
     P.NP = up(g.N, 8);
-    P.KC = 64;
-    P.LDY = pad4(P.KC);
     int nfmax = 1;
     for (int a = 0; a < g.dim; ++a) nfmax = std::max(nfmax, g.nface[a]);
     P.nfmax = nfmax;
     P.nfp = up(nfmax, 4);
     P.LDN = pad4(P.nfp);
-    P.ybuf = up(std::max(std::max(P.NP * P.LDY, 2 * P.NP * P.LDN), 16 * 64), 2);
-    c->proj_smem = 8 * ((size_t)P.NP * P.LD + P.ybuf + 6 * (size_t)g.n_loc + 3 * (size_t)nfmax) +
-                   4 * ((size_t)nfmax + g.n_loc);
+    P.nwc = std::max(8 * g.n_loc, 16 * 64);
+    c->proj_smem = 8 * ((size_t)P.NP * P.LD + P.nwc + 3 * (size_t)P.NP * P.LDN + ((g.n_loc + 1) & ~1) +
+                        3 * (size_t)P.nfp) +
+                   4 * 3 * (size_t)P.nfp;
     if (c->proj_smem > 227 * 1024)
       return bad("subdomain too large for the shared-memory projection (N * n_loc too big)");
   }
