@@ -820,6 +820,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
     P.nfp = up(nfmax, 4);
     P.LDN = pad4(P.nfp);
     P.nwc = std::max(8 * g.n_loc, 16 * 64);
+    P.bulk = (g.n_loc % 2 == 0 && g.s[0] % 2 == 0) ? 1 : 0;
     c->proj_smem = 8 * ((size_t)P.NP * P.LD + P.nwc + 3 * (size_t)P.NP * P.LDN + ((g.n_loc + 1) & ~1) +
                         3 * (size_t)P.nfp) +
                    4 * 3 * (size_t)P.nfp;
@@ -1055,6 +1056,7 @@ static lrbms_status launch_project(lrbms_ctx* c) {
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
   A.fc = c->at<double2>(c->fc); A.lam = c->lam_cur();
   A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs);
+  A.tstamp = c->debug_tstamp;
   k_project<<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
   c->have_blocks = true;

@@ -30,8 +30,15 @@ struct ProjArgs {
   double* rhs;
   int LD, nlp, NP, nfmax, nfp, LDN;
   int nwc;             // doubles of the per-cell weight table (>= 8 n_loc, >= 16 x 64 for the reduction)
+  int bulk;            // 1: n_loc and s_x even: Phi_E rows and the y/z face runs move in 16-byte granules
+  unsigned long long* tstamp;   // optional phase timestamps of every 8th CTA (debug), or nullptr
 };
 
+__device__ __forceinline__ unsigned long long gtimer_p() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -46,7 +53,6 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
-
 // fixed enumeration of the upper 8x8 tile pairs (ti <= tj < 4)
 __device__ __forceinline__ int pair_ti(int p) { return p < 4 ? 0 : p < 7 ? 1 : p < 9 ? 2 : 3; }
 __device__ __forceinline__ int pair_tj(int p) {
@@ -68,74 +74,122 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   int C[3];
   sub_xyz(g, E, C);
   const size_t base = (size_t)E * nl;
+  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 0] = gtimer_p();
 
-  // 1. stage Phi_E and the neighbour face slabs asynchronously (padding with plain stores)
+  // 1. stage Phi_E and the neighbour face slabs with cp.async (16-byte granules where the layout
+  //    allows: Phi_E rows and the contiguous x-runs of the y/z faces; 8-byte gathers for x-faces)
   const double* PhiE = A.Phi + (size_t)E * N * nl;
-  if ((nl & 1) == 0) {
+  const bool v16 = A.bulk;   // n_loc and s_x even: 16-byte aligned rows and runs
+  bool has[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) has[a] = a < g.dim && C[a] + 1 < g.S[a];
+  if (v16) {
     const int h = nl >> 1;
-    for (int t = tid; t < N * h; t += nt) {
-      const int k = t / h, c2 = t - k * h;
-      cp_async16(Phs + (size_t)k * LD + 2 * c2, PhiE + (size_t)k * nl + 2 * c2);
-    }
+    for (int k = warp; k < N; k += nwarp)
+      for (int c2 = lane; c2 < h; c2 += 32)
+        cp_async16(Phs + (size_t)k * LD + 2 * c2, PhiE + (size_t)k * nl + 2 * c2);
   } else {
-    for (int t = tid; t < N * nl; t += nt) {
-      const int k = t / nl, c1 = t - k * nl;
-      cp_async8(Phs + (size_t)k * LD + c1, PhiE + (size_t)k * nl + c1);
-    }
+    for (int k = warp; k < N; k += nwarp)
+      for (int c1 = lane; c1 < nl; c1 += 32) cp_async8(Phs + (size_t)k * LD + c1, PhiE + (size_t)k * nl + c1);
   }
-  for (int k = warp; k < NP; k += nwarp)
-    for (int c1 = (k < N ? nl : 0) + lane; c1 < LD; c1 += 32) Phs[(size_t)k * LD + c1] = 0.0;
   for (int a = 0; a < 3; ++a) {
-    const bool has = a < g.dim && C[a] + 1 < g.S[a];
     const int nf = a < g.dim ? g.nface[a] : 0;
-    const double* PhiN = A.Phi + (size_t)(E + (has ? g.Estride[a] : 0)) * N * nl;
     double* dst = PhN + (size_t)a * NP * LDN;
-    for (int t = tid; t < NP * LDN; t += nt) {
-      const int k = t / LDN, f = t - k * LDN;
-      if (has && k < N && f < nf) cp_async8(dst + t, PhiN + (size_t)k * nl + face_cell(g, f, a, 0));
-      else dst[t] = 0.0;
+    if (has[a]) {
+      const double* PhiN = A.Phi + (size_t)(E + g.Estride[a]) * N * nl;
+      if (a > 0 && v16) {
+        for (int k = warp; k < N; k += nwarp)
+          for (int f2 = 2 * lane; f2 < nf; f2 += 64)
+            cp_async16(dst + (size_t)k * LDN + f2, PhiN + (size_t)k * nl + face_cell(g, f2, a, 0));
+      } else {
+        for (int k = warp; k < N; k += nwarp)
+          for (int f = lane; f < nf; f += 32)
+            cp_async8(dst + (size_t)k * LDN + f, PhiN + (size_t)k * nl + face_cell(g, f, a, 0));
+      }
     }
+    for (int k = warp; k < NP; k += nwarp)
+      for (int f = (has[a] && k < N ? nf : 0) + lane; f < LDN; f += 32) dst[(size_t)k * LDN + f] = 0.0;
     for (int f = tid; f < nfp; f += nt) {
       fcell[a * nfp + f] = (f < nf) ? face_cell(g, f, a, g.s[a] - 1) : 0;
       wi[a * nfp + f] = 0.0;
     }
   }
   asm volatile("cp.async.commit_group;\n" ::);
+  for (int k = warp; k < NP; k += nwarp)
+    for (int c1 = (k < N ? nl : 0) + lane; c1 < LD; c1 += 32) Phs[(size_t)k * LD + c1] = 0.0;
+  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 1] = gtimer_p();
 
-  // 2. a1 + face weights (R2) from the static coefficients
+  // 2. a1 + face weights (R2) from the static coefficients.  Pass 1: every cell forms the weights of
+  //    its +a faces (all loads issued up front) and of its -a faces across a subdomain side; the +a
+  //    weight inside E is also the -a weight of the upper cell.  Pass 2: the diagonal.
   for (int l = tid; l < nl; l += nt) lam[l] = A.lam[base + l];
   __syncthreads();
   for (int l = tid; l < nl; l += nt) {
     int c[3];
     local_xyz(g, l, c);
     const double ll = lam[l];
-    double d = 0.0, w[6] = {0, 0, 0, 0, 0, 0};
+    double2 fp[3], fm[3];
+    double lp[3], lm[3];
+    int wpos[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      if (a >= g.dim) break;
+      fp[a] = fm[a] = make_double2(0.0, 0.0);
+      lp[a] = lm[a] = 0.0;
+      wpos[a] = -1;
+      if (a >= g.dim) continue;
       const int st = g.lstride[a];
-      if (c[a] > 0) {   // the lower cell of a face owns its coefficients
-        w[2 * a] = face_w(A.fc[(base + l - st) * 3 + a], lam[l - st], ll);
-        d += w[2 * a];
-      } else if (C[a] > 0) {
-        const int nb = neighbour(g, E, C, l, c, a, -1);
-        d += face_w(A.fc[(size_t)nb * 3 + a], A.lam[nb], ll);
-      }
       if (c[a] + 1 < g.s[a]) {
-        w[2 * a + 1] = face_w(A.fc[(base + l) * 3 + a], ll, lam[l + st]);
-        d += w[2 * a + 1];
+        fp[a] = A.fc[(base + l) * 3 + a];
+        lp[a] = lam[l + st];
       } else if (C[a] + 1 < g.S[a]) {
         const int nb = neighbour(g, E, C, l, c, a, +1);
-        const double wv = face_w(A.fc[(base + l) * 3 + a], ll, A.lam[nb]);
-        d += wv;
-        wi[a * nfp + face_pos(g, c, a)] = wv;
+        fp[a] = A.fc[(base + l) * 3 + a];
+        lp[a] = A.lam[nb];
+        wpos[a] = face_pos(g, c, a);
+      }
+      if (c[a] == 0 && C[a] > 0) {
+        const int nb = neighbour(g, E, C, l, c, a, -1);
+        fm[a] = A.fc[(size_t)nb * 3 + a];
+        lm[a] = A.lam[nb];
       }
     }
-    double2* wc2 = reinterpret_cast<double2*>(Wc + (size_t)l * 8);
-    wc2[0] = make_double2(d, w[0]);
-    wc2[1] = make_double2(w[1], w[2]);
-    wc2[2] = make_double2(w[3], w[4]);
-    wc2[3] = make_double2(w[5], 0.0);
+    double dc = 0.0;
+    double wl[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double wp = face_w(fp[a], ll, lp[a]);
+      wl[a] = 0.0;
+      if (a < g.dim) {
+        if (wpos[a] >= 0) {
+          wi[a * nfp + wpos[a]] = wp;
+          dc += wp;
+        } else if (c[a] + 1 < g.s[a]) {
+          wl[a] = wp;
+          Wc[(size_t)(l + g.lstride[a]) * 8 + 1 + 2 * a] = wp;   // -a weight of the upper cell
+        }
+        dc += face_w(fm[a], lm[a], ll);
+      }
+    }
+    // own slots only (the -a slots 1, 3, 5 belong to the lower cell inside E); slot 7 carries the
+    // side-face weights to pass 2
+    Wc[(size_t)l * 8 + 2] = wl[0];
+    Wc[(size_t)l * 8 + 4] = wl[1];
+    Wc[(size_t)l * 8 + 6] = wl[2];
+    Wc[(size_t)l * 8 + 7] = dc;
+  }
+  __syncthreads();
+  for (int l = tid; l < nl; l += nt) {
+    int c[3];
+    local_xyz(g, l, c);
+    double* w = Wc + (size_t)l * 8;
+    double d = w[7];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a >= g.dim || c[a] == 0) w[1 + 2 * a] = 0.0;
+      if (a < g.dim) d += w[1 + 2 * a] + w[2 + 2 * a];
+    }
+    w[0] = d;
+    w[7] = 0.0;
   }
   __syncthreads();
   if (tid == 0) {  // links of E (R6), sequential: deterministic
@@ -144,8 +198,10 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
       Wc[(size_t)l * 8] += A.L.gK[q] * lam[l];
     }
   }
+  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 2] = gtimer_p();
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
+  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 3] = gtimer_p();
 
   // 3. B_EE = Phi Y^T with Y = A_EE Phi^T formed in registers; warp-strided k-steps of 4 cells
   double acc[10][2];
@@ -190,28 +246,8 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
     for (int p = 0; p < 10; ++p)
       if (pair_tj(p) < T) dmma(acc[p][0], acc[p][1], af[pair_ti(p)], bf[pair_tj(p)]);
   }
-  // deterministic cross-warp reduction, one tile pair at a time; mirror for exact symmetry
+  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 4] = gtimer_p();
   double* BEE = A.blocks + (size_t)E * nb1 * N * N;
-  double* red = Wc;  // [nwarp][64]
-  __syncthreads();   // every warp is done with the weight table
-#pragma unroll
-  for (int p = 0; p < 10; ++p) {
-    if (pair_tj(p) >= T) continue;
-    red[warp * 64 + 2 * lane] = acc[p][0];
-    red[warp * 64 + 2 * lane + 1] = acc[p][1];
-    __syncthreads();
-    if (tid < 64) {
-      double v = 0.0;
-      for (int w = 0; w < nwarp; ++w) v += red[w * 64 + tid];
-      const int r = tid >> 3, cc = tid & 7, ti = pair_ti(p), tj = pair_tj(p);
-      const int i = 8 * ti + r, j = 8 * tj + cc;
-      if (i < N && j < N && (ti < tj || r <= cc)) {
-        BEE[i * N + j] = v;
-        BEE[j * N + i] = v;
-      }
-    }
-    __syncthreads();
-  }
 
   // 4. r_E = Phi_E^T b_E, b = sum_L g_L p_L e_L
   if (tid < N) {
@@ -223,26 +259,101 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
     A.rhs[E * N + tid] = rr;
   }
 
-  // 5. coupling blocks B_{E,E+a}[i][j] = -sum_f w_f Phi_E[i][a_f] Phi_{E+a}[j][b_f], one tile per task
-  for (int t = warp; t < g.dim * T * T; t += nwarp) {
-    const int a = t / (T * T), tt = t - a * T * T, ti = tt / T, tj = tt - ti * T;
-    double* BEN = BEE + (size_t)(1 + a) * N * N;
-    const int i = 8 * ti + fr, j0 = 8 * tj + 2 * fc;
-    double c0 = 0.0, c1 = 0.0;
-    if (C[a] + 1 < g.S[a]) {
-      const double* pn = PhN + (size_t)a * NP * LDN + (size_t)(8 * tj + fr) * LDN;
-      const double* pe = Phs + (size_t)(8 * ti + fr) * LD;
-      const int* fca = fcell + a * nfp;
-      const double* wa = wi + a * nfp;
-      for (int ks = 0; ks < nfp / 4; ++ks) {
-        const int f = 4 * ks + fc;
-        dmma(c0, c1, pe[fca[f]] * wa[f], pn[f]);
+  // 5. coupling blocks B_{E,E+a}[i][j] = -sum_f w_f Phi_E[i][a_f] Phi_{E+a}[j][b_f]; every warp
+  //    interleaves up to three 8x8 output tiles (independent DMMA accumulator chains)
+  const int ntask = g.dim * T * T;
+  for (int t0 = warp; t0 < ntask; t0 += 3 * nwarp) {
+    const double* pe[3];
+    const double* pn[3];
+    const int* fca[3];
+    const double* wa[3];
+    double cc[3][2];
+    bool live[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int t = t0 + u * nwarp;
+      cc[u][0] = cc[u][1] = 0.0;
+      live[u] = false;
+      pe[u] = Phs; pn[u] = PhN; fca[u] = fcell; wa[u] = wi;
+      if (t < ntask) {
+        const int a = t / (T * T), tt = t - a * T * T, ti = tt / T, tj = tt - ti * T;
+        live[u] = has[a];
+        pn[u] = PhN + (size_t)a * NP * LDN + (size_t)(8 * tj + fr) * LDN;
+        pe[u] = Phs + (size_t)(8 * ti + fr) * LD;
+        fca[u] = fcell + a * nfp;
+        wa[u] = wi + a * nfp;
       }
     }
-    if (i < N) {
-      if (j0 < N) BEN[i * N + j0] = -c0;
-      if (j0 + 1 < N) BEN[i * N + j0 + 1] = -c1;
+    for (int ks = 0; ks < nfp / 4; ++ks) {
+      const int f = 4 * ks + fc;
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (live[u]) dmma(cc[u][0], cc[u][1], pe[u][fca[u][f]] * wa[u][f], pn[u][f]);
     }
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int t = t0 + u * nwarp;
+      if (t >= ntask) continue;
+      const int a = t / (T * T), tt = t - a * T * T, ti = tt / T, tj = tt - ti * T;
+      double* BEN = BEE + (size_t)(1 + a) * N * N;
+      const int i = 8 * ti + fr, j0 = 8 * tj + 2 * fc;
+      if (i < N) {
+        if (j0 < N) BEN[i * N + j0] = -cc[u][0];
+        if (j0 + 1 < N) BEN[i * N + j0 + 1] = -cc[u][1];
+      }
+    }
+  }
+  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 5] = gtimer_p();
+
+  // 6. deterministic cross-warp reduction of B_EE (fixed warp order), mirrored for exact symmetry.
+  //    All tile pairs at once through the (now free) Phi_E buffer when it is large enough.
+  __syncthreads();   // all reads of Phs, Wc done
+  if ((size_t)nwarp * 10 * 64 <= (size_t)NP * LD) {
+    double* red = Phs;   // [nwarp][10 pairs][64]
+#pragma unroll
+    for (int p = 0; p < 10; ++p) {
+      red[((size_t)warp * 10 + p) * 64 + 2 * lane] = acc[p][0];
+      red[((size_t)warp * 10 + p) * 64 + 2 * lane + 1] = acc[p][1];
+    }
+    __syncthreads();
+    for (int o = tid; o < 10 * 64; o += nt) {
+      const int p = o >> 6, e = o & 63;
+      const int ti = pair_ti(p), tj = pair_tj(p);
+      if (tj >= T) continue;
+      double v = 0.0;
+      for (int w = 0; w < nwarp; ++w) v += red[(size_t)w * 10 * 64 + o];
+      // fragment layout: element e = 2 lane + h holds row lane >> 2 = e >> 3, column 2 (lane & 3) + h = e & 7
+      const int rr = e >> 3, cl = e & 7;
+      const int i = 8 * ti + rr, j = 8 * tj + cl;
+      if (i < N && j < N && (ti < tj || rr <= cl)) {
+        BEE[i * N + j] = v;
+        BEE[j * N + i] = v;
+      }
+    }
+  } else {
+    double* red = Wc;  // [nwarp][64]
+#pragma unroll
+    for (int p = 0; p < 10; ++p) {
+      if (pair_tj(p) >= T) continue;
+      red[warp * 64 + 2 * lane] = acc[p][0];
+      red[warp * 64 + 2 * lane + 1] = acc[p][1];
+      __syncthreads();
+      if (tid < 64) {
+        double v = 0.0;
+        for (int w = 0; w < nwarp; ++w) v += red[w * 64 + tid];
+        const int rr = tid >> 3, cl = tid & 7, ti = pair_ti(p), tj = pair_tj(p);
+        const int i = 8 * ti + rr, j = 8 * tj + cl;
+        if (i < N && j < N && (ti < tj || rr <= cl)) {
+          BEE[i * N + j] = v;
+          BEE[j * N + i] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (A.tstamp) {
+    __syncthreads();
+    if (tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 6] = gtimer_p();
   }
 }
 
