@@ -86,15 +86,19 @@ typedef struct {
 } lrbms_links;
 
 /* Reduced-solve options (a3).  The solve is preconditioned CG on the block-Jacobi-scaled system
- * L^-1 B L^-T y = L^-1 r (B_EE = L_E L_E^T) with a coarse correction on the subdomain-indicator
- * coefficients, started from the B-optimal combination of the last `history` solutions (Galerkin
- * projection onto their span), iterated until the preconditioned residual sqrt(rh.M^-1 rh) of the
- * scaled system is <= rtol ||L^-1 r||_2 (rh = L^-1 (r - B c); an energy-norm error proxy). */
+ * L^-1 B L^-T y = L^-1 r (B_EE = L_E L_E^T) with a coarse level on the subdomain-indicator
+ * coefficients (Galerkin coarse operator E = Z^T B Z), started from the B-optimal combination of the
+ * last `history` solutions (Galerkin projection onto their span), iterated until the preconditioned
+ * residual sqrt(rh.M^-1 rh) of the scaled system is <= rtol ||L^-1 r||_2 (rh = L^-1 (r - B c); an
+ * energy-norm error proxy).  Coarse level: use_coarse = 2 (default) deflation (A-DEF2, P^T + Q, with
+ * the DEF starting vector), whose coarse inverse is refreshed every coarse_refresh steps and kept
+ * current in between by one Newton-Schulz correction per step; 1 = additive (I + Q; the inverse is
+ * only refreshed every coarse_refresh steps); 0 = block Jacobi only. */
 typedef struct {
-  double rtol;            /* default 1e-12, on sqrt(r.M^-1 r) relative to ||L^-1 b|| */
+  double rtol;            /* default 5e-13, on sqrt(r.M^-1 r) relative to ||L^-1 b|| */
   int32_t max_iters;      /* default 5000 */
-  int32_t coarse_refresh; /* rebuild the coarse-level inverse every k steps (default 50; 1 = every step) */
-  int32_t use_coarse;     /* 1 (default) = two-level, 0 = block-Jacobi only */
+  int32_t coarse_refresh; /* full coarse inverse every k steps (default 50; 1 = every step) */
+  int32_t use_coarse;     /* 2 (default) = deflation, 1 = additive two-level, 0 = block Jacobi only */
   int32_t history;        /* previous solutions in the initial-guess projection, 0..8 (default 8) */
 } lrbms_solver_opts;
 

@@ -9,7 +9,9 @@
 //   k_recon      a4       p = Phi_E c_E, coalesced streaming read of Phi
 //   k_flux_cfl   a5       face/link fluxes with lambda(s^n), per-cell Q_i, global min dt
 //   k_transport  a6       explicit upwind update
-// plus k_coarse_assemble / k_coarse_gj (coarse-level inverse, rebuilt every few steps).
+// plus the coarse level (k_coarse_gj32 / k_coarse_gj inverses, k_coarse_rt + k_ns_gemm updates).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,6 +27,7 @@
 #include "lrbms_kernels.cuh"
 #include "lrbms_pcg.cuh"
 #include "lrbms_project.cuh"
+#include "lrbms_ns.cuh"
 
 using namespace lrbms;
 
@@ -113,44 +116,20 @@ __global__ void k_basis_indicator(Geo g, const double* __restrict__ Phi, double*
 }
 
 // ---------------------------------------------------------------------------- coarse level
-// Bc[E][E'] = zc_E^T B_EE' zc_E' (Galerkin coarse operator on the subdomain indicators).
-__global__ void k_coarse_assemble(Geo g, const double* __restrict__ blocks, const double* __restrict__ zc,
-                                  double* __restrict__ Bc, int n_pad) {
-  const int lane = threadIdx.x & 31;
-  const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (E >= n_pad) return;
-  if (E >= g.n_s) {
-    if (lane == 0) Bc[(size_t)E * n_pad + E] = 1.0;
+// dense fp64 coarse matrix from the stencil (identity padding), for the global fp64 sweep below
+__global__ void k_coarse_dense(Geo g, const double* __restrict__ Es, double* __restrict__ Bc, int n_pad) {
+  const int F = blockIdx.x * blockDim.x + threadIdx.x;
+  if (F >= n_pad) return;
+  double* row = Bc + (size_t)F * n_pad;
+  if (F >= g.n_s) {
+    row[F] = 1.0;
     return;
   }
-  const int N = g.N, nb1 = 1 + g.dim;
-  const bool act = lane < N;
-  const double* Bd = blocks + (size_t)E * nb1 * N * N;
-  const double zk = act ? zc[E * N + lane] : 0.0;
-  double t = 0.0;
-  for (int j = 0; j < N; ++j) {
-    const double zj = __shfl_sync(FULL, zk, j);
-    if (act) t += Bd[j * N + lane] * zj;
-  }
-  const double d = warp_sum(act ? t * zk : 0.0);
-  if (lane == 0) Bc[(size_t)E * n_pad + E] = d;
   int C[3];
-  sub_xyz(g, E, C);
-  for (int a = 0; a < g.dim; ++a) {
-    if (C[a] + 1 >= g.S[a]) continue;
-    const int En = E + g.Estride[a];
-    const double* U = Bd + (size_t)(1 + a) * N * N;
-    double u = 0.0;   // (U^T zc_E)[lane]
-    for (int k = 0; k < N; ++k) {
-      const double zkk = __shfl_sync(FULL, zk, k);
-      if (act) u += U[k * N + lane] * zkk;
-    }
-    const double o = warp_sum(act ? u * zc[En * N + lane] : 0.0);
-    if (lane == 0) {
-      Bc[(size_t)E * n_pad + En] = o;
-      Bc[(size_t)En * n_pad + E] = o;
-    }
-  }
+  sub_xyz(g, F, C);
+  row[F] = Es[(size_t)F * 8];
+  for (int s = 0; s < 6; ++s)
+    if (side_exists(g, C, s)) row[side_nb(g, F, s)] = Es[(size_t)F * 8 + 1 + s];
 }
 
 // Blocked in-place Gauss-Jordan inversion (sweep) of the SPD coarse matrix, 32 x 32 tiles.
@@ -251,6 +230,150 @@ __global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* flags)
   }
 }
 
+// RT = I - X E = (I - E X)^T for symmetric X (the tensor-core update keeps X exactly symmetric):
+// RT[i][j] = delta_ij - sum_{G in {j} + nb(j)} X[i][G] E_{jG}; j >= n_s: identity padding of E.
+// Row-wise, coalesced over j.  Its rows are the K-major B operand of k_ns_gemm_tc.
+__global__ void k_coarse_rt(Geo g, const float* __restrict__ X, const double* __restrict__ Es, float* __restrict__ RT,
+                            int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  if (j >= n) return;
+  const float* xi = X + (size_t)i * n;
+  float v;
+  if (j < g.n_s) {
+    const double* e = Es + (size_t)j * 8;
+    int C[3];
+    sub_xyz(g, j, C);
+    v = xi[j] * (float)e[0];
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (side_exists(g, C, s)) v = fmaf(xi[side_nb(g, j, s)], (float)e[1 + s], v);
+  } else {
+    v = xi[j];
+  }
+  RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+}
+
+// R = I - E X for the Newton-Schulz update of the coarse inverse (X is not exactly symmetric:
+// using (I - X E)^T instead would double X's antisymmetric part every step):
+// R[k][j] = delta_kj - sum_{G in {k} + nb(k)} E_{kG} X[G][j]; rows k >= n_s are the identity padding
+// of E.  fp32 (R ~ the one-step change of B_c^-1; its rounding only perturbs the correction).
+__global__ void k_coarse_r(Geo g, const float* __restrict__ X, const double* __restrict__ Es, float* __restrict__ R,
+                           int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (j >= n) return;
+  float v;
+  if (k < g.n_s) {
+    const double* e = Es + (size_t)k * 8;
+    int C[3];
+    sub_xyz(g, k, C);
+    v = X[(size_t)k * n + j] * (float)e[0];
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (side_exists(g, C, s)) v = fmaf((float)e[1 + s], X[(size_t)side_nb(g, k, s) * n + j], v);
+  } else {
+    v = X[(size_t)k * n + j];
+  }
+  R[(size_t)k * n + j] = (k == j ? 1.f : 0.f) - v;
+}
+
+// Xn = X + X R on the tensor cores (TF32 inputs, fp32 accumulate), both row-major (mma.sync
+// m16n8k8 row.col with the B fragments read from a k-major tile).  CTA tile 128 x 128, k-chunks of
+// 32 double-buffered with cp.async, 8 warps of 64 x 32.  n % 32 == 0.
+__device__ __forceinline__ unsigned to_tf32(float f) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], const unsigned (&b)[2]) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};\n"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+constexpr int NS_BM = 128, NS_BK = 32, NS_LDS = NS_BK + 4, NS_LDB = NS_BM + 8;
+constexpr int NS_SMEM = 4 * 2 * (NS_BM * NS_LDS + NS_BK * NS_LDB);
+__global__ void __launch_bounds__(256) k_ns_gemm(const float* __restrict__ X, const float* __restrict__ R,
+                                                 float* __restrict__ Xn, int n) {
+  extern __shared__ __align__(16) float sg[];
+  float* As = sg;                              // [2][128][36]  (m, k)
+  float* Bs = sg + 2 * NS_BM * NS_LDS;         // [2][32][136]  (k, n)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m0 = blockIdx.y * NS_BM, n0 = blockIdx.x * NS_BM;
+  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;   // warp tile 64 x 32
+  const int gq = lane >> 2, tq = lane & 3;
+  float acc[4][4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.f;
+  auto load = [&](int stage, int k0) {
+    float* as = As + stage * NS_BM * NS_LDS;
+    float* bs = Bs + stage * NS_BK * NS_LDB;
+    for (int t = tid; t < NS_BM * NS_BK / 4; t += blockDim.x) {
+      const int r = t >> 3, c4 = (t & 7) * 4;
+      if (m0 + r < n) cp_async16(as + r * NS_LDS + c4, X + (size_t)(m0 + r) * n + k0 + c4);
+      else *reinterpret_cast<float4*>(as + r * NS_LDS + c4) = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int kr = t >> 5, n4 = (t & 31) * 4;
+      if (n0 + n4 < n) cp_async16(bs + kr * NS_LDB + n4, R + (size_t)(k0 + kr) * n + n0 + n4);
+      else *reinterpret_cast<float4*>(bs + kr * NS_LDB + n4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  const int nk = n / NS_BK;
+  load(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      load((kc + 1) & 1, (kc + 1) * NS_BK);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const float* as = As + (kc & 1) * NS_BM * NS_LDS;
+    const float* bs = Bs + (kc & 1) * NS_BK * NS_LDB;
+#pragma unroll
+    for (int k8 = 0; k8 < NS_BK; k8 += 8) {
+      unsigned af[4][4], bf[4][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const float* ap = as + (wm + 16 * mi + gq) * NS_LDS + k8 + tq;
+        af[mi][0] = to_tf32(ap[0]);
+        af[mi][1] = to_tf32(ap[8 * NS_LDS]);
+        af[mi][2] = to_tf32(ap[4]);
+        af[mi][3] = to_tf32(ap[8 * NS_LDS + 4]);
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const float* bp = bs + (k8 + tq) * NS_LDB + wn + 8 * ni + gq;
+        bf[ni][0] = to_tf32(bp[0]);
+        bf[ni][1] = to_tf32(bp[4 * NS_LDB]);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) mma_tf32(acc[mi][ni], af[mi], bf[ni]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int r = m0 + wm + 16 * mi + gq, c = n0 + wn + 8 * ni + 2 * tq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rr = r + 8 * h;
+        if (rr < n && c < n) {
+          const float2 x = *reinterpret_cast<const float2*>(X + (size_t)rr * n + c);
+          *reinterpret_cast<float2*>(Xn + (size_t)rr * n + c) =
+              make_float2(x.x + acc[mi][ni][2 * h], x.y + acc[mi][ni][2 * h + 1]);
+        }
+      }
+    }
+}
+
 // Row-distributed Gauss-Jordan inversion in fp32 (the coarse inverse only steers the PCG; it is
 // stored in fp32 anyway): every CTA keeps its R = ceil(n / G) rows of the matrix in shared memory for
 // the whole sweep, so the only traffic per 32-wide panel K is the panel's 32 (old) pivot rows, which
@@ -275,7 +398,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& epoch) {
   __syncthreads();
 }
 constexpr int GJ_CH = 256;   // columns per staged chunk of the pivot rows
-__global__ void __launch_bounds__(512, 1) k_coarse_gj32(const double* __restrict__ Bc, float* __restrict__ out,
+__global__ void __launch_bounds__(512, 1) k_coarse_gj32(Geo g, const double* __restrict__ Es, float* __restrict__ out,
                                                        float* __restrict__ Rk, int n, unsigned* bar, int* bad) {
   extern __shared__ __align__(16) float smf[];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -287,7 +410,21 @@ __global__ void __launch_bounds__(512, 1) k_coarse_gj32(const double* __restrict
   float* Cf = Pm + 32 * 33;              // [R][32] coefficients c_i
   __shared__ int sbad;
   if (tid == 0) sbad = 0;
-  for (int t = tid; t < nr * n; t += blockDim.x) Ar[t] = (float)Bc[(size_t)r0 * n + t];
+  for (int t = tid; t < nr * n; t += blockDim.x) Ar[t] = 0.f;
+  __syncthreads();
+  for (int i = tid; i < nr; i += blockDim.x) {   // rows of the coarse stencil (identity padding)
+    const int gi = r0 + i;
+    float* row = Ar + (size_t)i * n;
+    if (gi < g.n_s) {
+      int C[3];
+      sub_xyz(g, gi, C);
+      row[gi] = (float)Es[(size_t)gi * 8];
+      for (int s = 0; s < 6; ++s)
+        if (side_exists(g, C, s)) row[side_nb(g, gi, s)] = (float)Es[(size_t)gi * 8 + 1 + s];
+    } else {
+      row[gi] = 1.f;
+    }
+  }
   unsigned epoch = 0;
   const int nb = n / 32;
   for (int K = 0; K < nb; ++K) {
@@ -575,16 +712,20 @@ struct lrbms_ctx {
   std::vector<int> h_sub_start, h_local, h_orig;
   std::vector<double> h_geo2, h_p, h_s;
   double fpmax = 0.0;
-  lrbms_solver_opts opts{1e-12, 5000, 50, 1, 8};
+  lrbms_solver_opts opts{5e-13, 5000, 50, 2, 8};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
+  int xcur = 0;            // which of Binv32 / Binv32b holds the current coarse inverse
+  CUtensorMap tmX[2], tmRT;  // TMA descriptors of the coarse inverse buffers and of RT
+  bool have_tmaps = false;
+  bool have_x = false;
   size_t gj32_smem = 0;
   ProjArgs proj{};   // layout fields (LD, NP, ...) fixed at create
   size_t proj_smem = 0;
   // workspace layout
   Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
-      Binv32, partials, scal, gbar, gjrk, gjbar,
+      Binv32, Binv32b, RTb, Es, Yd, cont, e0, partials, scal, gbar, gjrk, gjbar,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
@@ -858,6 +999,12 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->scal, 8 * 16);
   alloc(c->gbar, 256);
   alloc(c->gjrk, 2 * 32 * (size_t)c->n_pad * 4);
+  alloc(c->Binv32b, (size_t)c->n_pad * c->n_pad * 4);
+  alloc(c->RTb, (size_t)c->n_pad * c->n_pad * 4);
+  alloc(c->Es, (size_t)g.n_s * 8 * 8);
+  alloc(c->Yd, R * 6 * 8);
+  alloc(c->cont, (size_t)c->n_pad * 8 * 4);
+  alloc(c->e0, (size_t)c->n_pad * 8);
   alloc(c->gjbar, 256);
   alloc(c->flags, 4 * 16);
   alloc(c->iters, 4 * 16);
@@ -924,6 +1071,32 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   }
   CUDA_TRY(c, cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
+  {  // TMA descriptors (128 x 32 fp32 boxes, 128-byte swizzle) for the tensor-core Newton-Schulz GEMM
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    c->have_tmaps = false;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn &&
+        q == cudaDriverEntryPointSuccess) {
+      auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      const cuuint64_t dims[2] = {(cuuint64_t)c->n_pad, (cuuint64_t)c->n_pad};
+      const cuuint64_t strides[1] = {(cuuint64_t)c->n_pad * 4};
+      const cuuint32_t box[2] = {NS_TK, NS_TM}, estr[2] = {1, 1};
+      void* ptrs[3] = {c->at<float>(c->Binv32), c->at<float>(c->Binv32b), c->at<float>(c->RTb)};
+      CUtensorMap* maps[3] = {&c->tmX[0], &c->tmX[1], &c->tmRT};
+      bool ok = true;
+      for (int i = 0; i < 3; ++i)
+        ok = ok && encode(maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptrs[i], dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      c->have_tmaps = ok;
+    }
+    if (c->have_tmaps)
+      CUDA_TRY(c, cudaFuncSetAttribute(k_ns_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, NS_TC_SMEM));
+  }
+  // coarse-rhs contribution slots of absent neighbours are never written: zero them once
+  CUDA_TRY(c, cudaMemsetAsync(c->at<float>(c->cont), 0, (size_t)c->n_pad * 8 * 4, c->stream));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_ns_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   NS_SMEM));
   // link tables
   const Geo& g = c->g;
   CUDA_TRY(c, cudaMemcpyAsync(c->at<int>(c->l_start), c->h_sub_start.data(), 4 * (g.n_s + 1), cudaMemcpyHostToDevice, c->stream));
@@ -987,6 +1160,7 @@ lrbms_status lrbms_set_basis(lrbms_ctx* c, const double* Phi) {
   c->have_basis = true;
   c->have_blocks = false;
   c->last_rebuild_step = -1;
+  c->have_x = false;
   return LRBMS_OK;
 }
 
@@ -1011,6 +1185,7 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
   c->total_iters = 0;
   c->last_iters = 0;
   c->last_rebuild_step = -1;
+  c->have_x = false;
   c->have_sat = true;
   c->have_blocks = false;
   return LRBMS_OK;
@@ -1019,10 +1194,12 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
 lrbms_status lrbms_set_solver(lrbms_ctx* c, const lrbms_solver_opts* o) {
   lrbms_status st = check_ctx(c, false);
   if (st) return st;
-  if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1 || o->history < 0 || o->history > KHIST)
+  if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1 || o->history < 0 || o->history > KHIST ||
+      o->use_coarse < 0 || o->use_coarse > 2)
     return fail(c, LRBMS_E_CONFIG, "invalid solver options");
   c->opts = *o;
   c->last_rebuild_step = -1;
+  c->have_x = false;
   return LRBMS_OK;
 }
 
@@ -1063,60 +1240,91 @@ static lrbms_status launch_project(lrbms_ctx* c) {
   return LRBMS_OK;
 }
 
+static float* coarse_x(lrbms_ctx* c, int i) { return i == 0 ? c->at<float>(c->Binv32) : c->at<float>(c->Binv32b); }
+
+// Coarse level, after the scaling (the 7-point coarse stencil Es is a by-product of k_block_chol and
+// k_transform).  A full inverse every coarse_refresh steps (fp32 row-resident Gauss-Jordan, or the
+// fp64 global sweep when the rows do not fit in shared memory); in between, with deflation (mode 2),
+// one Newton-Schulz correction per step keeps it current: X <- X + X (I - E X) (tensor cores, TF32).
 static lrbms_status launch_coarse(lrbms_ctx* c) {
   StageScope sc_(c, 1);
   const Geo& g = c->g;
-  double* Bc = c->at<double>(c->Binv);
-  CUDA_TRY(c, cudaMemsetAsync(Bc, 0, c->Binv.bytes, c->stream));
-  k_coarse_assemble<<<cdiv(c->n_pad, 8), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->zc), Bc, c->n_pad);
-  LAUNCH_CHECK(c);
+  const int mode = c->opts.use_coarse;
   int n = c->n_pad;
-  if (c->gj32_G > 0) {
-    const double* Bcc = Bc;
-    float* out = c->at<float>(c->Binv32);
-    float* rk = c->at<float>(c->gjrk);
-    unsigned* bar = c->at<unsigned>(c->gjbar);
-    int* bad = reinterpret_cast<int*>(bar + 16);
-    CUDA_TRY(c, cudaMemsetAsync(bar, 0, 256, c->stream));
-    void* args[] = {&Bcc, &out, &rk, &n, &bar, &bad};
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), args,
-                                            c->gj32_smem, c->stream));
-    c->launches++;
-  } else {
-    int* fl = c->at<int>(c->flags);
-    void* args[] = {&Bc, &n, &fl};
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj, dim3(c->gj_G), dim3(256), args, 0, c->stream));
-    c->launches++;
-    k_to_f32<<<592, 256, 0, c->stream>>>(Bc, c->at<float>(c->Binv32), (size_t)c->n_pad * c->n_pad);
-    LAUNCH_CHECK(c);
+  const bool rebuild = !c->have_x || c->last_rebuild_step < 0 || c->steps - c->last_rebuild_step >= c->opts.coarse_refresh;
+  if (rebuild) {
+    if (c->gj32_G > 0) {
+      Geo gg = g;
+      const double* es = c->at<double>(c->Es);
+      float* out = coarse_x(c, c->xcur);
+      float* rk = c->at<float>(c->gjrk);
+      unsigned* bar = c->at<unsigned>(c->gjbar);
+      int* bad = reinterpret_cast<int*>(bar + 16);
+      CUDA_TRY(c, cudaMemsetAsync(bar, 0, 256, c->stream));
+      void* args[] = {&gg, &es, &out, &rk, &n, &bar, &bad};
+      CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), args,
+                                              c->gj32_smem, c->stream));
+      c->launches++;
+    } else {
+      double* Bc = c->at<double>(c->Binv);
+      CUDA_TRY(c, cudaMemsetAsync(Bc, 0, c->Binv.bytes, c->stream));
+      k_coarse_dense<<<cdiv(n, 256), 256, 0, c->stream>>>(g, c->at<double>(c->Es), Bc, n);
+      LAUNCH_CHECK(c);
+      int* fl = c->at<int>(c->flags);
+      void* args[] = {&Bc, &n, &fl};
+      CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj, dim3(c->gj_G), dim3(256), args, 0, c->stream));
+      c->launches++;
+      k_to_f32<<<592, 256, 0, c->stream>>>(Bc, coarse_x(c, c->xcur), (size_t)n * n);
+      LAUNCH_CHECK(c);
+    }
+    c->rebuilds++;
+    c->last_rebuild_step = c->steps;
+    c->have_x = true;
+  } else if (mode == 2) {
+    float* X = coarse_x(c, c->xcur);
+    float* Xn = coarse_x(c, 1 - c->xcur);
+    if (c->have_tmaps) {   // tcgen05 (TF32, TMEM accumulators), upper-triangular tiles, symmetric output
+      k_coarse_rt<<<dim3(cdiv(n, 256), n), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es), c->at<float>(c->RTb), n);
+      LAUNCH_CHECK(c);
+      const int nbt = cdiv(n, NS_TM);
+      k_ns_gemm_tc<<<nbt * (nbt + 1) / 2, 128, NS_TC_SMEM, c->stream>>>(c->tmX[c->xcur], c->tmRT, X, Xn, n);
+      LAUNCH_CHECK(c);
+    } else {                 // mma.sync fallback
+      k_coarse_r<<<dim3(cdiv(n, 256), n), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es), c->at<float>(c->RTb), n);
+      LAUNCH_CHECK(c);
+      k_ns_gemm<<<dim3(cdiv(n, NS_BM), cdiv(n, NS_BM)), 256, NS_SMEM, c->stream>>>(X, c->at<float>(c->RTb), Xn, n);
+      LAUNCH_CHECK(c);
+    }
+    c->xcur = 1 - c->xcur;
   }
-  c->rebuilds++;
-  c->last_rebuild_step = c->steps;
   return LRBMS_OK;
 }
 
 static lrbms_status launch_solve(lrbms_ctx* c) {
   const Geo& g = c->g;
-  const bool coarse = c->opts.use_coarse && g.n_s > 1;
-  if (coarse && (c->last_rebuild_step < 0 || c->steps - c->last_rebuild_step >= c->opts.coarse_refresh)) {
-    lrbms_status st = launch_coarse(c);   // from the untransformed blocks
-    if (st) return st;
-  }
+  const int mode = (c->opts.use_coarse && g.n_s > 1) ? c->opts.use_coarse : 0;
+  const bool coarse = mode > 0;
   {
-    StageScope sc_(c, 2);   // block Cholesky + scaling of the couplings: Bh = L^-1 B L^-T
+    StageScope sc_(c, 2);   // block Cholesky + scaling of the couplings: Bh = L^-1 B L^-T (+ coarse stencil)
+    double* es = coarse ? c->at<double>(c->Es) : nullptr;
     k_block_chol<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
                                                          c->at<double>(c->zc), c->at<double>(c->zh),
-                                                         c->at<int>(c->flags));
+                                                         c->at<int>(c->flags), es);
     LAUNCH_CHECK(c);
-    k_transform<<<g.n_s, 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv));
+    k_transform<<<g.n_s, 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
+                                              c->at<double>(c->zh), mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
     LAUNCH_CHECK(c);
+  }
+  if (coarse) {
+    lrbms_status st = launch_coarse(c);
+    if (st) return st;
   }
   c->have_blocks = false;   // the blocks are now in scaled form
   PcgArgs A;
   A.g = g;
   A.blocks = c->at<double>(c->blocks); A.Linv = c->at<double>(c->Linv);
   A.rhs = c->at<double>(c->rhs); A.zh = c->at<double>(c->zh);
-  A.Binv = c->at<float>(c->Binv32);
+  A.Binv = coarse_x(c, c->xcur);
   A.x = c->at<double>(c->c); A.y = c->at<double>(c->yv);
   const size_t R = (size_t)g.n_s * g.N;
   A.nh = std::min(c->hist_count, c->opts.history);
@@ -1148,10 +1356,11 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.pb0 = c->at<double>(c->pv); A.pb1 = c->at<double>(c->pv2);
   A.qp = c->at<double>(c->q); A.T = c->at<double>(c->T); A.wc = c->at<double>(c->wc);
   A.partials = c->at<double>(c->partials); A.iters = c->at<int>(c->iters); A.flags = c->at<int>(c->flags);
-  A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = coarse ? 1 : 0;
+  A.rtol = c->opts.rtol; A.max_iters = c->opts.max_iters; A.n_pad = c->n_pad; A.use_coarse = mode;
   A.binv_smem = c->pcg_binv_smem;
   A.tstamp = c->debug_tstamp;
   A.gbar = c->at<unsigned>(c->gbar);
+  A.Yd = c->at<double>(c->Yd); A.cont = c->at<float>(c->cont); A.e0 = c->at<double>(c->e0);
   StageScope sc_(c, 4);
   CUDA_TRY(c, cudaMemsetAsync(A.gbar, 0, sizeof(unsigned), c->stream));
   void* args[] = {&A};
@@ -1368,6 +1577,17 @@ int64_t lrbms_launch_count(const lrbms_ctx* c) { return c ? c->launches : 0; }
  * first 64 iterations, %globaltimer ns) written to a caller-owned device buffer, or NULL. */
 void lrbms_debug_set_tstamp(lrbms_ctx* c, unsigned long long* dev_buf) {
   if (c) c->debug_tstamp = dev_buf;
+}
+
+/* undocumented debugging hook: copies the current coarse inverse (n_pad x n_pad fp32) and the coarse
+ * stencil (n_s x 8 fp64) to host buffers (either may be NULL); returns n_pad. */
+int32_t lrbms_debug_coarse(lrbms_ctx* c, float* x_host, double* es_host) {
+  if (!c || !c->ws) return -1;
+  cudaStreamSynchronize(c->stream);
+  const size_t n = c->n_pad;
+  if (x_host) cudaMemcpy(x_host, coarse_x(c, c->xcur), n * n * 4, cudaMemcpyDeviceToHost);
+  if (es_host) cudaMemcpy(es_host, c->at<double>(c->Es), (size_t)c->g.n_s * 64, cudaMemcpyDeviceToHost);
+  return (int32_t)n;
 }
 
 lrbms_status lrbms_set_profiling(lrbms_ctx* c, int32_t enable) {

@@ -133,6 +133,16 @@ __device__ __forceinline__ int face_cell(const Geo& g, int f, int a, int ca) {
   return x + g.s[0] * (y + g.s[1] * ca);
 }
 
+// sides s of subdomain E (coordinates C): s = a -> E + e_a, s = 3 + a -> E - e_a
+__device__ __forceinline__ bool side_exists(const Geo& g, const int C[3], int s) {
+  const int a = s < 3 ? s : s - 3;
+  if (a >= g.dim) return false;
+  return s < 3 ? C[a] + 1 < g.S[a] : C[a] > 0;
+}
+__device__ __forceinline__ int side_nb(const Geo& g, int E, int s) {
+  return s < 3 ? E + g.Estride[s] : E - g.Estride[s - 3];
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);

@@ -56,11 +56,14 @@ struct PcgArgs {
   double rtol;
   int max_iters;
   int n_pad;
-  int use_coarse;
+  int use_coarse;         // 0: block Jacobi only; 1: additive coarse level; 2: A-DEF2 deflation
   int binv_smem;          // 1: the CTA's rows of Binv are staged in shared memory once per solve
   int nh;                 // number of history vectors (0..KH)
   unsigned long long* tstamp;  // optional phase timestamps (CTA 0, first iterations), or nullptr
   unsigned* gbar;         // grid-barrier arrival counter (zeroed before the launch)
+  const double* Yd;       // [n_s][6][N] deflation vectors Y_{E,F} = Bh_{E,F} zh_F (k_transform), mode 2
+  float* cont;            // [n_pad][8] contributions Y_{E,F}.r_E to the coarse rhs of F, by side
+  double* e0;             // [n_pad] coarse correction of the starting vector
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -119,7 +122,7 @@ __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
 // Warp per subdomain.  Lane j holds column j of the (padded-to-32 with identity) block.
 __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
                                                    const double* __restrict__ zc, double* __restrict__ zh,
-                                                   int* flags) {
+                                                   int* flags, double* __restrict__ Es) {
   const int lane = threadIdx.x & 31;
   const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (E >= g.n_s) return;
@@ -176,6 +179,10 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
       }
     zh[E * N + lane] = zhat;
   }
+  if (Es) {   // coarse operator diagonal zc^T B_EE zc = |L^T zc|^2; the side slots are set by k_transform
+    const double d = warp_sum(lane < N ? zhat * zhat : 0.0);
+    if (lane < 8) Es[(size_t)E * 8 + lane] = lane == 0 ? d : 0.0;
+  }
 }
 
 __device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double b) {
@@ -186,8 +193,13 @@ __device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double 
 
 // CTA (8 warps) per subdomain E: Bh_{E,E+a} = L_E^-1 U L_{E+a}^-T in place for its upper couplings,
 // two 32x32x32 products on the fp64 tensor cores (DMMA) through shared memory (rows padded to 36).
+//
+// For the deflation preconditioner it also forms Y_{E,F} = Bh_{E,F} zh_F for the neighbours F of E
+// (Yd[E][a] for F = E + e_a, Yd[E][3 + a] for F = E - e_a; Yd == nullptr: not needed).
 __global__ void __launch_bounds__(256) k_transform(Geo g, double* __restrict__ blocks,
-                                                  const double* __restrict__ Linv) {
+                                                  const double* __restrict__ Linv,
+                                                  const double* __restrict__ zh, double* __restrict__ Yd,
+                                                  double* __restrict__ Es) {
   constexpr int LDX = 36;
   __shared__ double XE[32 * LDX], Us[32 * LDX], XN[32 * LDX], T1[32 * LDX];
   const int E = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -230,6 +242,28 @@ __global__ void __launch_bounds__(256) k_transform(Geo g, double* __restrict__ b
       if (i < N) {
         if (j < N) U[i * N + j] = c0;
         if (j + 1 < N) U[i * N + j + 1] = c1;
+      }
+      Us[i * LDX + j] = c0;   // Bh (zero beyond N: X_E and X_N are zero padded)
+      Us[i * LDX + j + 1] = c1;
+    }
+    if (Es) {
+      __syncthreads();
+      const int En = E + g.Estride[a];
+      if (warp == 0) {   // Y_{E,E+a} = Bh zh_{E+a}; coarse coupling zc_E^T B_{E,E+a} zc_{E+a} = zh_E . Y
+        double acc = 0.0;
+        const double zn = lane < N ? zh[(size_t)En * N + lane] : 0.0;
+        for (int j = 0; j < N; ++j) acc += Us[lane * LDX + j] * __shfl_sync(FULL, zn, j);
+        if (Yd && lane < N) Yd[((size_t)E * 6 + a) * N + lane] = acc;
+        const double o = warp_sum(lane < N ? acc * zh[(size_t)E * N + lane] : 0.0);
+        if (lane == 0) {
+          Es[(size_t)E * 8 + 1 + a] = o;
+          Es[(size_t)En * 8 + 4 + a] = o;
+        }
+      } else if (warp == 1 && Yd) {   // Y_{E+a,E} = Bh^T zh_E
+        double acc = 0.0;
+        const double ze = lane < N ? zh[(size_t)E * N + lane] : 0.0;
+        for (int i = 0; i < N; ++i) acc += Us[i * LDX + lane] * __shfl_sync(FULL, ze, i);
+        if (lane < N) Yd[((size_t)En * 6 + 3 + a) * N + lane] = acc;
       }
     }
     __syncthreads();
@@ -345,28 +379,73 @@ __device__ __forceinline__ double lower_contrib(const PcgArgs& A, int E, const i
   return t;
 }
 
-// z_E = r_E + zh_E e_E with e_E = (B_c^-1 Zh^T r)_E  (coarse product in fp32: preconditioner)
+// e_E = (B_c^-1 g)_E for the staged coarse vector g (fp32: the coarse level only steers the
+// iteration); warp-uniform result.
+__device__ __forceinline__ float coarse_e(const PcgArgs& A, const float* wcv, const float* brow, int lane) {
+  const float4* row = reinterpret_cast<const float4*>(brow);
+  const float4* w4 = reinterpret_cast<const float4*>(wcv);
+  const int n4 = A.n_pad >> 2;
+  float e0 = 0.f, e1 = 0.f;
+#pragma unroll 4
+  for (int F = lane; F < n4; F += 32) {
+    const float4 b0 = row[F], c0 = w4[F];
+    e0 = fmaf(b0.x, c0.x, e0);
+    e1 = fmaf(b0.y, c0.y, e1);
+    e0 = fmaf(b0.z, c0.z, e0);
+    e1 = fmaf(b0.w, c0.w, e1);
+  }
+  float e = e0 + e1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
+  return e;
+}
+
+// Two-level preconditioners on the scaled system (block-Jacobi part = I, Q = Zh B_c^-1 Zh^T):
+//  mode 1, additive:  z = r + Q r                    (coarse rhs g = Zh^T r)
+//  mode 2, A-DEF2:    z = P^T r + Q r,  P = I - Bh Q  (coarse rhs g = Zh^T (I - Bh) r)
+// A-DEF2 needs a current B_c^-1 (kept current by a Newton-Schulz step per time step); its coarse
+// rhs only involves the couplings (Bh_EE = I): g_F = -sum_{E nb F} Y_{E,F} . r_E (defl_scatter).
+// In both, z_E = r_E + zh_E (B_c^-1 g)_E.
 __device__ __forceinline__ double precond(const PcgArgs& A, const float* wcv, const float* brow, int E, int lane, double rk) {
   const int N = A.g.N;
-  float e = 0.f;
-  if (A.use_coarse) {
-    const float4* row = reinterpret_cast<const float4*>(brow);
-    const float4* w4 = reinterpret_cast<const float4*>(wcv);
-    const int n4 = A.n_pad >> 2;
-    float e0 = 0.f, e1 = 0.f;
-#pragma unroll 4
-    for (int F = lane; F < n4; F += 32) {
-      const float4 b0 = row[F], c0 = w4[F];
-      e0 = fmaf(b0.x, c0.x, e0);
-      e1 = fmaf(b0.y, c0.y, e1);
-      e0 = fmaf(b0.z, c0.z, e0);
-      e1 = fmaf(b0.w, c0.w, e1);
-    }
-    e = e0 + e1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
-  }
+  const float e = A.use_coarse ? coarse_e(A, wcv, brow, lane) : 0.f;
   return lane < N ? rk + A.zh[E * N + lane] * (double)e : 0.0;
+}
+
+// contributions Y_{E,F} . r_E of subdomain E to the coarse rhs of its neighbours F: cont[F][s]
+// (slot s = the side of E that faces F: no slot has two writers).  One 8-value reduce-scatter
+// (9 shuffles) instead of six warp sums.
+__device__ __forceinline__ void defl_scatter(const PcgArgs& A, int E, const int C[3], int lane, double rk) {
+  const Geo& g = A.g;
+  const int N = g.N;
+  double d[8];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) d[s] = (lane < N && side_exists(g, C, s)) ? A.Yd[((size_t)E * 6 + s) * N + lane] * rk : 0.0;
+  d[6] = d[7] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 16;
+    const double send = hi ? d[i] : d[i + 4];
+    const double keep = hi ? d[i + 4] : d[i];
+    d[i] = keep + __shfl_xor_sync(FULL, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 8;
+    const double send = hi ? d[i] : d[i + 2];
+    const double keep = hi ? d[i + 2] : d[i];
+    d[i] = keep + __shfl_xor_sync(FULL, send, 8);
+  }
+  {
+    const bool hi = lane & 4;
+    const double send = hi ? d[0] : d[1];
+    const double keep = hi ? d[1] : d[0];
+    d[0] = keep + __shfl_xor_sync(FULL, send, 4);
+  }
+  d[0] += __shfl_xor_sync(FULL, d[0], 2);
+  d[0] += __shfl_xor_sync(FULL, d[0], 1);
+  const int s = lane >> 2;   // lane holds the total of value index s (lane bits 4, 3, 2)
+  if ((lane & 3) == 0 && s < 6 && side_exists(g, C, s)) A.cont[(size_t)side_nb(g, E, s) * 8 + s] = (float)d[0];
 }
 
 // per-CTA partial of a grid reduction: warps in order (deterministic).  red[slot][32] is only
@@ -740,10 +819,24 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
     return A.binv_smem ? bsm + (size_t)(((E - gw) / TW) * WPC + warp) * A.n_pad : A.Binv + (size_t)E * A.n_pad;
   };
   auto stage_wc = [&]() {   // Zh^T r -> shared memory (fp32, zero padded to n_pad)
-    if (A.use_coarse) {
-      for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) wcs[i] = i < g.n_s ? (float)A.wc[i] : 0.f;
-      __syncthreads();
+    for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) wcs[i] = i < g.n_s ? (float)__ldcg(A.wc + i) : 0.f;
+    __syncthreads();
+  };
+  auto stage_g = [&]() {    // Zh^T (I - Bh) r = -(sum of the six neighbour contributions), fixed order
+    for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) {
+      float v = 0.f;
+      if (i < g.n_s) {
+        const float4 u0 = __ldcg(reinterpret_cast<const float4*>(A.cont + (size_t)i * 8));
+        const float4 u1 = __ldcg(reinterpret_cast<const float4*>(A.cont + (size_t)i * 8 + 4));
+        v = -(((((u0.x + u0.y) + u0.z) + u0.w) + u1.x) + u1.y);
+      }
+      wcs[i] = v;
     }
+    __syncthreads();
+  };
+  auto stage_coarse = [&]() {
+    if (A.use_coarse == 1) stage_wc();
+    else if (A.use_coarse == 2) stage_g();
   };
 
   double bb, rr;
@@ -757,7 +850,32 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   int it = 0;
   if (!(rr <= 0.0) && bb > 0.0) {
     double prz = 0.0;
-    stage_wc();
+    if (A.use_coarse == 2) {
+      // DEF starting vector y0 = y + Zh e0, e0 = B_c^-1 Zh^T r, so that Zh^T r0 = 0 (up to the fp32
+      // coarse inverse): r0 = r - Bh Zh e0 = r - zh_E e0_E - sum_F Y_{E,F} e0_F
+      stage_wc();
+      for (int E = gw; E < g.n_s; E += TW) {
+        const float e = coarse_e(A, wcv, brow(E), lane);
+        if (lane == 0) A.e0[E] = (double)e;
+        if (act) A.y[E * N + lane] += A.zh[E * N + lane] * (double)e;
+      }
+      grid_reduce(0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      for (int E = gw; E < g.n_s; E += TW) {
+        int C[3];
+        sub_xyz(g, E, C);
+        double rk = 0.0;
+        if (act) {
+          rk = A.r[E * N + lane] - A.zh[E * N + lane] * __ldcg(A.e0 + E);
+#pragma unroll
+          for (int s = 0; s < 6; ++s)
+            if (side_exists(g, C, s)) rk -= A.Yd[((size_t)E * 6 + s) * N + lane] * __ldcg(A.e0 + side_nb(g, E, s));
+          A.r[E * N + lane] = rk;
+        }
+        defl_scatter(A, E, C, lane, rk);
+      }
+      grid_reduce(0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+    }
+    stage_coarse();
     for (int E = gw; E < g.n_s; E += TW) {
       const double rk = act ? A.r[E * N + lane] : 0.0;
       const double zk = precond(A, wcv, brow(E), E, lane, rk);
@@ -808,8 +926,12 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
           A.r[E * N + lane] = rk;
         }
         prr += warp_sum(rk * rk);
-        const double w = warp_sum(act ? A.zh[E * N + lane] * rk : 0.0);
-        if (lane == 0) A.wc[E] = w;
+        if (A.use_coarse == 1) {
+          const double w = warp_sum(act ? A.zh[E * N + lane] * rk : 0.0);
+          if (lane == 0) A.wc[E] = w;
+        } else if (A.use_coarse == 2) {
+          defl_scatter(A, E, C, lane, rk);
+        }
       }
       rr = grid_reduce(prr, red16, gparts, A.gbar, epoch, &bc[0]);
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
@@ -818,7 +940,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
       double prz2 = 0.0;
       if (A.use_coarse && !A.binv_smem)
         for (int E = gw; E < g.n_s; E += TW) prefetch_l1(A.Binv + (size_t)E * A.n_pad, A.n_pad * 4, lane);
-      stage_wc();
+      stage_coarse();
       for (int E = gw; E < g.n_s; E += TW) {
         const double rk = act ? A.r[E * N + lane] : 0.0;
         const double zk = precond(A, wcv, brow(E), E, lane, rk);
