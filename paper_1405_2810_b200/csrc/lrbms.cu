@@ -233,24 +233,41 @@ __global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* flags)
 // RT = I - X E = (I - E X)^T for symmetric X (the tensor-core update keeps X exactly symmetric):
 // RT[i][j] = delta_ij - sum_{G in {j} + nb(j)} X[i][G] E_{jG}; j >= n_s: identity padding of E.
 // Row-wise, coalesced over j.  Its rows are the K-major B operand of k_ns_gemm_tc.
-__global__ void k_coarse_rt(Geo g, const float* __restrict__ X, const double* __restrict__ Es, float* __restrict__ RT,
-                            int n) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+constexpr int RT_ROWS = 16;   // rows of RT per CTA (the column's stencil is loaded once per CTA)
+__global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restrict__ X, const double* __restrict__ Es,
+                                                   float* __restrict__ RT, int n) {
+  // thread <-> column j: its stencil (coefficients, neighbour columns) in registers, reused for
+  // RT_ROWS rows; the X reads of a warp are contiguous per stencil offset (L1-resident rows)
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i0 = blockIdx.y * RT_ROWS;
   if (j >= n) return;
-  const float* xi = X + (size_t)i * n;
-  float v;
+  float e[7];
+  int nb[7];
+  nb[0] = j;
   if (j < g.n_s) {
-    const double* e = Es + (size_t)j * 8;
     int C[3];
     sub_xyz(g, j, C);
-    v = xi[j] * (float)e[0];
+    e[0] = (float)Es[(size_t)j * 8];
 #pragma unroll
-    for (int s = 0; s < 6; ++s)
-      if (side_exists(g, C, s)) v = fmaf(xi[side_nb(g, j, s)], (float)e[1 + s], v);
+    for (int s = 0; s < 6; ++s) {
+      const bool ex = side_exists(g, C, s);
+      e[1 + s] = ex ? (float)Es[(size_t)j * 8 + 1 + s] : 0.f;
+      nb[1 + s] = ex ? side_nb(g, j, s) : j;
+    }
   } else {
-    v = xi[j];
+    e[0] = 1.f;
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      e[1 + s] = 0.f;
+      nb[1 + s] = j;
+    }
   }
-  RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+  for (int i = i0; i < min(n, i0 + RT_ROWS); ++i) {
+    const float* xi = X + (size_t)i * n;
+    float v = xi[nb[0]] * e[0];
+#pragma unroll
+    for (int s = 1; s < 7; ++s) v = fmaf(xi[nb[s]], e[s], v);
+    RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+  }
 }
 
 // R = I - E X for the Newton-Schulz update of the coarse inverse (X is not exactly symmetric:
@@ -1284,7 +1301,8 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
     float* X = coarse_x(c, c->xcur);
     float* Xn = coarse_x(c, 1 - c->xcur);
     if (c->have_tmaps) {   // tcgen05 (TF32, TMEM accumulators), upper-triangular tiles, symmetric output
-      k_coarse_rt<<<dim3(cdiv(n, 256), n), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es), c->at<float>(c->RTb), n);
+      k_coarse_rt<<<dim3(cdiv(n, 256), cdiv(n, RT_ROWS)), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es),
+                                                                              c->at<float>(c->RTb), n);
       LAUNCH_CHECK(c);
       const int nbt = cdiv(n, NS_TM);
       k_ns_gemm_tc<<<nbt * (nbt + 1) / 2, 128, NS_TC_SMEM, c->stream>>>(c->tmX[c->xcur], c->tmRT, X, Xn, n);

@@ -246,7 +246,7 @@ def test_c4_prefix_tight_solver():
     reduced solve; c and p carry the 1e-10 bar."""
     sc = inputs.make_scenario("C4")
     ref = O.run(sc, n_steps=10, keep=True)
-    ctx = ctx_for(sc, rtol=1e-14)
+    ctx = ctx_for(sc, rtol=1e-15)
     ctx.run(10)
     s, p, c = ctx.get_state()
     assert rel(np_(c), ref["cs"][-1]) <= 1e-10
