@@ -97,7 +97,7 @@ typedef struct {
 typedef struct {
   double rtol;            /* default 5e-13, on sqrt(r.M^-1 r) relative to ||L^-1 b|| */
   int32_t max_iters;      /* default 5000 */
-  int32_t coarse_refresh; /* full coarse inverse every k steps (default 50; 1 = every step) */
+  int32_t coarse_refresh; /* full coarse inverse every k steps (default 200; 1 = every step) */
   int32_t use_coarse;     /* 2 (default) = deflation, 1 = additive two-level, 0 = block Jacobi only */
   int32_t history;        /* previous solutions in the initial-guess projection, 0..8 (default 8) */
 } lrbms_solver_opts;

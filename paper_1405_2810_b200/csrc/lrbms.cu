@@ -729,7 +729,7 @@ struct lrbms_ctx {
   std::vector<int> h_sub_start, h_local, h_orig;
   std::vector<double> h_geo2, h_p, h_s;
   double fpmax = 0.0;
-  lrbms_solver_opts opts{5e-13, 5000, 50, 2, 8};
+  lrbms_solver_opts opts{5e-13, 5000, 200, 2, 8};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid

@@ -192,7 +192,7 @@ class LrbmsContext:
         self._check(self.L.lrbms_set_saturation(self.h, _ptr(t)))
         self.stream.synchronize()
 
-    def set_solver(self, rtol=5e-13, max_iters=5000, coarse_refresh=50, use_coarse=2, history=8):
+    def set_solver(self, rtol=5e-13, max_iters=5000, coarse_refresh=200, use_coarse=2, history=8):
         o = SolverOpts(rtol, max_iters, coarse_refresh, use_coarse, history)
         self._check(self.L.lrbms_set_solver(self.h, ctypes.byref(o)))
 
