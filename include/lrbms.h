@@ -100,6 +100,9 @@ typedef struct {
   int32_t coarse_refresh; /* full coarse inverse every k steps (default 200; 1 = every step) */
   int32_t use_coarse;     /* 2 (default) = deflation, 1 = additive two-level, 0 = block Jacobi only */
   int32_t history;        /* previous solutions in the initial-guess projection, 0..8 (default 8) */
+  int32_t onchip;         /* 1 (default): keep the scaled reduced operator on chip for the whole solve
+                             (couplings in tensor memory / shared memory, one warp per subdomain) when
+                             n_s <= 14 x SMs; 0: stream the couplings from L2 every iteration */
 } lrbms_solver_opts;
 
 typedef struct {

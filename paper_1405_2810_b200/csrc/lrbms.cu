@@ -26,6 +26,7 @@
 #include "../../include/lrbms.h"
 #include "lrbms_kernels.cuh"
 #include "lrbms_pcg.cuh"
+#include "lrbms_pcg_tm.cuh"
 #include "lrbms_project.cuh"
 #include "lrbms_ns.cuh"
 
@@ -729,9 +730,11 @@ struct lrbms_ctx {
   std::vector<int> h_sub_start, h_local, h_orig;
   std::vector<double> h_geo2, h_p, h_s;
   double fpmax = 0.0;
-  lrbms_solver_opts opts{5e-13, 5000, 200, 2, 8};
+  lrbms_solver_opts opts{5e-13, 5000, 200, 2, 8, 1};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
+  int tm_W = 0, tm_G = 0;   // on-chip PCG (k_pcg_tm) launch; tm_W = 0: not usable
+  size_t tm_smem = 0;
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
   int xcur = 0;            // which of Binv32 / Binv32b holds the current coarse inverse
   CUtensorMap tmX[2], tmRT;  // TMA descriptors of the coarse inverse buffers and of RT
@@ -1068,6 +1071,24 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
       }
     }
   }
+  {  // on-chip PCG: one warp per subdomain, at most 14 warps (448 threads) per CTA, one CTA per SM
+    c->tm_W = 0;
+    const int W = cdiv(c->g.n_s, sms);
+    if (W <= 14 && c->g.N <= 32) {
+      const int G = cdiv(c->g.n_s, W);
+      const TmLayout Ls = tm_layout(W, c->g.dim, c->n_pad);
+      if (Ls.total <= 227 * 1024 - 1024) {
+        // at least 116 KB so that no two CTAs share an SM (each allocates all 512 TMEM columns)
+        const size_t smem = std::max<size_t>(Ls.total, 116 * 1024);
+        CUDA_TRY(c, cudaFuncSetAttribute(k_pcg_tm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ_tm = 0;
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tm, (const void*)k_pcg_tm, 32 * W, smem));
+        if (occ_tm == 1 && G <= sms) {
+          c->tm_W = W; c->tm_G = G; c->tm_smem = smem;
+        }
+      }
+    }
+  }
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_coarse_gj, 256, 0));
   if (occ < 1) return fail(c, LRBMS_E_CUDA, "GJ kernel cannot be resident");
   c->gj_G = sms * std::min(occ, 2);
@@ -1212,7 +1233,7 @@ lrbms_status lrbms_set_solver(lrbms_ctx* c, const lrbms_solver_opts* o) {
   lrbms_status st = check_ctx(c, false);
   if (st) return st;
   if (!o || !(o->rtol > 0) || o->max_iters < 1 || o->coarse_refresh < 1 || o->history < 0 || o->history > KHIST ||
-      o->use_coarse < 0 || o->use_coarse > 2)
+      o->use_coarse < 0 || o->use_coarse > 2 || o->onchip < 0 || o->onchip > 1)
     return fail(c, LRBMS_E_CONFIG, "invalid solver options");
   c->opts = *o;
   c->last_rebuild_step = -1;
@@ -1382,8 +1403,13 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   StageScope sc_(c, 4);
   CUDA_TRY(c, cudaMemsetAsync(A.gbar, 0, sizeof(unsigned), c->stream));
   void* args[] = {&A};
-  CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,
-                                          c->stream));
+  if (c->opts.onchip && c->tm_W > 0) {
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg_tm, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,
+                                            c->stream));
+  } else {
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,
+                                            c->stream));
+  }
   c->launches++;
   c->solves++;
   c->hist_head = out_slot;

@@ -1,0 +1,550 @@
+// lrbms_pcg_tm.cuh -- a3 (eq:reducedSystem): the deflated PCG of lrbms_pcg.cuh
+// with the scaled reduced operator held ON CHIP for the whole solve.
+//
+// One cooperative persistent kernel, one CTA per SM, one warp per subdomain E (lane k <-> reduced
+// coefficient k, N <= 32), so every per-subdomain vector (y, r, z, p, q) lives in registers and only
+// the exchange with neighbouring subdomains goes through L2.  The scaled couplings
+// Bh_{E,E+a} = L_E^-1 B_{E,E+a} L_{E+a}^-T (upper storage, 8 KB each) are loaded ONCE per solve:
+//
+//   tensor memory (TMEM, 256 KB per SM, 512 columns x 128 lanes): warp w may only address lane
+//     quadrant q = w % 4, which holds 8 blocks (each lane keeps its 4 x 8 register tile of a block in
+//     64 32-bit columns).  The m-th warp of the quadrant (m = w / 4) owns quadrant block slots
+//     b = dim m + a; slots b < 8 are TMEM columns 64 b .. +63, read back with tcgen05.ld every
+//     iteration (~300 B/SM-cycle measured, tools/mb_tmem.cu, vs ~127 B/cycle for shared memory);
+//   the overflow slots b >= 8 (3D, more than two warps per quadrant) -> shared memory,
+//     element-interleaved over lanes (bank-conflict free).  C5 (14 warps): 46 blocks in TMEM, 10 in
+//     shared memory;
+//   deflation vectors Y_{E,F} (6 per subdomain) and the fp32 rows of the coarse inverse B_c^-1 of
+//     the CTA's subdomains -> shared memory (C5: 221 KB in all).
+//
+// Iteration (3 grid barriers, each fused with its reduction, deterministic fixed-order sums):
+//   A: p = z + beta p; q_own = p + sum_a U_a p_{E+a} (p_{E+a} rebuilt from the neighbour's published
+//      z and previous p); U_a^T p_E -> T[E+a][a]; p.Bh p (symmetric form)              -> reduce
+//   B: q = q_own + lower hand-overs; y += alpha p; r -= alpha q; r.r; deflation scatter -> reduce
+//   C: g = Zh^T (I - Bh) r staged; e_E = (B_c^-1 g)_E; z = r + zh e_E; publish z; r.z  -> reduce
+#pragma once
+#include "lrbms_pcg.cuh"
+
+namespace lrbms {
+
+__device__ __forceinline__ uint32_t smem_addr_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 32 lanes x 32 consecutive 32-bit TMEM columns <-> 32 registers per lane
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
+
+// Block tile of lane l = 4 a + b (see spmv_part): element k = 8 i + j is U[4a + i][b + 4j].
+// Half h (0, 1) holds rows i = 2h, 2h + 1: 16 doubles = 32 TMEM columns.
+//
+// Accumulates pu[i] += sum_j U[.][.] vc[j] (rows) and pt[j] += sum_i U[.][.] vr[i] (columns).
+__device__ __forceinline__ void tile_half(const double (&u)[16], int h, const double (&vr)[4], const double (&vc)[8],
+                                          double (&pu)[4], double (&pt)[8]) {
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double x = u[ii * 8 + j];
+      pu[2 * h + ii] = fma(x, vc[j], pu[2 * h + ii]);
+      pt[j] = fma(x, vr[2 * h + ii], pt[j]);
+    }
+}
+
+// 4-lane (rows) and 8-lane (columns) reduce-scatters of the tile partials: lane l ends with
+// (U v)[l] in the return value and (U^T w)[l] in tcol.
+__device__ __forceinline__ double tile_scatter(double (&pu)[4], double (&pt)[8], int lane, double& tcol) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 2;
+    const double send = hi ? pu[i] : pu[i + 2];
+    const double keep = hi ? pu[i + 2] : pu[i];
+    pu[i] = keep + __shfl_xor_sync(FULL, send, 2);
+  }
+  {
+    const bool hi = lane & 1;
+    const double send = hi ? pu[0] : pu[1];
+    const double keep = hi ? pu[1] : pu[0];
+    pu[0] = keep + __shfl_xor_sync(FULL, send, 1);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool hi = lane & 16;
+    const double send = hi ? pt[j] : pt[j + 4];
+    const double keep = hi ? pt[j + 4] : pt[j];
+    pt[j] = keep + __shfl_xor_sync(FULL, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool hi = lane & 8;
+    const double send = hi ? pt[j] : pt[j + 2];
+    const double keep = hi ? pt[j + 2] : pt[j];
+    pt[j] = keep + __shfl_xor_sync(FULL, send, 8);
+  }
+  {
+    const bool hi = lane & 4;
+    const double send = hi ? pt[0] : pt[1];
+    const double keep = hi ? pt[1] : pt[0];
+    pt[0] = keep + __shfl_xor_sync(FULL, send, 4);
+  }
+  tcol = pt[0];
+  return pu[0];
+}
+
+// Sums of the k_hist_gram partials and the nh x nh Galerkin system for the history weights
+// (every thread solves it redundantly; the same arithmetic as pcg_initial_guess).
+__device__ __noinline__ void hist_weights(const PcgArgs& A, double* sh, double (&alpha_h)[8]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nh = A.nh;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) alpha_h[j] = 0.0;
+  if (nh <= 0) return;
+  if (warp == 0) {
+    for (int q = 0; q < 44; ++q) {
+      double v = 0.0;
+      for (int b = lane; b < A.ngram; b += 32) v += A.gpart[q * A.ngram + b];
+      v = warp_sum(v);
+      if (lane == 0) sh[q] = v;
+    }
+  }
+  __syncthreads();
+  double G[8][8], rhs8[8];
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = i; j < 8; ++j) {
+      const double v = (j < nh) ? sh[q] : 0.0;
+      G[i][j] = v; G[j][i] = v;
+      ++q;
+    }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rhs8[i] = i < nh ? sh[36 + i] : 0.0;
+  bool keep[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    keep[k] = k < nh && G[k][k] > 1e-12 * fabs(G[0][0]) && G[k][k] > 0.0;
+    if (keep[k]) {
+      const double piv = G[k][k];
+#pragma unroll
+      for (int i = k + 1; i < 8; ++i) {
+        const double f = G[i][k] / piv;
+#pragma unroll
+        for (int j = k; j < 8; ++j) G[i][j] -= f * G[k][j];
+        rhs8[i] -= f * rhs8[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 7; k >= 0; --k) {
+    if (k < nh && keep[k]) {
+      double v = rhs8[k];
+#pragma unroll
+      for (int j = k + 1; j < 8; ++j) v -= G[k][j] * alpha_h[j];
+      alpha_h[k] = v / G[k][k];
+    }
+  }
+}
+
+// TMEM block slots per lane quadrant (512 columns / 64 per block)
+constexpr int TM_SLOTS = 8;
+constexpr int TM_COLS = 512;
+// blocks of warp w that do not fit its TMEM quadrant, and the first shared-memory slot of warp w
+__host__ __device__ inline int tm_overflow(int w, int dim) {
+  const int m = w >> 2, o = dim * m + dim - TM_SLOTS;
+  return o < 0 ? 0 : (o > dim ? dim : o);
+}
+__host__ __device__ inline int tm_slot_base(int w, int dim) {
+  int b = 0;
+  for (int v = 0; v < w; ++v) b += tm_overflow(v, dim);
+  return b;
+}
+
+// shared-memory layout of k_pcg_tm (dynamic part), in this order:
+//   double ov[n_ov][32][32] (overflow coupling blocks, element k of lane l at [k][l])
+//   double yd[W][6][32]     (deflation vectors, zero for missing sides / lanes >= N)
+//   float  gs[n_pad]        (staged coarse vector)
+//   float  bs[W][n_pad]     (rows of the coarse inverse)
+struct TmLayout {
+  size_t ov, yd, gs, bs, total;
+};
+__host__ __device__ inline TmLayout tm_layout(int W, int dim, int n_pad) {
+  TmLayout L;
+  size_t o = 0;
+  L.ov = o; o += (size_t)tm_slot_base(W, dim) * 1024 * 8;
+  L.yd = o; o += (size_t)W * 6 * 32 * 8;
+  L.gs = o; o += (size_t)n_pad * 4;
+  L.bs = o; o += (size_t)W * n_pad * 4;
+  L.total = o;
+  return L;
+}
+
+// debug progress marker (tstamp buffer, entries 256 + CTA): last stage reached by each CTA
+#define TM_PROG(code)                                                                          \
+  do {                                                                                         \
+    if (A.tstamp && threadIdx.x == 0) {                                                        \
+      reinterpret_cast<volatile unsigned long long*>(A.tstamp)[256 + blockIdx.x] = (code);     \
+      __threadfence_system();                                                                  \
+    }                                                                                          \
+  } while (0)
+
+__global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ uint32_t tbase_s;
+  __shared__ double red16[16];
+  __shared__ double bc[4];
+  __shared__ double sh46[46];
+  const Geo& g = A.g;
+  const int N = g.N, dim = g.dim;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int E = blockIdx.x * W + warp;
+  const bool own = E < g.n_s;
+  const bool act = own && lane < N;
+  const TmLayout L = tm_layout(W, dim, A.n_pad);
+  double* ov = reinterpret_cast<double*>(dsm + L.ov) + (size_t)tm_slot_base(warp, dim) * 1024;
+  const int a_ov = max(0, TM_SLOTS - dim * (warp >> 2));   // blocks a >= a_ov of this warp are in shared memory
+  double* yd = reinterpret_cast<double*>(dsm + L.yd) + (size_t)warp * 6 * 32;
+  float* gs = reinterpret_cast<float*>(dsm + L.gs);
+  float* bs = reinterpret_cast<float*>(dsm + L.bs) + (size_t)warp * A.n_pad;
+  const int n4 = A.n_pad >> 2;   // float4 chunks of a coarse row
+  const int tm_ncols = TM_COLS;
+
+  // ---- TMEM: allocate, then every warp writes its a = 0, 1 coupling tiles
+  TM_PROG(1);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr_u32(&tbase_s)),
+                 "r"(tm_ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // TMEM address of block a of this warp: lane quadrant (warp % 4), columns 64 (dim (warp / 4) + a)
+  const uint32_t tcol = tbase_s + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(dim * (warp >> 2));
+
+  TM_PROG(2);
+  int C[3] = {0, 0, 0};
+  if (own) sub_xyz(g, E, C);
+  bool up[3], lo[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    up[a] = own && a < dim && C[a] + 1 < g.S[a];
+    lo[a] = own && a < dim && C[a] > 0;
+  }
+  const int ra = (lane >> 2) * 4, cb = lane & 3;
+  {
+    const double* Bd = A.blocks + (size_t)(own ? E : 0) * (1 + dim) * N * N;
+#pragma unroll 1
+    for (int a = 0; a < dim; ++a) {
+      if (!up[a]) continue;
+      const double* U = Bd + (size_t)(1 + a) * N * N;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t v[32];
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = ra + 2 * h + ii, c = cb + 4 * j;
+            const double x = (r < N && c < N) ? U[r * N + c] : 0.0;
+            if (a < a_ov) {
+              v[2 * (ii * 8 + j)] = (uint32_t)__double2loint(x);
+              v[2 * (ii * 8 + j) + 1] = (uint32_t)__double2hiint(x);
+            } else {
+              ov[(size_t)(a - a_ov) * 1024 + (size_t)(16 * h + ii * 8 + j) * 32 + lane] = x;
+            }
+          }
+        if (a < a_ov) tm_st32(tcol + 64u * a + 32u * h, v);
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    double v = 0.0;
+    if (A.use_coarse == 2 && act && side_exists(g, C, s)) v = A.Yd[((size_t)E * 6 + s) * N + lane];
+    yd[s * 32 + lane] = v;
+  }
+  if (A.use_coarse) {
+    const float4* src = reinterpret_cast<const float4*>(A.Binv + (size_t)(own ? E : 0) * A.n_pad);
+    float4* dst = reinterpret_cast<float4*>(bs);
+    for (int q = lane; q < (A.n_pad >> 2); q += 32) dst[q] = own ? __ldcs(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const double zh = act ? A.zh[E * N + lane] : 0.0;
+  TM_PROG(3);
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  TM_PROG(4);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+
+  // coarse product e_E = (B_c^-1 gs)_E, the row of E in shared memory
+  auto coarse_dot = [&]() -> float {
+    const float4* g4 = reinterpret_cast<const float4*>(gs);
+    const float4* b4 = reinterpret_cast<const float4*>(bs);
+    float e0 = 0.f, e1 = 0.f;
+#pragma unroll 4
+    for (int F = lane; F < n4; F += 32) {
+      const float4 b = b4[F], c = g4[F];
+      e0 = fmaf(b.x, c.x, e0);
+      e1 = fmaf(b.y, c.y, e1);
+      e0 = fmaf(b.z, c.z, e0);
+      e1 = fmaf(b.w, c.w, e1);
+    }
+    float e = e0 + e1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
+    return e;
+  };
+  auto stage_wc = [&]() {
+    for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) gs[i] = i < g.n_s ? (float)__ldcg(A.wc + i) : 0.f;
+    __syncthreads();
+  };
+  auto stage_g = [&]() {   // Zh^T (I - Bh) r = -(sum of the six neighbour contributions), fixed order
+    for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) {
+      float v = 0.f;
+      if (i < g.n_s) {
+        const float4 c0 = __ldcg(reinterpret_cast<const float4*>(A.cont + (size_t)i * 8));
+        const float4 c1 = __ldcg(reinterpret_cast<const float4*>(A.cont + (size_t)i * 8 + 4));
+        v = -(((((c0.x + c0.y) + c0.z) + c0.w) + c1.x) + c1.y);
+      }
+      gs[i] = v;
+    }
+    __syncthreads();
+  };
+  // contributions Y_{E,F} . r_E to the coarse rhs of the neighbours F (as defl_scatter)
+  auto scatter = [&](double rk) {
+    double d[8];
+#pragma unroll
+    for (int s = 0; s < 6; ++s) d[s] = yd[s * 32 + lane] * rk;
+    d[6] = d[7] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool hi = lane & 16;
+      const double send = hi ? d[i] : d[i + 4];
+      const double keep = hi ? d[i + 4] : d[i];
+      d[i] = keep + __shfl_xor_sync(FULL, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const bool hi = lane & 8;
+      const double send = hi ? d[i] : d[i + 2];
+      const double keep = hi ? d[i + 2] : d[i];
+      d[i] = keep + __shfl_xor_sync(FULL, send, 8);
+    }
+    {
+      const bool hi = lane & 4;
+      const double send = hi ? d[0] : d[1];
+      const double keep = hi ? d[1] : d[0];
+      d[0] = keep + __shfl_xor_sync(FULL, send, 4);
+    }
+    d[0] += __shfl_xor_sync(FULL, d[0], 2);
+    d[0] += __shfl_xor_sync(FULL, d[0], 1);
+    const int s = lane >> 2;
+    if (own && (lane & 3) == 0 && s < 6 && side_exists(g, C, s)) A.cont[(size_t)side_nb(g, E, s) * 8 + s] = (float)d[0];
+  };
+
+  unsigned epoch = 0;
+  double* gparts = A.partials + 8 * (size_t)gridDim.x;
+
+  // ---- initial guess: Galerkin combination of the history, y0 = W alpha, r0 = rb - V alpha
+  double alpha_h[8];
+  hist_weights(A, sh46, alpha_h);
+  const size_t R = (size_t)g.n_s * N;
+  double y = 0.0, r = 0.0;
+  double pbb = 0.0;
+  if (own) {
+    const double rbk = act ? A.rb[E * N + lane] : 0.0;
+    r = rbk;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < A.nh && act) {
+        y += alpha_h[j] * A.W[j * R + E * N + lane];
+        r -= alpha_h[j] * A.V[j * R + E * N + lane];
+      }
+    pbb = warp_sum(rbk * rbk);
+    const double w = warp_sum(zh * r);
+    if (lane == 0) A.wc[E] = w;
+  }
+  TM_PROG(5);
+  const double bb = grid_reduce(pbb, red16, gparts, A.gbar, epoch, &bc[0]);
+  TM_PROG(6);
+  const double tol2 = A.rtol * A.rtol * bb;
+  double rr = 1.0;
+  int it = 0;
+  if (bb > 0.0) {
+    if (A.use_coarse == 2) {
+      // DEF starting vector (see k_pcg): y0 += Zh e0, e0 = B_c^-1 Zh^T r; r0 -= Bh Zh e0
+      TM_PROG(60);
+      stage_wc();
+      TM_PROG(61);
+      const float e = coarse_dot();
+      TM_PROG(62);
+      if (own) {
+        if (lane == 0) A.e0[E] = (double)e;
+        y += zh * (double)e;
+      }
+      grid_reduce(0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      TM_PROG(63);
+      if (own) {
+        double rk = r - zh * __ldcg(A.e0 + E);
+#pragma unroll
+        for (int s = 0; s < 6; ++s)
+          if (act && side_exists(g, C, s)) rk -= yd[s * 32 + lane] * __ldcg(A.e0 + side_nb(g, E, s));
+        r = act ? rk : 0.0;
+      }
+      TM_PROG(64);
+      scatter(r);
+      TM_PROG(65);
+      grid_reduce(0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      TM_PROG(66);
+      stage_g();
+      TM_PROG(67);
+    } else if (A.use_coarse == 1) {
+      stage_wc();
+    }
+    double z = r;
+    if (A.use_coarse) { const float ec = coarse_dot(); z = act ? r + zh * (double)ec : 0.0; }
+    if (act) A.z[E * N + lane] = z;
+    TM_PROG(68);
+    double rz = grid_reduce(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+    TM_PROG(69);
+    double beta = 0.0, p = 0.0;
+    for (it = (rz <= tol2) ? A.max_iters + 2 : 1; it <= A.max_iters; ++it) {
+      double* pcur = (it & 1) ? A.pb1 : A.pb0;
+      const double* pold = (it & 1) ? A.pb0 : A.pb1;
+      const bool first = it == 1;
+      TM_PROG(1000 + 10 * it);
+      // ---------------- A: p, q_own = (I + U) p, hand-overs, p.Bh p
+      p = first ? z : z + beta * p;
+      double qown = p, local = p * p;
+      if (own) {
+        if (act) pcur[E * N + lane] = p;
+        double zn[3], pn[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          zn[a] = 0.0; pn[a] = 0.0;
+          if (up[a] && act) {
+            const int En = E + g.Estride[a];
+            zn[a] = __ldcg(A.z + En * N + lane);
+            if (!first) pn[a] = __ldcg(pold + En * N + lane);
+          }
+        }
+        double vr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vr[i] = __shfl_sync(FULL, p, ra + i);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (!up[a]) continue;
+          const double vN = first ? zn[a] : fma(beta, pn[a], zn[a]);
+          double vc[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) vc[j] = __shfl_sync(FULL, vN, cb + 4 * j);
+          double pu[4] = {0.0, 0.0, 0.0, 0.0}, pt[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double u[16];
+            if (a < a_ov) {
+              uint32_t v[32];
+              tm_ld32(tcol + 64u * a + 32u * h, v);
+#pragma unroll
+              for (int k = 0; k < 16; ++k) u[k] = __hiloint2double((int)v[2 * k + 1], (int)v[2 * k]);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) u[k] = ov[(size_t)(a - a_ov) * 1024 + (size_t)(16 * h + k) * 32 + lane];
+            }
+            tile_half(u, h, vr, vc, pu, pt);
+          }
+          double tc;
+          const double tu = tile_scatter(pu, pt, lane, tc);
+          qown += tu;
+          local = fma(2.0 * p, tu, local);
+          if (act) A.T[((size_t)(E + g.Estride[a]) * 3 + a) * N + lane] = tc;
+        }
+      }
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 0] = gtimer();
+      const double pq = grid_reduce(own ? warp_sum(act ? local : 0.0) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 1] = gtimer();
+      if (!(pq > 0.0)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
+        break;
+      }
+      TM_PROG(1000 + 10 * it + 1);
+      const double alpha = rz / pq;
+      // ---------------- B: y, r, r.r, coarse rhs contributions
+      double q = qown;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        if (lo[a] && act) q += __ldcg(A.T + ((size_t)E * 3 + a) * N + lane);
+      y = fma(alpha, p, y);
+      r = act ? fma(-alpha, q, r) : 0.0;
+      if (A.use_coarse == 2) {
+        scatter(r);
+      } else if (A.use_coarse == 1 && own) {
+        const double w = warp_sum(zh * r);
+        if (lane == 0) A.wc[E] = w;
+      }
+      rr = grid_reduce(own ? warp_sum(r * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
+      if (!(rr > 0.0)) break;
+      // ---------------- C: z = M^-1 r, r.z
+      if (A.use_coarse == 2) stage_g();
+      else if (A.use_coarse == 1) stage_wc();
+      z = r;
+      if (A.use_coarse) { const float ec = coarse_dot(); z = act ? r + zh * (double)ec : 0.0; }
+      if (act) A.z[E * N + lane] = z;
+      const double rz_new = grid_reduce(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
+      if (rz_new <= tol2) break;
+      beta = rz_new / rz;
+      rz = rz_new;
+    }
+    if (it == A.max_iters + 2) it = 0;
+  } else {
+    rr = 0.0;
+  }
+  TM_PROG(7);
+  // ---- back-transform c = L^-T y
+  if (own) {
+    const double* Li = A.Linv + (size_t)E * N * N;
+    double xk = 0.0;
+    for (int i = 0; i < N; ++i) {
+      const double yi = __shfl_sync(FULL, y, i);
+      if (act) xk += Li[i * N + lane] * yi;
+    }
+    if (act) {
+      A.x[E * N + lane] = xk;
+      A.hist_out[E * N + lane] = xk;
+      A.y[E * N + lane] = y;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.iters[0] = it;
+    A.iters[1] += min(it, A.max_iters);
+    if (it > A.max_iters) atomicOr(A.flags, FLAG_NOCONV);
+    if (!(rr == rr)) atomicOr(A.flags, FLAG_NAN);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase_s), "r"(tm_ncols));
+}
+
+}  // namespace lrbms

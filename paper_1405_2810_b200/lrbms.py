@@ -50,7 +50,8 @@ class Links(ctypes.Structure):
 
 class SolverOpts(ctypes.Structure):
     _fields_ = [("rtol", ctypes.c_double), ("max_iters", ctypes.c_int32), ("coarse_refresh", ctypes.c_int32),
-                ("use_coarse", ctypes.c_int32), ("history", ctypes.c_int32)]
+                ("use_coarse", ctypes.c_int32), ("history", ctypes.c_int32),
+                ("onchip", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -192,8 +193,8 @@ class LrbmsContext:
         self._check(self.L.lrbms_set_saturation(self.h, _ptr(t)))
         self.stream.synchronize()
 
-    def set_solver(self, rtol=5e-13, max_iters=5000, coarse_refresh=200, use_coarse=2, history=8):
-        o = SolverOpts(rtol, max_iters, coarse_refresh, use_coarse, history)
+    def set_solver(self, rtol=5e-13, max_iters=5000, coarse_refresh=200, use_coarse=2, history=8, onchip=1):
+        o = SolverOpts(rtol, max_iters, coarse_refresh, use_coarse, history, onchip)
         self._check(self.L.lrbms_set_solver(self.h, ctypes.byref(o)))
 
     def run(self, n_steps, cfl=None, dt_fixed=0.0, log_dt=False):
