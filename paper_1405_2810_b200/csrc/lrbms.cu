@@ -745,7 +745,7 @@ struct lrbms_ctx {
   size_t proj_smem = 0;
   // workspace layout
   Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
-      Binv32, Binv32b, RTb, Es, Yd, cont, e0, partials, scal, gbar, gjrk, gjbar,
+      Binv32, Binv32b, RTb, Es, Yd, cont, pflags, e0, partials, scal, gbar, gjrk, gjbar,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
@@ -1012,7 +1012,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->T, R * 3 * 8);
   alloc(c->Linv, (size_t)g.n_s * g.N * g.N * 8);
   alloc(c->zh, R * 8); alloc(c->yv, R * 8);
-  alloc(c->wc, (size_t)c->n_pad * 8);
+  alloc(c->wc, 4 * (size_t)c->n_pad * 8);
   alloc(c->Binv, (size_t)c->n_pad * c->n_pad * 8);
   alloc(c->Binv32, (size_t)c->n_pad * c->n_pad * 4);
   alloc(c->partials, 8 * (size_t)48 * 4096);
@@ -1023,7 +1023,8 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->RTb, (size_t)c->n_pad * c->n_pad * 4);
   alloc(c->Es, (size_t)g.n_s * 8 * 8);
   alloc(c->Yd, R * 6 * 8);
-  alloc(c->cont, (size_t)c->n_pad * 8 * 4);
+  alloc(c->cont, (size_t)c->n_pad * (8 + 2 * 16) * 4);   // k_pcg [n_pad][8], then k_pcg_tm [2][n_pad][16]
+  alloc(c->pflags, 32 * (size_t)g.n_s * 4);
   alloc(c->e0, (size_t)c->n_pad * 8);
   alloc(c->gjbar, 256);
   alloc(c->flags, 4 * 16);
@@ -1132,7 +1133,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
       CUDA_TRY(c, cudaFuncSetAttribute(k_ns_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, NS_TC_SMEM));
   }
   // coarse-rhs contribution slots of absent neighbours are never written: zero them once
-  CUDA_TRY(c, cudaMemsetAsync(c->at<float>(c->cont), 0, (size_t)c->n_pad * 8 * 4, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<float>(c->cont), 0, (size_t)c->n_pad * (8 + 2 * 16) * 4, c->stream));
   CUDA_TRY(c, cudaFuncSetAttribute(k_ns_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    NS_SMEM));
   // link tables
@@ -1399,11 +1400,13 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.binv_smem = c->pcg_binv_smem;
   A.tstamp = c->debug_tstamp;
   A.gbar = c->at<unsigned>(c->gbar);
-  A.Yd = c->at<double>(c->Yd); A.cont = c->at<float>(c->cont); A.e0 = c->at<double>(c->e0);
+  A.Yd = c->at<double>(c->Yd); A.cont = c->at<float>(c->cont); A.cont_tm = A.cont + (size_t)c->n_pad * 8; A.e0 = c->at<double>(c->e0);
   StageScope sc_(c, 4);
-  CUDA_TRY(c, cudaMemsetAsync(A.gbar, 0, sizeof(unsigned), c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(A.gbar, 0, 256, c->stream));
   void* args[] = {&A};
+  A.pflags = c->at<unsigned>(c->pflags);
   if (c->opts.onchip && c->tm_W > 0) {
+    CUDA_TRY(c, cudaMemsetAsync(A.pflags, 0, 32 * sizeof(unsigned) * g.n_s, c->stream));
     CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg_tm, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,
                                             c->stream));
   } else {

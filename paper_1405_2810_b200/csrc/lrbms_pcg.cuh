@@ -64,6 +64,8 @@ struct PcgArgs {
   const double* Yd;       // [n_s][6][N] deflation vectors Y_{E,F} = Bh_{E,F} zh_F (k_transform), mode 2
   float* cont;            // [n_pad][8] contributions Y_{E,F}.r_E to the coarse rhs of F, by side
   double* e0;             // [n_pad] coarse correction of the starting vector
+  float* cont_tm;         // k_pcg_tm coarse-rhs data: [n_pad][8] (r), then per parity [6][n_pad] (w) + [n_pad] (g(r))
+  unsigned* pflags;       // [2][n_s][32] k_pcg_tm neighbour flags (one 128-byte line each) (u published, hand-overs published), zeroed per launch
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
