@@ -138,20 +138,40 @@ def stage_bytes(sc, iters_per_step):
     couplings = 8.0 * ns * dim * N * N
     diagb = 8.0 * ns * N * N
     n_pad = -(-ns // 32) * 32
-    # one PCG iteration: every scaled coupling block once, the six deflation vectors Y_{E,F} per
-    # subdomain, ~12 R-vectors and the fp32 coarse rhs (n_pad x 8 contribution slots); the rows of the
-    # fp32 coarse inverse are staged into shared memory once per solve
-    per_iter = couplings + 8.0 * 6 * R + 8.0 * 12 * R + 32.0 * n_pad
+    # The PCG (k_pcg_tm) loads the scaled couplings once per solve into tensor memory / shared memory
+    # (one warp per subdomain) and keeps the CTA's rows of the fp32 coarse inverse in shared memory:
+    # its compulsory DRAM/L2 bytes per launch are one pass of the couplings, the deflation vectors and
+    # the coarse rows, the history vectors of the initial guess, L^-1 for the back-transform, plus per
+    # iteration the neighbour exchange through L2 (z, p written and read by the neighbours, the
+    # hand-overs T, the coarse-rhs contributions: ~8 R-vectors)
+    per_iter = 8.0 * 8 * R + 4.0 * 8 * n_pad
+    onchip = couplings + 8.0 * 6 * R + 4.0 * n_pad * n_pad + 8.0 * R * (2 * 8 + 4) + diagb
     return {
         "project": phi + iface + 8.0 * n + 48.0 * n + blocks + 8.0 * R,
         "coarse": 20.0 * n_pad * n_pad,                   # Newton-Schulz: X -> RT, X, RT -> Xn (fp32)
         "scale": blocks + 2 * diagb + couplings + 8.0 * 6 * R,   # read B, write L, L^-1, couplings, Y
         "guess": couplings + 8.0 * R * 8 * 6,             # one multi-vector SpMV pass + history vectors
-        "pcg": 4.0 * n_pad * n_pad + (iters_per_step + 1) * per_iter + diagb,   # + back-transform (L^-1)
+        "pcg": onchip + (iters_per_step + 1) * per_iter,
         "recon": phi + 8.0 * n + 8.0 * R,
         "flux_cfl": 8.0 * n * 4 + 48.0 * n,               # p, lambda, f, netw + static face coefficients
         "transport": 8.0 * n * 5,                         # s, netw in; s, lambda, f out
     }
+
+
+# measured cost of one deterministic grid-wide reduction fused with a grid barrier (147 CTAs x 448
+# threads, a neighbour store + load before each; tools/mb_gridreduce.cu, release-reduction arrival)
+GRID_REDUCE_US = 2.84
+
+
+def sync_roofline(stages, K, iters):
+    """The PCG's latency floor: three grid-wide synchronisations per iteration (two reductions and one
+    barrier), each at least the measured GRID_REDUCE_US; frac = floor / measured time per iteration."""
+    if "pcg" not in stages or iters <= 0:
+        return None
+    us_iter = 1e3 * stages["pcg"][0] / K / iters
+    floor = 3 * GRID_REDUCE_US
+    return {"us_per_iteration": us_iter, "floor_us_per_iteration": floor, "frac": floor / us_iter,
+            "floor_source": "3 x measured grid reduction (tools/mb_gridreduce.cu, mode 3)"}
 
 
 def cpu_threads():
@@ -309,12 +329,15 @@ def run_ours(args, rank, local, world):
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * sc.n,
                 "d2h_bytes_per_step": 16 * sc.n, "steps": Ke},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_pcg" if dom == "pcg" else dom, "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_pcg_tm" if dom == "pcg" else dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": algo, "avg_launch_ms": dom_ms,
-                     "note": "k_pcg's per-iteration working set (scaled couplings, deflation vectors) is "
-                             "L2-resident and its rows of the fp32 coarse inverse sit in shared memory; "
-                             "achieved = algorithmic bytes / CUDA-event time of the launch"},
+                     "note": ("k_pcg_tm holds the scaled reduced operator on chip (tensor memory + shared memory) "
+                              "for the whole solve: its compulsory DRAM/L2 bytes are one pass of the operator and "
+                              "the per-iteration neighbour exchange, so it is far from the HBM roofline by "
+                              "construction; it is bound by the latency of its three grid-wide synchronisations "
+                              "per iteration (sync_roofline)") if dom == "pcg" else ""},
+        "sync_roofline": sync_roofline(stages, K, iters),
         "step_roofline": {"algorithmic_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (step_ms / 1e3) / 1e9,
                           "frac": step_bytes / (step_ms / 1e3) / 1e9 / peak},
         "stage_share": stage_share,
