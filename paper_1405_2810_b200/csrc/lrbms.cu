@@ -733,6 +733,7 @@ struct lrbms_ctx {
   lrbms_solver_opts opts{5e-13, 5000, 200, 2, 8, 1};
   int n_pad = 0;
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
+  int sms = 148;   // SM count of the device (wave size of the one-CTA-per-SM kernels)
   int tm_W = 0, tm_G = 0;   // on-chip PCG (k_pcg_tm) launch; tm_W = 0: not usable
   size_t tm_smem = 0;
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
@@ -766,6 +767,10 @@ struct lrbms_ctx {
   // stage profiling (CUDA events)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
+  // side stream: the Newton-Schulz update of the coarse inverse runs concurrently with the
+  // initial-guess kernels (both only need the scaled operator; the PCG needs both)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   std::vector<std::pair<int, int>> ev_pending;  // (stage, index of start event in pool)
   size_t ev_used = 0;
   double stage_ms[LRBMS_N_STAGES] = {0};
@@ -962,6 +967,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (sms <= 0) sms = 148;
+  c->sms = sms;
   int W = 1;
   while (W < 16 && sms * W < g.n_s) W *= 2;
   c->pcg_W = W;
@@ -1046,6 +1052,13 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   if (((uintptr_t)ws) % 256) return fail(c, LRBMS_E_CONFIG, "workspace must be 256-byte aligned");
   c->ws = (char*)ws;
   c->stream = (cudaStream_t)stream;
+  if (!c->side) {
+    int prio_lo = 0, prio_hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+  }
   // occupancy-limited cooperative grids
   int dev = 0, sms = 148;
   CUDA_TRY(c, cudaGetDevice(&dev));
@@ -1355,9 +1368,24 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
                                               c->at<double>(c->zh), mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
     LAUNCH_CHECK(c);
   }
+  // The coarse update (Newton-Schulz: non-cooperative kernels) goes to the side stream, forked
+  // here and joined before the PCG; a full rebuild (cooperative Gauss-Jordan) stays on the main
+  // stream so that its grid is co-resident.
+  bool forked = false;
   if (coarse) {
+    const bool rebuild = !c->have_x || c->last_rebuild_step < 0 ||
+                         c->steps - c->last_rebuild_step >= c->opts.coarse_refresh;
+    cudaStream_t main = c->stream;
+    if (!rebuild && mode == 2 && c->side) {
+      CUDA_TRY(c, cudaEventRecord(c->fork_ev, main));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->fork_ev, 0));
+      c->stream = c->side;
+      forked = true;
+    }
     lrbms_status st = launch_coarse(c);
+    c->stream = main;
     if (st) return st;
+    if (forked) CUDA_TRY(c, cudaEventRecord(c->join_ev, c->side));
   }
   c->have_blocks = false;   // the blocks are now in scaled form
   PcgArgs A;
@@ -1405,6 +1433,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   CUDA_TRY(c, cudaMemsetAsync(A.gbar, 0, 256, c->stream));
   void* args[] = {&A};
   A.pflags = c->at<unsigned>(c->pflags);
+  if (forked) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->join_ev, 0));
   if (c->opts.onchip && c->tm_W > 0) {
     CUDA_TRY(c, cudaMemsetAsync(A.pflags, 0, 32 * sizeof(unsigned) * g.n_s, c->stream));
     CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg_tm, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,
@@ -1662,6 +1691,9 @@ const char* lrbms_last_error(const lrbms_ctx* c) { return c ? c->err.c_str() : "
 void lrbms_destroy(lrbms_ctx* c) {
   if (!c) return;
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->join_ev) cudaEventDestroy(c->join_ev);
   delete c;
 }
 

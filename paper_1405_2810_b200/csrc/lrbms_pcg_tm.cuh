@@ -184,13 +184,14 @@ __device__ __noinline__ void hist_weights(const PcgArgs& A, double* sh, double (
 #pragma unroll
   for (int j = 0; j < 8; ++j) alpha_h[j] = 0.0;
   if (nh <= 0) return;
-  if (warp == 0) {
-    for (int q = 0; q < 44; ++q) {
-      double v = 0.0;
-      for (int b = lane; b < A.ngram; b += 32) v += A.gpart[q * A.ngram + b];
-      v = warp_sum(v);
-      if (lane == 0) sh[q] = v;
-    }
+  // the 44 fixed-order sums of the per-CTA partials, spread over the warps (one L2 round trip chain
+  // per warp instead of 44 in one warp)
+  const int W = blockDim.x >> 5;
+  for (int q = warp; q < 44; q += W) {
+    double v = 0.0;
+    for (int b = lane; b < A.ngram; b += 32) v += __ldcg(A.gpart + q * A.ngram + b);
+    v = warp_sum(v);
+    if (lane == 0) sh[q] = v;
   }
   __syncthreads();
   double G[8][8], rhs8[8];

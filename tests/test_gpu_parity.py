@@ -81,12 +81,15 @@ def test_stage_parity_small(name, make):
     ctx.close()
 
 
+@pytest.mark.parametrize("onchip", [1, 0], ids=["onchip", "l2stream"])
 @pytest.mark.parametrize("name,make", SMALL, ids=[s[0] for s in SMALL])
-def test_full_run_small(name, make):
+def test_full_run_small(name, make, onchip):
+    """Both reduced-solve kernels: k_pcg_tm (operator held in tensor / shared memory, the default)
+    and k_pcg (couplings streamed from L2 every iteration)."""
     sc = make()
     n = 20
     ref = O.run(sc, n_steps=n, keep=True)
-    ctx = ctx_for(sc)
+    ctx = ctx_for(sc, onchip=onchip)
     dts = np_(ctx.run(n, log_dt=True))
     s, p, c = ctx.get_state()
     assert rel(dts, ref["dts"]) <= 1e-10
@@ -96,6 +99,35 @@ def test_full_run_small(name, make):
     st = ctx.stats()
     assert st["steps"] == n and st["total_iters"] > 0
     ctx.close()
+
+
+@pytest.mark.parametrize("use_coarse", [0, 1, 2])
+@pytest.mark.parametrize("onchip", [1, 0], ids=["onchip", "l2stream"])
+def test_coarse_modes_c2(use_coarse, onchip):
+    """Block Jacobi only (0), additive two-level (1) and deflation (2), in both PCG kernels, on C2:
+    a 10-step run against the oracle (reduced coefficients and saturations at the parity bar)."""
+    sc = inputs.make_scenario("C2", n_steps=10)
+    ref = O.run(sc, n_steps=10, keep=True)
+    ctx = ctx_for(sc, use_coarse=use_coarse, onchip=onchip)
+    ctx.run(10)
+    s, p, c = ctx.get_state()
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
+    assert ctx.stats()["total_iters"] > 0
+
+
+def test_onchip_matches_l2stream_c5_prefix():
+    """The two PCG kernels on the bench workload (C5, 5 steps): the same trajectory to round-off."""
+    sc = inputs.make_scenario("C5", n_steps=5)
+    outs = []
+    for oc in (1, 0):
+        ctx = ctx_for(sc, onchip=oc)
+        ctx.run(5)
+        s, p, c = ctx.get_state()
+        outs.append((np_(s), np_(c)))
+        ctx.close()
+    assert rel(outs[0][1], outs[1][1]) <= 1e-10
+    assert np.max(np.abs(outs[0][0] - outs[1][0])) <= 1e-12
 
 
 def test_full_basis_reproduces_fine_scheme_gpu():
