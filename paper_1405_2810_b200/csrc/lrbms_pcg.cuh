@@ -121,10 +121,26 @@ __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
 
 // ============================================================================ factorisation + transform
 
+#ifndef CHOL_SMEM_INV
+#define CHOL_SMEM_INV 1   // L^-1 by forward substitution from L staged in shared memory (the register
+                          // Cholesky's column array is dead by then): ~100 instead of 255 registers,
+                          // 16 instead of 8 warps per SM, one wave for C5
+#endif
+
 // Warp per subdomain.  Lane j holds column j of the (padded-to-32 with identity) block.
+#ifndef CHOL_MINB
+#define CHOL_MINB 4
+#endif
+#if CHOL_SMEM_INV
+__global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
+                                                      const double* __restrict__ zc, double* __restrict__ zh,
+                                                      int* flags, double* __restrict__ Es) {
+  __shared__ double Ls[4][32 * 33];
+#else
 __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
                                                    const double* __restrict__ zc, double* __restrict__ zh,
                                                    int* flags, double* __restrict__ Es) {
+#endif
   const int lane = threadIdx.x & 31;
   const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (E >= g.n_s) return;
@@ -157,6 +173,39 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
         if (i < k) m[i] = 0.0;
     }
   }
+  if (bad && lane == 0) atomicOr(flags, FLAG_PIVOT);
+  const double zk = lane < N ? zc[E * N + lane] : 0.0;
+  double zhat = 0.0;   // (L^T zc)[lane] = sum_i L[i][lane] zc[i]
+#pragma unroll
+  for (int i = 0; i < 32; ++i) zhat += m[i] * __shfl_sync(FULL, zk, i);
+#if CHOL_SMEM_INV
+  // lane holds column lane of L in m[]: L[i][lane] = m[i] -> Ls[i][lane]
+  double* ls = Ls[threadIdx.x >> 5];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) ls[i * 33 + lane] = m[i];
+  if (lane < N) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < N) Bd[i * N + lane] = m[i];   // L in the diagonal slot
+  }
+  __syncwarp();
+  // L^-1 by forward substitution, one column per lane: L x = e_lane, L rows read from shared memory
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) acc -= ls[i * 33 + k] * x[k];
+    x[i] = acc * (1.0 / ls[i * 33 + i]);
+  }
+  if (lane < N) {
+    double* Li = Linv + (size_t)E * N * N;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < N) Li[i * N + lane] = x[i];
+    zh[E * N + lane] = zhat;
+  }
+#else
   // L^-1 by forward substitution, one column per lane: L x = e_lane
   double x[32];
 #pragma unroll
@@ -166,11 +215,6 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
     for (int k = 0; k < i; ++k) acc -= __shfl_sync(FULL, m[i], k) * x[k];
     x[i] = acc * (1.0 / __shfl_sync(FULL, m[i], i));
   }
-  if (bad && lane == 0) atomicOr(flags, FLAG_PIVOT);
-  const double zk = lane < N ? zc[E * N + lane] : 0.0;
-  double zhat = 0.0;   // (L^T zc)[lane] = sum_i L[i][lane] zc[i]
-#pragma unroll
-  for (int i = 0; i < 32; ++i) zhat += m[i] * __shfl_sync(FULL, zk, i);
   if (lane < N) {
     double* Li = Linv + (size_t)E * N * N;
 #pragma unroll
@@ -181,6 +225,7 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
       }
     zh[E * N + lane] = zhat;
   }
+#endif
   if (Es) {   // coarse operator diagonal zc^T B_EE zc = |L^T zc|^2; the side slots are set by k_transform
     const double d = warp_sum(lane < N ? zhat * zhat : 0.0);
     if (lane < 8) Es[(size_t)E * 8 + lane] = lane == 0 ? d : 0.0;
