@@ -1364,8 +1364,17 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
                                                          c->at<double>(c->zc), c->at<double>(c->zh),
                                                          c->at<int>(c->flags), es);
     LAUNCH_CHECK(c);
+#ifndef TRANSFORM_WARP
+#define TRANSFORM_WARP 1
+#endif
+#if TRANSFORM_WARP
+    k_transform_w<<<cdiv(g.n_s * g.dim, 8), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
+                                                                c->at<double>(c->zh),
+                                                                mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
+#else
     k_transform<<<g.n_s, 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
                                               c->at<double>(c->zh), mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
+#endif
     LAUNCH_CHECK(c);
   }
   // The coarse update (Newton-Schulz: non-cooperative kernels) goes to the side stream, forked

@@ -317,6 +317,145 @@ __global__ void __launch_bounds__(256) k_transform(Geo g, double* __restrict__ b
   }
 }
 
+#ifndef TRW_MINB
+#define TRW_MINB 1
+#endif
+// Warp per coupling block (E, a): Bh_{E,E+a} = X_E U X_{E+a}^T (X = L^-1) in place, as k_transform,
+// without shared memory or CTA barriers: both 32x32x32 products on DMMA with operand fragments read
+// straight from L2, the intermediate T1 = X_E U re-laid out from the accumulator layout into A
+// fragments by quad shuffles.  Y_{E,E+a} = Bh zh_{E+a}, Y_{E+a,E} = Bh^T zh_E and the coarse coupling
+// zh_E . Y from the accumulator layout (quad / column reductions).  Grid: n_s * dim warps.
+__global__ void __launch_bounds__(256, TRW_MINB) k_transform_w(Geo g, double* __restrict__ blocks,
+                                                    const double* __restrict__ Linv,
+                                                    const double* __restrict__ zh, double* __restrict__ Yd,
+                                                    double* __restrict__ Es) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= g.n_s * g.dim) return;
+  const int E = t / g.dim, a = t - E * g.dim;
+  int C[3];
+  sub_xyz(g, E, C);
+  if (C[a] + 1 >= g.S[a]) return;   // no upper neighbour along a (warp-uniform)
+  const int N = g.N, NN = N * N, En = E + g.Estride[a];
+  double* U = blocks + ((size_t)E * (1 + g.dim) + 1 + a) * NN;
+  const double* XE = Linv + (size_t)E * NN;
+  const double* XN = Linv + (size_t)En * NN;
+  const int fr = lane >> 2, q = lane & 3;
+  auto ld = [&](const double* M, int r, int c) -> double { return (r < N && c < N) ? M[r * N + c] : 0.0; };
+  // T1 = X_E U: tile (ti, tj) accumulators c[ti][tj][2] (row 8 ti + fr, columns 8 tj + 2 q + {0, 1})
+  double t1[4][4][2];
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) t1[ti][tj][0] = t1[ti][tj][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    double af[4], bf[4];
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti) af[ti] = ld(XE, 8 * ti + fr, 4 * ks + q);
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) bf[tj] = ld(U, 4 * ks + q, 8 * tj + fr);
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) dmma_t(t1[ti][tj][0], t1[ti][tj][1], af[ti], bf[tj]);
+  }
+  // Bh = T1 X_N^T: A fragment (ti, ks) = T1[8 ti + fr][4 ks + q], held by quad lane 2 (ks % 2) + q / 2
+  // in register q % 2 of tile (ti, ks / 2)
+  double bh[4][4][2];
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) bh[ti][tj][0] = bh[ti][tj][1] = 0.0;
+  const int src_lo = (lane & ~3) + (q >> 1), src_hi = (lane & ~3) + 2 + (q >> 1);
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const int src = (ks & 1) ? src_hi : src_lo;
+    double af[4], bf[4];
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti) {
+      const double v0 = __shfl_sync(FULL, t1[ti][ks >> 1][0], src);
+      const double v1 = __shfl_sync(FULL, t1[ti][ks >> 1][1], src);
+      af[ti] = (q & 1) ? v1 : v0;
+    }
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) bf[tj] = ld(XN, 8 * tj + fr, 4 * ks + q);   // X_N^T[4 ks + q][8 tj + fr]
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) dmma_t(bh[ti][tj][0], bh[ti][tj][1], af[ti], bf[tj]);
+  }
+  // store Bh in place (zero beyond N by construction)
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) {
+      const int i = 8 * ti + fr, j = 8 * tj + 2 * q;
+      if (i < N) {
+        if (j < N) U[i * N + j] = bh[ti][tj][0];
+        if (j + 1 < N) U[i * N + j + 1] = bh[ti][tj][1];
+      }
+    }
+  if (!Es) return;
+  // Y_{E,E+a}[i] = sum_j Bh[i][j] zh_N[j]: per lane over its columns, then over the quad
+  const double* zN = zh + (size_t)En * N;
+  const double* zE = zh + (size_t)E * N;
+  double yr[4], yc[4];
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti) {
+    double v = 0.0;
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) {
+      const int j = 8 * tj + 2 * q;
+      v = fma(bh[ti][tj][0], j < N ? zN[j] : 0.0, v);
+      v = fma(bh[ti][tj][1], j + 1 < N ? zN[j + 1] : 0.0, v);
+    }
+    v += __shfl_xor_sync(FULL, v, 1);
+    v += __shfl_xor_sync(FULL, v, 2);
+    yr[ti] = v;   // row 8 ti + fr (all lanes of the quad)
+  }
+  // Y_{E+a,E}[j] = sum_i Bh[i][j] zh_E[i]: per lane over its rows, then over fr (lane bits 2..4)
+#pragma unroll
+  for (int tj = 0; tj < 4; ++tj) {
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int ti = 0; ti < 4; ++ti) {
+      const int i = 8 * ti + fr;
+      const double z = i < N ? zE[i] : 0.0;
+      v0 = fma(bh[ti][tj][0], z, v0);
+      v1 = fma(bh[ti][tj][1], z, v1);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      v0 += __shfl_xor_sync(FULL, v0, o);
+      v1 += __shfl_xor_sync(FULL, v1, o);
+    }
+    yc[tj] = (fr & 1) ? v1 : v0;   // lanes with fr odd report column 8 tj + 2 q + 1
+  }
+  double o = 0.0;
+#pragma unroll
+  for (int ti = 0; ti < 4; ++ti) {
+    const int i = 8 * ti + fr;
+    if (q == 0 && i < N) {
+      if (Yd) Yd[((size_t)E * 6 + a) * N + i] = yr[ti];
+      o = fma(yr[ti], zE[i], o);
+    }
+  }
+  // lanes fr in {0, 1}, q: columns 8 tj + 2 q + fr
+  if (Yd && fr < 2) {
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) {
+      const int j = 8 * tj + 2 * q + fr;
+      if (j < N) Yd[((size_t)En * 6 + 3 + a) * N + j] = yc[tj];
+    }
+  }
+  o = warp_sum(o);
+  if (lane == 0) {
+    Es[(size_t)E * 8 + 1 + a] = o;
+    Es[(size_t)En * 8 + 4 + a] = o;
+  }
+}
+
 // ============================================================================ PCG on the scaled system
 
 // Part A of q = Bh v for subdomain E: returns lane's (v_E + sum_a U_a v_{E+a}); stores U_a^T v_E
