@@ -1421,7 +1421,14 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     k_hist_transform<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
     LAUNCH_CHECK(c);
     if (H.nh > 0) {
+#ifndef HIST_TILED
+#define HIST_TILED 1
+#endif
+#if HIST_TILED
+      k_hist_spmv_t<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
+#else
       k_hist_spmv<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
+#endif
       LAUNCH_CHECK(c);
       k_hist_gram<<<nb, 256, 0, c->stream>>>(H);
       LAUNCH_CHECK(c);

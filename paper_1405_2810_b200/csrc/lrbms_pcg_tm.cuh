@@ -176,6 +176,69 @@ __device__ __forceinline__ void grid_barrier_rel(unsigned* bar, unsigned& epoch)
   __syncthreads();
 }
 
+// Multi-vector SpMV of the initial guess (replaces k_hist_spmv): V_j = W_j + sum_a U_a W_{E+a,j}
+// (own part) and TH[j][E+a][a] = U_a^T W_{E,j} (hand-overs, added by k_hist_gram), warp per
+// subdomain.  Each coupling block is read once into the 4 x 8 register tiling of the PCG SpMV and
+// applied to all nh vectors; the vector operands come through L1 (read-only) instead of 2 x 32
+// shuffles per block column, so the kernel is FMA-bound instead of shuffle-bound.
+__global__ void __launch_bounds__(128) k_hist_spmv_t(HistArgs A) {
+  const Geo& g = A.g;
+  const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int E = blockIdx.x * 4 + warp;
+  if (E >= g.n_s) return;
+  const bool act = lane < N;
+  const size_t R = (size_t)g.n_s * N;
+  const int nh = A.nh;
+  int C[3];
+  sub_xyz(g, E, C);
+  const int ra = (lane >> 2) * 4, cb = lane & 3;
+  const double* Bd = A.blocks + (size_t)E * (1 + g.dim) * N * N;
+  double v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = (j < nh && act) ? __ldg(A.W + j * R + E * N + lane) : 0.0;
+  for (int a = 0; a < g.dim; ++a) {
+    if (C[a] + 1 >= g.S[a]) continue;
+    const int En = E + g.Estride[a];
+    const double* U = Bd + (size_t)(1 + a) * N * N;
+    double u[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int r = ra + i, c = cb + 4 * jj;
+        u[i][jj] = (r < N && c < N) ? __ldg(U + r * N + c) : 0.0;
+      }
+#pragma unroll 1
+    for (int j = 0; j < nh; ++j) {
+      const double* wE = A.W + j * R + (size_t)E * N;
+      const double* wN = A.W + j * R + (size_t)En * N;
+      double vr[4], vc[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) vr[i] = ra + i < N ? __ldg(wE + ra + i) : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) vc[jj] = cb + 4 * jj < N ? __ldg(wN + cb + 4 * jj) : 0.0;
+      double pu[4] = {0.0, 0.0, 0.0, 0.0}, pt[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          pu[i] = fma(u[i][jj], vc[jj], pu[i]);
+          pt[jj] = fma(u[i][jj], vr[i], pt[jj]);
+        }
+      double tc;
+      const double tu = tile_scatter(pu, pt, lane, tc);
+      // v[j] += tu (j is a runtime index: select)
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q == j) v[q] += tu;
+      if (act) A.TH[((size_t)j * g.n_s * 3 + (size_t)En * 3 + a) * N + lane] = tc;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (j < nh && act) A.V[j * R + E * N + lane] = v[j];
+}
+
 // Sums of the k_hist_gram partials and the nh x nh Galerkin system for the history weights
 // (every thread solves it redundantly; the same arithmetic as pcg_initial_guess).
 __device__ __noinline__ void hist_weights(const PcgArgs& A, double* sh, double (&alpha_h)[8]) {
