@@ -76,6 +76,44 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   const size_t base = (size_t)E * nl;
   if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 0] = gtimer_p();
 
+  // 0. inputs of the face weights (a1 + R2) of the thread's first cell, loaded before the Phi staging
+  //    floods the memory system with cp.async requests (the weights phase then no longer waits
+  //    behind them)
+  auto load_winputs = [&](int l, const int c[3], double& ll, double2 (&fp)[3], double2 (&fm)[3], double (&lp)[3],
+                          double (&lm)[3], int (&wpos)[3]) {
+    ll = A.lam[base + l];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      fp[a] = fm[a] = make_double2(0.0, 0.0);
+      lp[a] = lm[a] = 0.0;
+      wpos[a] = -1;
+      if (a >= g.dim) continue;
+      const int st = g.lstride[a];
+      if (c[a] + 1 < g.s[a]) {
+        fp[a] = A.fc[(base + l) * 3 + a];
+        lp[a] = A.lam[base + l + st];
+      } else if (C[a] + 1 < g.S[a]) {
+        const int nb = neighbour(g, E, C, l, c, a, +1);
+        fp[a] = A.fc[(base + l) * 3 + a];
+        lp[a] = A.lam[nb];
+        wpos[a] = face_pos(g, c, a);
+      }
+      if (c[a] == 0 && C[a] > 0) {
+        const int nb = neighbour(g, E, C, l, c, a, -1);
+        fm[a] = A.fc[(size_t)nb * 3 + a];
+        lm[a] = A.lam[nb];
+      }
+    }
+  };
+  double w_ll = 0.0, w_lp[3], w_lm[3];
+  double2 w_fp[3], w_fm[3];
+  int w_wpos[3];
+  if (tid < nl) {
+    int c0[3];
+    local_xyz(g, tid, c0);
+    load_winputs(tid, c0, w_ll, w_fp, w_fm, w_lp, w_lm, w_wpos);
+  }
+
   // 1. stage Phi_E and the neighbour face slabs with cp.async (16-byte granules where the layout
   //    allows: Phi_E rows and the contiguous x-runs of the y/z faces; 8-byte gathers for x-faces)
   const double* PhiE = A.Phi + (size_t)E * N * nl;
@@ -122,37 +160,24 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   // 2. a1 + face weights (R2) from the static coefficients.  Pass 1: every cell forms the weights of
   //    its +a faces (all loads issued up front) and of its -a faces across a subdomain side; the +a
   //    weight inside E is also the -a weight of the upper cell.  Pass 2: the diagonal.
-  for (int l = tid; l < nl; l += nt) lam[l] = A.lam[base + l];
-  __syncthreads();
+  __syncthreads();   // wi / fcell initialised by the staging loop
   for (int l = tid; l < nl; l += nt) {
     int c[3];
     local_xyz(g, l, c);
-    const double ll = lam[l];
+    double ll;
     double2 fp[3], fm[3];
     double lp[3], lm[3];
     int wpos[3];
+    if (l == tid) {   // the thread's first cell: inputs loaded before the Phi staging
+      ll = w_ll;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      fp[a] = fm[a] = make_double2(0.0, 0.0);
-      lp[a] = lm[a] = 0.0;
-      wpos[a] = -1;
-      if (a >= g.dim) continue;
-      const int st = g.lstride[a];
-      if (c[a] + 1 < g.s[a]) {
-        fp[a] = A.fc[(base + l) * 3 + a];
-        lp[a] = lam[l + st];
-      } else if (C[a] + 1 < g.S[a]) {
-        const int nb = neighbour(g, E, C, l, c, a, +1);
-        fp[a] = A.fc[(base + l) * 3 + a];
-        lp[a] = A.lam[nb];
-        wpos[a] = face_pos(g, c, a);
+      for (int a = 0; a < 3; ++a) {
+        fp[a] = w_fp[a]; fm[a] = w_fm[a]; lp[a] = w_lp[a]; lm[a] = w_lm[a]; wpos[a] = w_wpos[a];
       }
-      if (c[a] == 0 && C[a] > 0) {
-        const int nb = neighbour(g, E, C, l, c, a, -1);
-        fm[a] = A.fc[(size_t)nb * 3 + a];
-        lm[a] = A.lam[nb];
-      }
+    } else {
+      load_winputs(l, c, ll, fp, fm, lp, lm, wpos);
     }
+    lam[l] = ll;
     double dc = 0.0;
     double wl[3];
 #pragma unroll
