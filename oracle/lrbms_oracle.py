@@ -433,37 +433,86 @@ def transport(sc, s, Ff, Fl, dt):
 
 
 # ----------------------------------------------------------------------------
+# the paper's affine online variant (NEXT-1): theta fit + precomputed reduced quantities
+# ----------------------------------------------------------------------------
+
+
+def profile_mobilities(sc, s_profiles):
+    """lambda_{t,q} = lambda_{w,q} + lambda_{n,q} of the profile saturation fields (eq:parameterizedMob
+    P:570-589, profiles of P:650-662; the total mobility is what eq:leastSquaresFit fits)."""
+    return np.stack([total_mobility(sq, sc) for sq in s_profiles])
+
+
+def theta_fit(sc, lam, lam_q):
+    """eq:leastSquaresFit: Theta(s) = argmin_theta || lambda_t(s) - sum_q theta_q
+    lambda_{t,q} ||_{l2} over the fine degrees of freedom (k = 0: cells).  Library LAPACK lstsq."""
+    theta, *_ = np.linalg.lstsq(np.asarray(lam_q).T, lam, rcond=None)
+    return theta
+
+
+def affine_offline(sc, lam_q):
+    """Offline quantities of sec:offlineOnlineDecomposition as reduced blocks:
+    b_q = Phi^T A(lambda_{t,q}) Phi, d_q = Phi^T b(lambda_{t,q}).  Under reading R2 the k = 0 operator
+    and its Dirichlet right-hand side are linear in lambda (no lambda-free penalty term): c = 0, e = 0."""
+    bq, dq = [], []
+    for lq in lam_q:
+        A, rhs = fine_operator(sc, lq)
+        b, r = project(sc, A, rhs)
+        bq.append(b)
+        dq.append(r)
+    return np.stack(bq), np.stack(dq)
+
+
+def affine_system(theta, bq, dq):
+    """eq:reducedSystem with c = e = 0: (sum_q theta_q b_q) p_H = sum_q theta_q d_q."""
+    return np.tensordot(theta, bq, axes=1), np.tensordot(theta, dq, axes=1)
+
+
 # the online step (alg:fullTwoPhaseScheme P:846-882 with direct projection, reading R3)
 # ----------------------------------------------------------------------------
 
 
-def lrbms_step(sc, s, fpmax=None, method=None, x0=None, dt_fixed=0.0):
+def lrbms_step(sc, s, fpmax=None, method=None, x0=None, dt_fixed=0.0, affine=None):
     """One online LRBMS step: (a1) lambda(s^n); (a2) assemble + project; (a3) reduced solve;
-    (a4) reconstruct p; (a5) fluxes + dt; (a6) upwind transport.  Returns a dict."""
+    (a4) reconstruct p; (a5) fluxes + dt; (a6) upwind transport.  Returns a dict.
+    affine = (lam_q, bq, dq): the paper's variant instead of (a2) (alg:fullTwoPhaseScheme step (a),
+    P:863-868): theta fit (eq:leastSquaresFit) and the affine reduced system (eq:reducedSystem); the
+    fluxes still use the true lambda(s^n)."""
     if fpmax is None:
         fpmax = fprime_max(sc)
     lam = total_mobility(s, sc)
-    A, rhs = fine_operator(sc, lam)
-    blocks, r = project(sc, A, rhs)
+    theta = None
+    if affine is None:
+        A, rhs = fine_operator(sc, lam)
+        blocks, r = project(sc, A, rhs)
+    else:
+        lam_q, bq, dq = affine
+        theta = theta_fit(sc, lam, lam_q)
+        blocks, r = affine_system(theta, bq, dq)
     c = solve_reduced(sc, blocks, r, method=method, x0=x0)
     p = reconstruct(sc, c)
     Ff, Fl = fluxes(sc, p, lam)
     dt = dt_fixed if dt_fixed > 0 else cfl_time_step(sc, Ff, Fl, fpmax)
     s_new = transport(sc, s, Ff, Fl, dt)
-    return dict(s=s_new, p=p, c=c, dt=dt, blocks=blocks, r=r, Ff=Ff, Fl=Fl)
+    return dict(s=s_new, p=p, c=c, dt=dt, blocks=blocks, r=r, Ff=Ff, Fl=Fl, theta=theta)
 
 
-def run(sc, n_steps=None, method=None, keep=False, dt_fixed=0.0):
+def run(sc, n_steps=None, method=None, keep=False, dt_fixed=0.0, s_profiles=None):
     """alg:fullTwoPhaseScheme step 5 for n = 0..n_steps-1 from s^0 = sc.s0 (k = 0 projection of
-    s_0 is the cell value).  Returns final state and per-step logs."""
+    s_0 is the cell value).  Returns final state and per-step logs.  s_profiles: the
+    profile saturation fields of the paper's affine variant (NEXT-1), else the direct projection."""
     n_steps = sc.n_steps if n_steps is None else n_steps
     fpmax = fprime_max(sc)
+    affine = None
+    if s_profiles is not None:
+        lam_q = profile_mobilities(sc, s_profiles)
+        affine = (lam_q,) + affine_offline(sc, lam_q)
     s = np.array(sc.s0, np.float64)
     dts, cs, ps = [], [], []
     out = None
     c_prev = None
     for _ in range(n_steps):
-        out = lrbms_step(sc, s, fpmax=fpmax, method=method, x0=c_prev, dt_fixed=dt_fixed)
+        out = lrbms_step(sc, s, fpmax=fpmax, method=method, x0=c_prev, dt_fixed=dt_fixed, affine=affine)
         s = out["s"]
         c_prev = out["c"]
         dts.append(out["dt"])

@@ -1385,7 +1385,10 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     const bool rebuild = !c->have_x || c->last_rebuild_step < 0 ||
                          c->steps - c->last_rebuild_step >= c->opts.coarse_refresh;
     cudaStream_t main = c->stream;
-    if (!rebuild && mode == 2 && c->side) {
+#ifndef USE_SIDE_STREAM
+#define USE_SIDE_STREAM 1
+#endif
+    if (USE_SIDE_STREAM && !rebuild && mode == 2 && c->side) {
       CUDA_TRY(c, cudaEventRecord(c->fork_ev, main));
       CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->fork_ev, 0));
       c->stream = c->side;

@@ -291,6 +291,38 @@ def random_basis(sc: Scenario, seed: int) -> np.ndarray:
 # scenarios
 # ----------------------------------------------------------------------------
 
+# ----------------------------------------------------------------------------
+# mobility profiles of the paper's affine online variant (NEXT-1): saturation fields only
+# ----------------------------------------------------------------------------
+
+def profile_saturations(sc: Scenario, M: int = 8) -> np.ndarray:
+    """Saturation fields s_q (q = 1..M) whose mobilities are the profiles lambda_{alpha,q} of
+    eq:parameterizedMob, following the recipe of P:650-662: q = 1 is S0 everywhere,
+    q = M the injected saturation everywhere, and q = 2..M-1 carry the injected saturation where the
+    time of flight is below the q-th threshold.  Reading (A22): the time of flight is
+    replaced by its geometric proxy, the Euclidean distance of the cell centre from the injection
+    cells (links with s_ext > S0), normalised to [0, 1], with thresholds (q - 1) / (M - 1).
+    Returns [M][n] (natural cell order).  Holds no method arithmetic: the mobilities of these fields
+    are evaluated by the oracle and by the library themselves."""
+    from scipy.ndimage import distance_transform_edt
+    s_lo = float(np.min(sc.s0)) if sc.s0 is not None else 0.0
+    inj = sc.link_cell[sc.link_s > s_lo]
+    s_hi = float(np.max(sc.link_s))
+    mask = np.ones(sc.n, bool)
+    mask[inj] = False
+    d = distance_transform_edt(mask.reshape(sc.nz, sc.ny, sc.nx), sampling=(sc.hz, sc.hy, sc.hx)).reshape(-1)
+    tau = d / max(float(d.max()), 1e-300)
+    out = np.empty((M, sc.n))
+    for q in range(1, M + 1):
+        if q == 1:
+            out[q - 1] = s_lo
+        elif q == M:
+            out[q - 1] = s_hi
+        else:
+            out[q - 1] = np.where(tau <= (q - 1) / (M - 1), s_hi, s_lo)
+    return out
+
+
 def make_scenario(name: str, basis: str = "poly", n_steps: Optional[int] = None) -> Scenario:
     """The seeded synthetic scenario for BASELINE.json config ``name`` (C1..C5)."""
     cfg = CONFIGS[name]

@@ -393,3 +393,63 @@ def test_inputs_deterministic_and_shaped():
         G = np.einsum("eki,eli->ekl", sc.Phi, sc.Phi)
         assert np.max(np.abs(G - np.eye(sc.N))) < 1e-12
         assert np.allclose(sc.Phi[:, 0, :], 1 / math.sqrt(sc.n_loc), atol=1e-14)
+
+
+# ---------------------------------------------------------------------------- NEXT-1: the paper's
+# affine online variant (eq:leastSquaresFit P:581-586, sec:offlineOnlineDecomposition P:784-833)
+
+def _affine_case():
+    sc = inputs.custom_scenario(12, 8, 1, 4, 4, 1, 5, seed=31, mu_o=10.0)
+    sp = inputs.profile_saturations(sc, M=6)
+    return sc, sp, O.profile_mobilities(sc, sp)
+
+
+def test_profiles_follow_the_recipe():
+    """q = 1 is S0, q = M the injected saturation, the fronts grow monotonically."""
+    sc, sp, _ = _affine_case()
+    assert np.all(sp[0] == 0.0) and np.all(sp[-1] == 1.0)
+    filled = [int((q > 0).sum()) for q in sp]
+    assert filled == sorted(filled) and filled[1] > 0 and filled[-2] < sc.n
+    inj = sc.link_cell[sc.link_s > 0]
+    assert np.all(sp[1][inj] == 1.0)   # the injection cells are inside the first front
+
+
+def test_theta_fit_recovers_an_exact_combination():
+    """eq:leastSquaresFit: lambda = sum theta*_q lambda_q (profiles 2..M, full rank) => theta = theta*."""
+    sc, sp, lq = _affine_case()
+    sub = lq[1:]
+    rng = np.random.default_rng(5)
+    th = rng.uniform(0.1, 1.0, sub.shape[0])
+    lam = th @ sub
+    assert np.allclose(O.theta_fit(sc, lam, sub), th, rtol=1e-10, atol=0)
+    # and the residual of a generic lambda is l2-orthogonal to every profile (normal equations)
+    lam2 = O.total_mobility(rng.uniform(0, 1, sc.n), sc)
+    t2 = O.theta_fit(sc, lam2, lq)
+    res = lam2 - t2 @ lq
+    assert np.max(np.abs(lq @ res)) <= 1e-10 * np.linalg.norm(lam2) * np.linalg.norm(lq)
+
+
+def test_affine_decomposition_equals_direct_projection():
+    """c = e = 0 under reading R2: sum theta_q b_q, sum theta_q d_q equal the direct projection of the
+    operator of sum theta_q lambda_q for any theta (the affine splitting eq:parameterizedMob relies on)."""
+    sc, sp, lq = _affine_case()
+    bq, dq = O.affine_offline(sc, lq)
+    th = np.random.default_rng(6).uniform(-0.5, 1.5, lq.shape[0])
+    B, r = O.affine_system(th, bq, dq)
+    A, rhs = O.fine_operator(sc, th @ lq)
+    Bd, rd = O.project(sc, A, rhs)
+    assert np.max(np.abs(B - Bd)) <= 1e-13 * np.max(np.abs(Bd))
+    assert np.max(np.abs(r - rd)) <= 1e-13 * np.max(np.abs(rd))
+
+
+def test_affine_step_equals_direct_step_in_span():
+    """S:556 offline-online consistency: when lambda(s) lies in the span of the profiles (here s = a
+    profile's saturation field) the affine online step reproduces the direct projection."""
+    sc, sp, lq = _affine_case()
+    bq, dq = O.affine_offline(sc, lq)
+    s = sp[3].copy()
+    a = O.lrbms_step(sc, s, method="dense", affine=(lq, bq, dq))
+    d = O.lrbms_step(sc, s, method="dense")
+    assert np.max(np.abs(a["blocks"] - d["blocks"])) <= 1e-12 * np.max(np.abs(d["blocks"]))
+    assert np.max(np.abs(a["c"] - d["c"])) <= 1e-10 * np.max(np.abs(d["c"]))
+    assert np.max(np.abs(a["s"] - d["s"])) <= 1e-12
