@@ -132,6 +132,27 @@ lrbms_status lrbms_set_basis(lrbms_ctx *ctx, const double *Phi);
 lrbms_status lrbms_set_saturation(lrbms_ctx *ctx, const double *s);
 lrbms_status lrbms_set_solver(lrbms_ctx *ctx, const lrbms_solver_opts *opts);
 
+/* NEXT-1, the paper's affine online variant of step a2 (eq:parameterizedMob P:570-589,
+ * eq:leastSquaresFit P:581-586, sec:offlineOnlineDecomposition P:784-813, eq:reducedSystem
+ * P:818-821): the reduced system of a step is sum_q theta_q b_q, sum_q theta_q d_q with theta the
+ * least-squares fit of lambda_t(s^n) by M mobility profiles (normal equations; a profile that depends
+ * on the previous ones is dropped), and b_q, d_q the projections of the operator and right-hand side
+ * of profile q (c = e = 0 under reading R2).  The fluxes keep the true lambda(s^n).
+ *
+ * lrbms_profiles_bytes: size of the caller-owned profile workspace for M profiles (0 if M is not in
+ * [1, 16]).  lrbms_set_profiles: s_profiles (dev, [M][n], natural order) are the SATURATION fields of
+ * the profiles (the library evaluates lambda_t of them itself); ws (dev, 256-byte aligned, >= the
+ * size above) stays owned by the caller and must outlive the context's use of the affine variant.
+ * Computes lambda_q, b_q, d_q (M projections) and the Gram matrix once; synchronises the stream.
+ * Needs set_medium and set_basis.  Errors: CONFIG (M, NULL, small or misaligned workspace), STATE.
+ * lrbms_set_online: 1 = affine variant (needs set_profiles), 0 = direct projection (default).
+ * lrbms_stage_theta: theta of the current saturation (dev, M doubles); a test hook. */
+size_t       lrbms_profiles_bytes(const lrbms_ctx *ctx, int32_t M);
+lrbms_status lrbms_set_profiles(lrbms_ctx *ctx, const double *s_profiles, int32_t M, void *ws,
+                                size_t bytes);
+lrbms_status lrbms_set_online(lrbms_ctx *ctx, int32_t affine);
+lrbms_status lrbms_stage_theta(lrbms_ctx *ctx, double *theta);
+
 /* Advance n_steps online steps a1..a6 on the bound stream, no host round trip per step.
  * dt_fixed > 0 overrides the CFL step (the paper's fixed N_T); otherwise
  * dt^n = cfl * min_i phi_i V_i / (f'_max Q_i) (reading R4).  dt_log (dev, n_steps) or NULL.

@@ -29,6 +29,7 @@
 #include "lrbms_pcg_tm.cuh"
 #include "lrbms_project.cuh"
 #include "lrbms_ns.cuh"
+#include "lrbms_affine.cuh"
 
 using namespace lrbms;
 
@@ -767,6 +768,11 @@ struct lrbms_ctx {
   // stage profiling (CUDA events)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
+  // NEXT-1 (the paper's affine online variant): caller-owned profile workspace
+  char* pws = nullptr;
+  int prof_M = 0, prof_G = 0;
+  bool affine = false;
+  size_t off_lamq = 0, off_bq = 0, off_dq = 0, off_gram = 0, off_part = 0, off_theta = 0;
   // side stream: the Newton-Schulz update of the coarse inverse runs concurrently with the
   // initial-guess kernels (both only need the scaled operator; the PCG needs both)
   cudaStream_t side = nullptr;
@@ -1278,16 +1284,45 @@ static lrbms_status ready(lrbms_ctx* c) {
   return LRBMS_OK;
 }
 
-static lrbms_status launch_project(lrbms_ctx* c) {
-  StageScope sc_(c, 0);
+static lrbms_status launch_project_to(lrbms_ctx* c, const double* lam, double* blocks, double* rhs) {
   ProjArgs A = c->proj;
   A.g = c->g; A.f = c->f; A.L = links_of(c);
   A.s = c->s_cur(); A.K = c->at<double>(c->K); A.Phi = c->at<double>(c->Phi);
-  A.fc = c->at<double2>(c->fc); A.lam = c->lam_cur();
-  A.blocks = c->at<double>(c->blocks); A.rhs = c->at<double>(c->rhs);
+  A.fc = c->at<double2>(c->fc); A.lam = lam;
+  A.blocks = blocks; A.rhs = rhs;
   A.tstamp = c->debug_tstamp;
   k_project<<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
+  return LRBMS_OK;
+}
+
+static size_t block_len(const lrbms_ctx* c) { return (size_t)c->g.n_s * (1 + c->g.dim) * c->g.N * c->g.N; }
+
+// a2 of the step: the direct projection of A(lambda(s^n)) (north star, reading R3), or the paper's
+// affine variant (NEXT-1): theta fit + sum_q theta_q b_q, d_q
+static lrbms_status launch_project(lrbms_ctx* c) {
+  StageScope sc_(c, 0);
+  lrbms_status st = LRBMS_OK;
+  if (c->affine) {
+    const size_t n = c->g.n, R = (size_t)c->g.n_s * c->g.N;
+    double* part = reinterpret_cast<double*>(c->pws + c->off_part);
+    double* theta = reinterpret_cast<double*>(c->pws + c->off_theta);
+    k_theta_partials<<<c->prof_G, 256, 0, c->stream>>>(c->lam_cur(), reinterpret_cast<double*>(c->pws + c->off_lamq),
+                                                       c->prof_M, n, part);
+    LAUNCH_CHECK(c);
+    k_theta_solve<<<1, 32, 0, c->stream>>>(part, c->prof_G, c->prof_M, reinterpret_cast<double*>(c->pws + c->off_gram),
+                                          theta);
+    LAUNCH_CHECK(c);
+    k_affine_combine<<<4 * c->sms, 256, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_bq), theta,
+                                                        c->prof_M, block_len(c), c->at<double>(c->blocks));
+    LAUNCH_CHECK(c);
+    k_affine_combine<<<cdiv((int)(R / 2 + 1), 256), 256, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_dq),
+                                                                          theta, c->prof_M, R, c->at<double>(c->rhs));
+    LAUNCH_CHECK(c);
+  } else {
+    st = launch_project_to(c, c->lam_cur(), c->at<double>(c->blocks), c->at<double>(c->rhs));
+  }
+  if (st) return st;
   c->have_blocks = true;
   return LRBMS_OK;
 }
@@ -1598,6 +1633,96 @@ lrbms_status lrbms_get_state(lrbms_ctx* c, double* s, double* p, double* cc) {
   if (s) { k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->s_cur(), s); LAUNCH_CHECK(c); }
   if (p) { k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->at<double>(c->p), p); LAUNCH_CHECK(c); }
   if (cc) CUDA_TRY(c, cudaMemcpyAsync(cc, c->at<double>(c->c), c->c.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return LRBMS_OK;
+}
+
+static void profile_layout(const lrbms_ctx* c, int M, size_t* offs, size_t* total) {
+  const size_t n = c->g.n, R = (size_t)c->g.n_s * c->g.N;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) / 256 * 256; return r; };
+  offs[0] = take(8 * (size_t)M * n);                 // lambda_{t,q}, internal order
+  offs[1] = take(8 * (size_t)M * block_len(c));      // b_q
+  offs[2] = take(8 * (size_t)M * R);                 // d_q
+  offs[3] = take(8 * (size_t)M * M);                 // Gram
+  offs[4] = take(8 * (size_t)M * 4 * (size_t)c->sms);   // per-CTA partials
+  offs[5] = take(8 * AFF_MAXM);                      // theta
+  *total = o;
+}
+
+size_t lrbms_profiles_bytes(const lrbms_ctx* c, int32_t M) {
+  if (!c || M < 1 || M > AFF_MAXM) return 0;
+  size_t offs[6], total = 0;
+  profile_layout(c, M, offs, &total);
+  return total;
+}
+
+lrbms_status lrbms_set_profiles(lrbms_ctx* c, const double* s_profiles, int32_t M, void* ws, size_t bytes) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (M < 1 || M > AFF_MAXM) return fail(c, LRBMS_E_CONFIG, "number of profiles M = %d not in [1, %d]", M, AFF_MAXM);
+  if (!s_profiles) return fail(c, LRBMS_E_CONFIG, "s_profiles is NULL");
+  if (!c->have_medium || !c->have_basis) return fail(c, LRBMS_E_STATE, "set_medium and set_basis must precede set_profiles");
+  size_t offs[6], total = 0;
+  profile_layout(c, M, offs, &total);
+  if (!ws || bytes < total) return fail(c, LRBMS_E_CONFIG, "profile workspace too small (%zu < %zu)", bytes, total);
+  if (((uintptr_t)ws) % 256) return fail(c, LRBMS_E_CONFIG, "profile workspace must be 256-byte aligned");
+  c->pws = (char*)ws;
+  c->prof_M = M;
+  c->prof_G = 4 * c->sms;
+  c->off_lamq = offs[0]; c->off_bq = offs[1]; c->off_dq = offs[2];
+  c->off_gram = offs[3]; c->off_part = offs[4]; c->off_theta = offs[5];
+  const Geo& g = c->g;
+  const size_t n = g.n, R = (size_t)g.n_s * g.N;
+  const int nb = cdiv(g.n, 256);
+  double* lamq = reinterpret_cast<double*>(c->pws + c->off_lamq);
+  double* scratch = c->at<double>(c->netw);   // f_w of the profiles is not needed
+  for (int q = 0; q < M; ++q) {   // a1 of the profile saturations, then b_q, d_q by the projection kernel
+    k_to_internal<<<nb, 256, 0, c->stream>>>(g, s_profiles + (size_t)q * n, c->at<double>(c->tmp));
+    LAUNCH_CHECK(c);
+    k_mobility<<<nb, 256, 0, c->stream>>>(g, c->f, c->at<double>(c->tmp), lamq + (size_t)q * n, scratch);
+    LAUNCH_CHECK(c);
+    if ((st = launch_project_to(c, lamq + (size_t)q * n, reinterpret_cast<double*>(c->pws + c->off_bq) + q * block_len(c),
+                                reinterpret_cast<double*>(c->pws + c->off_dq) + q * R)))
+      return st;
+  }
+  double* part = reinterpret_cast<double*>(c->pws + c->off_part);
+  for (int r = 0; r < M; ++r) {   // Gram matrix G_qr = <lambda_q, lambda_r>
+    k_theta_partials<<<c->prof_G, 256, 0, c->stream>>>(lamq + (size_t)r * n, lamq, M, n, part);
+    LAUNCH_CHECK(c);
+    k_gram_row<<<1, 32, 0, c->stream>>>(part, c->prof_G, M, reinterpret_cast<double*>(c->pws + c->off_gram), r);
+    LAUNCH_CHECK(c);
+  }
+  c->have_blocks = false;
+  // the kernels above replaced the scratch f_w: recompute the mobilities of the current saturation
+  k_mobility<<<nb, 256, 0, c->stream>>>(g, c->f, c->s_cur(), c->lam_cur(), c->fw_cur());
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_set_online(lrbms_ctx* c, int32_t affine) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (affine != 0 && affine != 1) return fail(c, LRBMS_E_CONFIG, "online mode must be 0 (direct) or 1 (affine)");
+  if (affine && c->prof_M < 1) return fail(c, LRBMS_E_STATE, "the affine online variant needs set_profiles");
+  c->affine = affine == 1;
+  c->have_blocks = false;
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_stage_theta(lrbms_ctx* c, double* theta) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  if (c->prof_M < 1) return fail(c, LRBMS_E_STATE, "stage_theta needs set_profiles");
+  double* part = reinterpret_cast<double*>(c->pws + c->off_part);
+  double* th = reinterpret_cast<double*>(c->pws + c->off_theta);
+  k_theta_partials<<<c->prof_G, 256, 0, c->stream>>>(c->lam_cur(), reinterpret_cast<double*>(c->pws + c->off_lamq),
+                                                     c->prof_M, c->g.n, part);
+  LAUNCH_CHECK(c);
+  k_theta_solve<<<1, 32, 0, c->stream>>>(part, c->prof_G, c->prof_M, reinterpret_cast<double*>(c->pws + c->off_gram), th);
+  LAUNCH_CHECK(c);
+  if (theta) CUDA_TRY(c, cudaMemcpyAsync(theta, th, 8 * (size_t)c->prof_M, cudaMemcpyDeviceToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return LRBMS_OK;
 }

@@ -22,7 +22,8 @@ STATUS_NAMES = {0: "OK", 2: "CONFIG", 3: "NUMERICAL", 4: "IO", 5: "CUDA", 6: "ST
 EXPORTS = ["lrbms_create", "lrbms_workspace_bytes", "lrbms_bind", "lrbms_set_medium", "lrbms_set_basis",
            "lrbms_set_saturation", "lrbms_set_solver", "lrbms_run", "lrbms_run_host", "lrbms_get_state",
            "lrbms_stage_project", "lrbms_stage_solve", "lrbms_stage_reconstruct", "lrbms_stage_transport",
-           "lrbms_get_stats", "lrbms_set_profiling", "lrbms_get_stage_times", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy"]
+           "lrbms_get_stats", "lrbms_set_profiling", "lrbms_get_stage_times", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy",
+           "lrbms_profiles_bytes", "lrbms_set_profiles", "lrbms_set_online", "lrbms_stage_theta"]
 
 
 class LrbmsError(RuntimeError):
@@ -94,6 +95,10 @@ def load_library(path: str = LIB_PATH):
         "lrbms_get_stats": (st, [P, ctypes.POINTER(Stats)]),
         "lrbms_launch_count": (ctypes.c_int64, [P]),
         "lrbms_set_profiling": (st, [P, I]),
+        "lrbms_profiles_bytes": (ctypes.c_size_t, [P, I]),
+        "lrbms_set_profiles": (st, [P, P, I, P, ctypes.c_size_t]),
+        "lrbms_set_online": (st, [P, I]),
+        "lrbms_stage_theta": (st, [P, P]),
         "lrbms_get_stage_times": (st, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), I]),
         "lrbms_last_error": (ctypes.c_char_p, [P]),
         "lrbms_version": (ctypes.c_char_p, []),
@@ -230,6 +235,30 @@ class LrbmsContext:
         s, p, c = self.empty(sc.n), self.empty(sc.n), self.empty(sc.n_s * sc.N)
         self._check(self.L.lrbms_get_state(self.h, _ptr(s), _ptr(p), _ptr(c)))
         return s, p, c.view(sc.n_s, sc.N)
+
+    def set_profiles(self, s_profiles):
+        """NEXT-1: the M profile saturation fields ([M][n], natural order) of the paper's affine online
+        variant; allocates the caller-owned profile workspace (marshalling only)."""
+        torch = self.torch
+        sp = np.ascontiguousarray(s_profiles, np.float64)
+        M = int(sp.shape[0])
+        nbytes = self.L.lrbms_profiles_bytes(self.h, M)
+        if nbytes == 0:
+            raise LrbmsError(LRBMS_E_CONFIG, f"number of profiles M = {M} not supported")
+        with torch.cuda.device(self.device):
+            self.profile_ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        ptr = (self.profile_ws.data_ptr() + 255) // 256 * 256
+        self._profiles_dev = self.dev(sp.reshape(M, -1))
+        self.n_profiles = M
+        self._check(self.L.lrbms_set_profiles(self.h, _ptr(self._profiles_dev), M, ctypes.c_void_p(ptr), nbytes))
+
+    def set_online(self, affine: bool):
+        self._check(self.L.lrbms_set_online(self.h, 1 if affine else 0))
+
+    def stage_theta(self):
+        th = self.empty(self.n_profiles)
+        self._check(self.L.lrbms_stage_theta(self.h, _ptr(th)))
+        return th
 
     def stage_project(self):
         sc = self.sc

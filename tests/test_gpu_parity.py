@@ -284,3 +284,98 @@ def test_c4_prefix_tight_solver():
     assert rel(np_(c), ref["cs"][-1]) <= 1e-10
     assert rel(np_(p), ref["ps"][-1]) <= 1e-10
     assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
+
+
+# ---------------------------------------------------------------------------- NEXT-1: affine variant
+
+AFFINE = [
+    ("C1", lambda: inputs.make_scenario("C1")),
+    ("C2", lambda: inputs.make_scenario("C2")),
+    ("ragged3d", lambda: inputs.custom_scenario(9, 6, 4, 3, 3, 2, 11, seed=22, mu_o=10.0, bc="corner_columns_3d",
+                                                hx=0.5, hy=1.5, hz=2.0)),
+]
+
+
+@pytest.mark.parametrize("name,make", AFFINE, ids=[a[0] for a in AFFINE])
+def test_affine_stage_parity(name, make):
+    """theta fit (as the fitted mobility sum_q theta_q lambda_q, unique even when profiles are
+    dependent), the affine reduced system and its solve against the oracle, on a random saturation."""
+    sc = make()
+    sp = inputs.profile_saturations(sc)
+    rng = np.random.default_rng(11)
+    sc.s0 = rng.uniform(0.0, 1.0, sc.n)
+    ctx = ctx_for(sc)
+    ctx.set_profiles(sp)
+    ctx.set_online(True)
+    lq = O.profile_mobilities(sc, sp)
+    lam = O.total_mobility(sc.s0, sc)
+    th_o = O.theta_fit(sc, lam, lq)
+    th_g = np_(ctx.stage_theta())
+    fit_o, fit_g = th_o @ lq, th_g @ lq
+    assert np.max(np.abs(fit_g - fit_o)) <= 1e-12 * np.max(np.abs(fit_o))
+    bq, dq = O.affine_offline(sc, lq)
+    ob, orr = O.affine_system(th_o, bq, dq)
+    blocks, r = ctx.stage_project()
+    assert rel(np_(blocks), ob) <= 1e-12
+    assert rel(np_(r), orr) <= 1e-12
+    c = ctx.stage_solve()
+    oc = O.solve_reduced(sc, ob, orr, method="dense")
+    assert rel(np_(c), oc) <= 1e-10
+
+
+@pytest.mark.parametrize("name,make", AFFINE, ids=[a[0] for a in AFFINE])
+def test_affine_full_run(name, make):
+    sc = make()
+    n = 20
+    sp = inputs.profile_saturations(sc)
+    ref = O.run(sc, n_steps=n, keep=True, s_profiles=sp)
+    ctx = ctx_for(sc)
+    ctx.set_profiles(sp)
+    ctx.set_online(True)
+    dts = np_(ctx.run(n, log_dt=True))
+    s, p, c = ctx.get_state()
+    assert rel(dts, ref["dts"]) <= 1e-10
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
+
+
+def test_affine_equals_direct_in_span_gpu():
+    """S:556 on the GPU: at a profile's own saturation field the affine reduced system is the direct
+    projection (both computed by the library)."""
+    sc = inputs.make_scenario("C2")
+    sp = inputs.profile_saturations(sc)
+    sc.s0 = sp[3].copy()
+    ctx = ctx_for(sc)
+    bd, rd = (np_(t) for t in ctx.stage_project())
+    ctx.set_profiles(sp)
+    ctx.set_online(True)
+    ba, ra = (np_(t) for t in ctx.stage_project())
+    assert rel(ba, bd) <= 1e-12 and rel(ra, rd) <= 1e-12
+
+
+def test_affine_c5_prefix():
+    """The bench workload in the affine variant: 2 steps against the oracle's affine run."""
+    sc = inputs.make_scenario("C5")
+    sp = inputs.profile_saturations(sc)
+    ref = O.run(sc, n_steps=2, keep=True, s_profiles=sp)
+    ctx = ctx_for(sc)
+    ctx.set_profiles(sp)
+    ctx.set_online(True)
+    ctx.run(2)
+    s, p, c = ctx.get_state()
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
+
+
+def test_affine_errors():
+    from paper_1405_2810_b200.lrbms import LrbmsError, LRBMS_E_STATE, LRBMS_E_CONFIG
+    sc = inputs.make_scenario("C1")
+    ctx = ctx_for(sc)
+    with pytest.raises(LrbmsError) as e:
+        ctx.set_online(True)
+    assert e.value.status == LRBMS_E_STATE
+    with pytest.raises(LrbmsError) as e:
+        ctx.set_profiles(np.zeros((17, sc.n)))
+    assert e.value.status == LRBMS_E_CONFIG
