@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--coarse-refresh", type=int, default=None)
     ap.add_argument("--rtol", type=float, default=None)
+    ap.add_argument("--affine-steps", type=int, default=50,
+                    help="steps timed in the paper's affine online variant (NEXT-1; 0 = skip)")
     return ap.parse_args()
 
 
@@ -287,6 +289,37 @@ def run_ours(args, rank, local, world):
     ms_e2e = max_over_ranks(ms_e2e, world, device)
     e2e_value = world * Ke / (ms_e2e / 1e3)
 
+    # ---- NEXT-1: the paper's affine online variant on the same workload (theta fit + sum_q theta_q
+    #      b_q instead of the direct projection); reported beside the north-star metric, not as it
+    affine = None
+    if args.affine_steps > 0:
+        sp = inputs.profile_saturations(sc)
+        ctx.set_profiles(sp)
+        ctx.set_online(True)
+        ctx.run(3)
+        sa0 = ctx.stats()
+        barrier(world)
+        torch.cuda.synchronize()
+        ctx.set_profiling(True)
+        e4 = torch.cuda.Event(enable_timing=True)
+        e5 = torch.cuda.Event(enable_timing=True)
+        e4.record(stream)
+        ctx.run(args.affine_steps)
+        e5.record(stream)
+        torch.cuda.synchronize()
+        ms_a = max_over_ranks(e4.elapsed_time(e5), world, device)
+        st_a = ctx.stage_times()
+        ctx.set_profiling(False)
+        sa1 = ctx.stats()
+        ctx.set_online(False)
+        affine = {"value": world * args.affine_steps / (ms_a / 1e3), "unit": "steps/s",
+                  "ms_per_step": ms_a / args.affine_steps, "steps": args.affine_steps, "profiles": int(sp.shape[0]),
+                  "pcg_iters_per_step": (sa1["total_iters"] - sa0["total_iters"]) / args.affine_steps,
+                  "stage_us_per_step": {k: round(1e3 * v[0] / args.affine_steps, 1) for k, v in st_a.items()},
+                  "note": "the paper's online variant (eq:leastSquaresFit theta fit + eq:reducedSystem "
+                          "sum_q theta_q b_q, d_q; NEXT-1), continuing the trajectory above; "
+                          "the north-star metric is the direct-projection line"}
+
     if rank != 0:
         return 0
 
@@ -343,6 +376,7 @@ def run_ours(args, rank, local, world):
         "stage_share": stage_share,
         "stage_us_per_step": stage_us,
         "pcg_iters_per_step": iters,
+        "affine_variant": affine,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

@@ -1313,7 +1313,10 @@ static lrbms_status launch_project(lrbms_ctx* c) {
     k_theta_solve<<<1, 32, 0, c->stream>>>(part, c->prof_G, c->prof_M, reinterpret_cast<double*>(c->pws + c->off_gram),
                                           theta);
     LAUNCH_CHECK(c);
-    k_affine_combine<<<4 * c->sms, 256, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_bq), theta,
+#ifndef AFF_GRID
+#define AFF_GRID 8
+#endif
+    k_affine_combine<<<AFF_GRID * c->sms, 256, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_bq), theta,
                                                         c->prof_M, block_len(c), c->at<double>(c->blocks));
     LAUNCH_CHECK(c);
     k_affine_combine<<<cdiv((int)(R / 2 + 1), 256), 256, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_dq),
@@ -1637,6 +1640,9 @@ lrbms_status lrbms_get_state(lrbms_ctx* c, double* s, double* p, double* cc) {
   return LRBMS_OK;
 }
 
+#ifndef AFF_PGRID
+#define AFF_PGRID 4
+#endif
 static void profile_layout(const lrbms_ctx* c, int M, size_t* offs, size_t* total) {
   const size_t n = c->g.n, R = (size_t)c->g.n_s * c->g.N;
   size_t o = 0;
@@ -1645,7 +1651,7 @@ static void profile_layout(const lrbms_ctx* c, int M, size_t* offs, size_t* tota
   offs[1] = take(8 * (size_t)M * block_len(c));      // b_q
   offs[2] = take(8 * (size_t)M * R);                 // d_q
   offs[3] = take(8 * (size_t)M * M);                 // Gram
-  offs[4] = take(8 * (size_t)M * 4 * (size_t)c->sms);   // per-CTA partials
+  offs[4] = take(8 * (size_t)M * AFF_PGRID * (size_t)c->sms);   // per-CTA partials
   offs[5] = take(8 * AFF_MAXM);                      // theta
   *total = o;
 }
@@ -1669,7 +1675,7 @@ lrbms_status lrbms_set_profiles(lrbms_ctx* c, const double* s_profiles, int32_t 
   if (((uintptr_t)ws) % 256) return fail(c, LRBMS_E_CONFIG, "profile workspace must be 256-byte aligned");
   c->pws = (char*)ws;
   c->prof_M = M;
-  c->prof_G = 4 * c->sms;
+  c->prof_G = AFF_PGRID * c->sms;
   c->off_lamq = offs[0]; c->off_bq = offs[1]; c->off_dq = offs[2];
   c->off_gram = offs[3]; c->off_part = offs[4]; c->off_theta = offs[5];
   const Geo& g = c->g;

@@ -12,8 +12,12 @@ from paper_1405_2810_b200.lrbms import LrbmsContext  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+affine = len(sys.argv) > 3 and sys.argv[3] == "affine"
 sc = inputs.make_scenario(cfg)
 ctx = LrbmsContext(sc)
+if affine:
+    ctx.set_profiles(inputs.profile_saturations(sc))
+    ctx.set_online(True)
 ctx.run(5)
 s0 = ctx.stats()
 e0 = torch.cuda.Event(enable_timing=True)
