@@ -263,11 +263,14 @@ __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restric
       nb[1 + s] = j;
     }
   }
-  for (int i = i0; i < min(n, i0 + RT_ROWS); ++i) {
+#pragma unroll 8
+  for (int r = 0; r < RT_ROWS; ++r) {   // unrolled: the 7 loads of several rows in flight at once
+    const int i = i0 + r;
+    if (i >= n) break;
     const float* xi = X + (size_t)i * n;
-    float v = xi[nb[0]] * e[0];
+    float v = __ldg(xi + nb[0]) * e[0];
 #pragma unroll
-    for (int s = 1; s < 7; ++s) v = fmaf(xi[nb[s]], e[s], v);
+    for (int s = 1; s < 7; ++s) v = fmaf(__ldg(xi + nb[s]), e[s], v);
     RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
   }
 }
