@@ -71,6 +71,7 @@ __device__ __forceinline__ void tm_st32(uint32_t taddr, const uint32_t (&v)[32])
 // Half h (0, 1) holds rows i = 2h, 2h + 1: 16 doubles = 32 TMEM columns.
 //
 // Accumulates pu[i] += sum_j U[.][.] vc[j] (rows) and pt[j] += sum_i U[.][.] vr[i] (columns).
+template <bool ROWS = true, bool COLS = true>
 __device__ __forceinline__ void tile_half(const double (&u)[16], int h, const double (&vr)[4], const double (&vc)[8],
                                           double (&pu)[4], double (&pt)[8]) {
 #pragma unroll
@@ -78,8 +79,8 @@ __device__ __forceinline__ void tile_half(const double (&u)[16], int h, const do
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const double x = u[ii * 8 + j];
-      pu[2 * h + ii] = fma(x, vc[j], pu[2 * h + ii]);
-      pt[j] = fma(x, vr[2 * h + ii], pt[j]);
+      if (ROWS) pu[2 * h + ii] = fma(x, vc[j], pu[2 * h + ii]);
+      if (COLS) pt[j] = fma(x, vr[2 * h + ii], pt[j]);
     }
 }
 
@@ -650,11 +651,8 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           if (!up[a]) continue;
-          const double vN = first ? zn[a] : fma(beta, pn[a], zn[a]);
-          double vc[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) vc[j] = __shfl_sync(FULL, vN, cb + 4 * j);
           double pu[4] = {0.0, 0.0, 0.0, 0.0}, pt[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+          double vc[8];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             double u[16];
@@ -667,7 +665,14 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
 #pragma unroll
               for (int k = 0; k < 16; ++k) u[k] = ov[(size_t)(a - a_ov) * 1024 + (size_t)(16 * h + k) * 32 + lane];
             }
-            tile_half(u, h, vr, vc, pu, pt);
+            // the column part first (own p only), so the neighbour loads of zn, pn are still in flight
+            tile_half<false, true>(u, h, vr, vc, pu, pt);
+            if (h == 0) {
+              const double vN = first ? zn[a] : fma(beta, pn[a], zn[a]);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) vc[j] = __shfl_sync(FULL, vN, cb + 4 * j);
+            }
+            tile_half<true, false>(u, h, vr, vc, pu, pt);
           }
           double tc;
           const double tu = tile_scatter(pu, pt, lane, tc);
