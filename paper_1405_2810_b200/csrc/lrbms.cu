@@ -1406,9 +1406,13 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
                                                          c->at<int>(c->flags), es);
     LAUNCH_CHECK(c);
 #ifndef TRANSFORM_WARP
-#define TRANSFORM_WARP 1
+#define TRANSFORM_WARP 2
 #endif
-#if TRANSFORM_WARP
+#if TRANSFORM_WARP == 2
+    k_transform_h<<<cdiv(g.n_s * g.dim, 4), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
+                                                                c->at<double>(c->zh),
+                                                                mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
+#elif TRANSFORM_WARP
     k_transform_w<<<cdiv(g.n_s * g.dim, 8), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
                                                                 c->at<double>(c->zh),
                                                                 mode == 2 ? c->at<double>(c->Yd) : nullptr, es);

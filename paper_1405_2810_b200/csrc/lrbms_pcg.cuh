@@ -456,6 +456,142 @@ __global__ void __launch_bounds__(256, TRW_MINB) k_transform_w(Geo g, double* __
   }
 }
 
+// As k_transform_w with TWO warps per coupling block, each owning 16 rows of Bh: rows of
+// Bh = (X_E U) X_N^T depend only on the same rows of X_E U, so the halves are independent; half the
+// accumulators per lane (~128 registers, 16 warps per SM instead of 8).  The column sums of
+// Y_{E+a,E} and the coarse coupling combine the two halves through shared memory in a fixed order.
+// CTA = 4 blocks x 2 halves.
+__global__ void __launch_bounds__(256, 2) k_transform_h(Geo g, double* __restrict__ blocks,
+                                                    const double* __restrict__ Linv,
+                                                    const double* __restrict__ zh, double* __restrict__ Yd,
+                                                    double* __restrict__ Es) {
+  __shared__ double colp[4][2][32];
+  __shared__ double ecp[4][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = warp >> 1, half = warp & 1;
+  const int t = blockIdx.x * 4 + slot;
+  bool live = t < g.n_s * g.dim;
+  int E = 0, a = 0, En = 0;
+  if (live) {
+    E = t / g.dim;
+    a = t - E * g.dim;
+    int C[3];
+    sub_xyz(g, E, C);
+    live = C[a] + 1 < g.S[a];
+    En = live ? E + g.Estride[a] : E;
+  }
+  const int N = g.N, NN = N * N;
+  const int fr = lane >> 2, q = lane & 3;
+  double bh[2][4][2];
+  if (live) {
+    double* U = blocks + ((size_t)E * (1 + g.dim) + 1 + a) * NN;
+    const double* XE = Linv + (size_t)E * NN;
+    const double* XN = Linv + (size_t)En * NN;
+    auto ld = [&](const double* M, int r, int c) -> double { return (r < N && c < N) ? M[r * N + c] : 0.0; };
+    double t1[2][4][2];
+#pragma unroll
+    for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) t1[ti][tj][0] = t1[ti][tj][1] = bh[ti][tj][0] = bh[ti][tj][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int ti = 0; ti < 2; ++ti) af[ti] = ld(XE, 16 * half + 8 * ti + fr, 4 * ks + q);
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) bf[tj] = ld(U, 4 * ks + q, 8 * tj + fr);
+#pragma unroll
+      for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj) dmma_t(t1[ti][tj][0], t1[ti][tj][1], af[ti], bf[tj]);
+    }
+    const int src_lo = (lane & ~3) + (q >> 1), src_hi = (lane & ~3) + 2 + (q >> 1);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int src = (ks & 1) ? src_hi : src_lo;
+      double af[2], bf[4];
+#pragma unroll
+      for (int ti = 0; ti < 2; ++ti) {
+        const double v0 = __shfl_sync(FULL, t1[ti][ks >> 1][0], src);
+        const double v1 = __shfl_sync(FULL, t1[ti][ks >> 1][1], src);
+        af[ti] = (q & 1) ? v1 : v0;
+      }
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) bf[tj] = ld(XN, 8 * tj + fr, 4 * ks + q);
+#pragma unroll
+      for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj) dmma_t(bh[ti][tj][0], bh[ti][tj][1], af[ti], bf[tj]);
+    }
+#pragma unroll
+    for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        const int i = 16 * half + 8 * ti + fr, j = 8 * tj + 2 * q;
+        if (i < N) {
+          if (j < N) U[i * N + j] = bh[ti][tj][0];
+          if (j + 1 < N) U[i * N + j + 1] = bh[ti][tj][1];
+        }
+      }
+  }
+  if (!Es && !Yd) return;   // uniform over the grid
+  double o = 0.0;
+  if (live) {
+    const double* zN = zh + (size_t)En * N;
+    const double* zE = zh + (size_t)E * N;
+    // Y_{E,E+a}[i] for this half's rows (quad reduction), and its part of zh_E . Y
+#pragma unroll
+    for (int ti = 0; ti < 2; ++ti) {
+      double v = 0.0;
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        const int j = 8 * tj + 2 * q;
+        v = fma(bh[ti][tj][0], j < N ? zN[j] : 0.0, v);
+        v = fma(bh[ti][tj][1], j + 1 < N ? zN[j + 1] : 0.0, v);
+      }
+      v += __shfl_xor_sync(FULL, v, 1);
+      v += __shfl_xor_sync(FULL, v, 2);
+      const int i = 16 * half + 8 * ti + fr;
+      if (q == 0 && i < N) {
+        if (Yd) Yd[((size_t)E * 6 + a) * N + i] = v;
+        o = fma(v, zE[i], o);
+      }
+    }
+    // this half's part of the column sums sum_i Bh[i][j] zh_E[i]
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj) {
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int ti = 0; ti < 2; ++ti) {
+        const int i = 16 * half + 8 * ti + fr;
+        const double z = i < N ? zE[i] : 0.0;
+        v0 = fma(bh[ti][tj][0], z, v0);
+        v1 = fma(bh[ti][tj][1], z, v1);
+      }
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        v0 += __shfl_xor_sync(FULL, v0, off);
+        v1 += __shfl_xor_sync(FULL, v1, off);
+      }
+      if (fr == 0) {
+        colp[slot][half][8 * tj + 2 * q] = v0;
+        colp[slot][half][8 * tj + 2 * q + 1] = v1;
+      }
+    }
+    o = warp_sum(o);
+    if (lane == 0) ecp[slot][half] = o;
+  }
+  __syncthreads();
+  if (live && half == 0) {
+    if (Yd && lane < N) Yd[((size_t)En * 6 + 3 + a) * N + lane] = colp[slot][0][lane] + colp[slot][1][lane];
+    if (Es && lane == 0) {
+      const double e = ecp[slot][0] + ecp[slot][1];
+      Es[(size_t)E * 8 + 1 + a] = e;
+      Es[(size_t)En * 8 + 4 + a] = e;
+    }
+  }
+}
+
 // ============================================================================ PCG on the scaled system
 
 // Part A of q = Bh v for subdomain E: returns lane's (v_E + sum_a U_a v_{E+a}); stores U_a^T v_E
