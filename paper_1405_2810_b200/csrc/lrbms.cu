@@ -1022,7 +1022,8 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->hist, KHIST * R * 8); alloc(c->Wh, KHIST * R * 8); alloc(c->Vh, KHIST * R * 8);
   alloc(c->TH, KHIST * 3 * R * 8);
   alloc(c->rbv, R * 8);
-  alloc(c->gpart, 8 * 44 * (size_t)cdiv(g.n_s, 8)); alloc(c->z, R * 8); alloc(c->pv, R * 8);
+  alloc(c->gpart, 8 * (44 * (size_t)cdiv(g.n_s, 8) + 64));   // partials, then the 44 sums
+  alloc(c->z, R * 8); alloc(c->pv, R * 8);
   alloc(c->pv2, R * 8); alloc(c->q, R * 8);
   alloc(c->T, R * 3 * 8);
   alloc(c->Linv, (size_t)g.n_s * g.N * g.N * 8);
@@ -1483,6 +1484,11 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     }
     A.gpart = H.gpart;
     A.ngram = nb;
+    A.gsum = H.gpart + (size_t)44 * nb;
+    if (H.nh > 0) {
+      k_hist_sum<<<44, 32, 0, c->stream>>>(H.gpart, nb, const_cast<double*>(A.gsum));
+      LAUNCH_CHECK(c);
+    }
   }
   A.r = c->at<double>(c->r); A.z = c->at<double>(c->z);
   A.pb0 = c->at<double>(c->pv); A.pb1 = c->at<double>(c->pv2);

@@ -41,6 +41,7 @@ struct PcgArgs {
   const double* V;        // [KH][n_s][N] Bh W
   const double* rb;       // [n_s][N] L^-1 b
   const double* gpart;    // [44][ngram] Gram / rhs partials from k_hist_gram
+  const double* gsum;     // [44] their sums (k_hist_sum), read by k_pcg_tm
   int ngram;
   double* y;              // transformed unknown L^T c
   double* r;
@@ -1019,6 +1020,15 @@ __global__ void __launch_bounds__(256) k_hist_gram(HistArgs A) {
     for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
     A.gpart[threadIdx.x * gridDim.x + blockIdx.x] = t;
   }
+}
+
+// the 44 fixed-order sums of the k_hist_gram partials, one warp per sum (for k_pcg_tm's setup)
+__global__ void k_hist_sum(const double* __restrict__ gpart, int ngram, double* __restrict__ gsum) {
+  const int q = blockIdx.x, lane = threadIdx.x;
+  double v = 0.0;
+  for (int b = lane; b < ngram; b += 32) v += gpart[(size_t)q * ngram + b];
+  v = warp_sum(v);
+  if (lane == 0) gsum[q] = v;
 }
 
 // Solve of one PCG run's setup (out of line: its register pressure stays out of the iteration

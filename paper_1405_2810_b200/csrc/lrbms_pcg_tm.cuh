@@ -34,6 +34,9 @@
 #ifndef TM_BARB
 #define TM_BARB 1    // the barrier after the r update carries no reduction (r.r is not needed: rz detects NaN / exact)
 #endif
+#ifndef TM_ASYNC_STAGE
+#define TM_ASYNC_STAGE 1   // 1: cp.async staging of the coarse rows / shared-memory blocks / Y during the TMEM fill
+#endif
 #ifndef TM_GEMV
 #define TM_GEMV 0    // coarse product sliced by columns over the CTA's warps (rows read once), 0 = row per warp
 #endif
@@ -42,6 +45,13 @@ namespace lrbms {
 
 __device__ __forceinline__ uint32_t smem_addr_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void tm_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void tm_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr_u32(dst)), "l"(src) : "memory");
 }
 
 // 32 lanes x 32 consecutive 32-bit TMEM columns <-> 32 registers per lane
@@ -248,15 +258,8 @@ __device__ __noinline__ void hist_weights(const PcgArgs& A, double* sh, double (
 #pragma unroll
   for (int j = 0; j < 8; ++j) alpha_h[j] = 0.0;
   if (nh <= 0) return;
-  // the 44 fixed-order sums of the per-CTA partials, spread over the warps (one L2 round trip chain
-  // per warp instead of 44 in one warp)
-  const int W = blockDim.x >> 5;
-  for (int q = warp; q < 44; q += W) {
-    double v = 0.0;
-    for (int b = lane; b < A.ngram; b += 32) v += __ldcg(A.gpart + q * A.ngram + b);
-    v = warp_sum(v);
-    if (lane == 0) sh[q] = v;
-  }
+  // the 44 fixed-order sums of the Gram / rhs partials (formed by k_hist_sum before the launch)
+  for (int q = threadIdx.x; q < 44; q += blockDim.x) sh[q] = A.gsum[q];
   __syncthreads();
   double G[8][8], rhs8[8];
   int q = 0;
@@ -338,6 +341,12 @@ __host__ __device__ inline TmLayout tm_layout(int W, int dim, int n_pad) {
       A.tstamp[4096 + 8 * ((size_t)it * gridDim.x + blockIdx.x) + (k)] = gtimer();             \
   } while (0)
 
+// debug setup stamps (slots of "iteration 0": tstamp[4096 + 8 CTA + k])
+#define TM_SSTAMP(k)                                                                           \
+  do {                                                                                         \
+    if (A.tstamp && threadIdx.x == 0) A.tstamp[4096 + 8 * (size_t)blockIdx.x + (k)] = gtimer();  \
+  } while (0)
+
 __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ uint32_t tbase_s;
@@ -363,6 +372,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
   const int n4 = A.n_pad >> 2;   // float4 chunks of a coarse row
   const int tm_ncols = TM_COLS;
 
+  TM_SSTAMP(0);
   // ---- TMEM: allocate, then every warp writes its a = 0, 1 coupling tiles
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr_u32(&tbase_s)),
@@ -384,6 +394,60 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     lo[a] = own && a < dim && C[a] > 0;
   }
   const int ra = (lane >> 2) * 4, cb = lane & 3;
+#if TM_ASYNC_STAGE
+  // Staging: the rows of the coarse inverse, the shared-memory coupling blocks and the deflation
+  // vectors are copied with cp.async (no registers: they stream in the background) while the
+  // TMEM-resident blocks go through registers and tcgen05.st.
+  if (A.use_coarse) {
+    const float4* src = reinterpret_cast<const float4*>(A.Binv + (size_t)(own ? E : 0) * A.n_pad);
+    float4* dst = reinterpret_cast<float4*>(bs);
+    for (int q = lane; q < (A.n_pad >> 2); q += 32) {
+      if (own) tm_cp16(dst + q, src + q);
+      else dst[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    if (A.use_coarse == 2 && act && side_exists(g, C, s)) tm_cp8(yd + s * 32 + lane, A.Yd + ((size_t)E * 6 + s) * N + lane);
+    else yd[s * 32 + lane] = 0.0;
+  }
+  {
+    const double* Bd = A.blocks + (size_t)(own ? E : 0) * (1 + dim) * N * N;
+    for (int a = a_ov; a < dim; ++a) {   // shared-memory blocks
+      const double* U = Bd + (size_t)(1 + a) * N * N;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int i = k >> 3, j = k & 7, r = ra + i, c = cb + 4 * j;
+        double* d = ov + (size_t)(a - a_ov) * 1024 + (size_t)k * 32 + lane;
+        if (up[a] && r < N && c < N) tm_cp8(d, U + r * N + c);
+        else *d = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    for (int a = 0; a < min(dim, a_ov); ++a) {   // TMEM blocks
+      if (!up[a]) continue;
+      const double* U = Bd + (size_t)(1 + a) * N * N;
+      double x[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int i = k >> 3, j = k & 7, r = ra + i, c = cb + 4 * j;
+        x[k] = (r < N && c < N) ? __ldg(U + r * N + c) : 0.0;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t v[32];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          v[2 * k] = (uint32_t)__double2loint(x[16 * h + k]);
+          v[2 * k + 1] = (uint32_t)__double2hiint(x[16 * h + k]);
+        }
+        tm_st32(tcol + 64u * a + 32u * h, v);
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
+#else
   {
     const double* Bd = A.blocks + (size_t)(own ? E : 0) * (1 + dim) * N * N;
 #pragma unroll 1
@@ -422,7 +486,9 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     float4* dst = reinterpret_cast<float4*>(bs);
     for (int q = lane; q < (A.n_pad >> 2); q += 32) dst[q] = own ? __ldcs(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+#endif
   const double zh = act ? A.zh[E * N + lane] : 0.0;
+  TM_SSTAMP(1);
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -576,7 +642,9 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
 
   // ---- initial guess: Galerkin combination of the history, y0 = W alpha, r0 = rb - V alpha
   double alpha_h[8];
+  TM_SSTAMP(2);
   hist_weights(A, sh46, alpha_h);
+  TM_SSTAMP(3);
   const size_t R = (size_t)g.n_s * N;
   double y = 0.0, r = 0.0;
   double pbb = 0.0;
@@ -593,7 +661,9 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     const double w = warp_sum(zh * r);
     if (lane == 0) A.wc[E] = w;
   }
+  TM_SSTAMP(4);
   const double bb = grid_reduce_rel(pbb, red16, gparts, A.gbar, epoch, &bc[0]);
+  TM_SSTAMP(5);
   const double tol2 = A.rtol * A.rtol * bb;
   double rr = 1.0;
   int it = 0;
@@ -624,6 +694,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     if (A.use_coarse) { const float ec = coarse_dot(); z = act ? r + zh * (double)ec : 0.0; }
     if (act) A.z[E * N + lane] = z;
     double rz = grid_reduce_rel(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+    TM_SSTAMP(6);
     double beta = 0.0, p = 0.0;
     for (it = (rz <= tol2) ? A.max_iters + 2 : 1; it <= A.max_iters; ++it) {
       double* pcur = (it & 1) ? A.pb1 : A.pb0;
@@ -738,6 +809,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
   } else {
     rr = 0.0;
   }
+  TM_SSTAMP(7);
   // ---- back-transform c = L^-T y
   if (own) {
     const double* Li = A.Linv + (size_t)E * N * N;

@@ -34,3 +34,13 @@ print(f"{cfg}: G={G} W={W} iters={it}, us per iteration {r[-1]:.2f}")
 for k, n in enumerate(names):
     print(f"  {n:10s} median {r[k]:5.2f}  max {r[7 + k]:5.2f}")
 print(f"  arrival spread at the reductions: pq {r[14]:.2f} rr {r[15]:.2f} rz {r[16]:.2f}")
+
+# setup stamps (iteration-0 slots): entry, after TMEM/shared staging, before/after the history weights,
+# before/after the first reduction, after the DEF start + r.z, and the loop exit
+s0 = t[0]
+names0 = ["staging (TMEM, smem)", "-> hist weights", "history weights", "initial guess", "bb reduction",
+          "DEF start + r.z", "iterations"]
+d0 = np.diff(s0[:, :8], axis=1)
+print("setup phases (median / max over CTAs, us):")
+for k, nm in enumerate(names0):
+    print(f"  {nm:22s} {np.median(d0[:, k]):7.2f} {d0[:, k].max():7.2f}")
