@@ -631,6 +631,8 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
   int C[3];
   sub_xyz(g, E, C);
   const size_t base = (size_t)E * nl;
+  // the link range of E, loaded at entry (its latency hides behind the face loop)
+  const int q0 = A.L.sub_start[E], q1 = A.L.sub_start[E + 1];
   for (int l = threadIdx.x; l < nl; l += blockDim.x) {
     int c[3];
     local_xyz(g, l, c);
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
+    for (int q = q0; q < q1; ++q) {
       const int l = A.L.local[q];
       const double F = A.L.gK[q] * A.lam[base + l] * (A.p[base + l] - A.L.p[q]);
       opos[l] += fmax(F, 0.0);

@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   int C[3];
   sub_xyz(g, E, C);
   const size_t base = (size_t)E * nl;
+  const int lq0 = A.L.sub_start[E], lq1 = A.L.sub_start[E + 1];   // link range of E, loaded at entry
   if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 0] = gtimer_p();
 
   // 0. inputs of the face weights (a1 + R2) of the thread's first cell, loaded before the Phi staging
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   }
   __syncthreads();
   if (tid == 0) {  // links of E (R6), sequential: deterministic
-    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
+    for (int q = lq0; q < lq1; ++q) {
       const int l = A.L.local[q];
       Wc[(size_t)l * 8] += A.L.gK[q] * lam[l];
     }
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   // 4. r_E = Phi_E^T b_E, b = sum_L g_L p_L e_L
   if (tid < N) {
     double rr = 0.0;
-    for (int q = A.L.sub_start[E]; q < A.L.sub_start[E + 1]; ++q) {
+    for (int q = lq0; q < lq1; ++q) {
       const int l = A.L.local[q];
       rr += Phs[(size_t)tid * LD + l] * (A.L.gK[q] * lam[l] * A.L.p[q]);
     }
