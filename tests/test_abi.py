@@ -50,6 +50,26 @@ def test_library_targets_sm100a_only():
     assert "DMMA" in sass            # the projection's fp64 tensor-core path
 
 
+def _sass_of(fn):
+    from paper_1405_2810_b200 import build
+    import subprocess
+    return subprocess.run(["cuobjdump", "-sass", "-fun", fn, build.SO], capture_output=True, text=True).stdout
+
+
+def test_onchip_pcg_uses_tensor_memory():
+    """k_pcg_tm keeps the scaled couplings in tensor memory: tcgen05.st at staging (STTM), tcgen05.ld
+    every iteration (LDTM), cp.async staging (LDGSTS) and release reductions for its grid barriers."""
+    sass = _sass_of("_ZN5lrbms8k_pcg_tmENS_7PcgArgsE")
+    for op in ("LDTM", "STTM", "LDGSTS", "REDG.E.ADD.STRONG.GPU"):
+        assert op in sass, op
+
+
+def test_newton_schulz_on_tcgen05():
+    """The coarse inverse's Newton-Schulz GEMM issues tcgen05.mma (UTCHMMA) from TMA-staged tiles."""
+    sass = _sass_of("_ZN5lrbms12k_ns_gemm_tcE14CUtensorMap_stS0_PKfPfi")
+    assert "UTC" in sass and "UTMALDG" in sass
+
+
 def _create(lib, **over):
     from paper_1405_2810_b200 import lrbms
     import numpy as np
