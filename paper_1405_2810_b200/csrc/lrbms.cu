@@ -1408,21 +1408,9 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
                                                          c->at<double>(c->zc), c->at<double>(c->zh),
                                                          c->at<int>(c->flags), es);
     LAUNCH_CHECK(c);
-#ifndef TRANSFORM_WARP
-#define TRANSFORM_WARP 2
-#endif
-#if TRANSFORM_WARP == 2
     k_transform_h<<<cdiv(g.n_s * g.dim, 4), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
                                                                 c->at<double>(c->zh),
                                                                 mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
-#elif TRANSFORM_WARP
-    k_transform_w<<<cdiv(g.n_s * g.dim, 8), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
-                                                                c->at<double>(c->zh),
-                                                                mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
-#else
-    k_transform<<<g.n_s, 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
-                                              c->at<double>(c->zh), mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
-#endif
     LAUNCH_CHECK(c);
   }
   // The coarse update (Newton-Schulz: non-cooperative kernels) goes to the side stream, forked
@@ -1433,10 +1421,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     const bool rebuild = !c->have_x || c->last_rebuild_step < 0 ||
                          c->steps - c->last_rebuild_step >= c->opts.coarse_refresh;
     cudaStream_t main = c->stream;
-#ifndef USE_SIDE_STREAM
-#define USE_SIDE_STREAM 1
-#endif
-    if (USE_SIDE_STREAM && !rebuild && mode == 2 && c->side) {
+    if (!rebuild && mode == 2 && c->side) {
       CUDA_TRY(c, cudaEventRecord(c->fork_ev, main));
       CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->fork_ev, 0));
       c->stream = c->side;
@@ -1472,14 +1457,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     k_hist_transform<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
     LAUNCH_CHECK(c);
     if (H.nh > 0) {
-#ifndef HIST_TILED
-#define HIST_TILED 1
-#endif
-#if HIST_TILED
       k_hist_spmv_t<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
-#else
-      k_hist_spmv<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
-#endif
       LAUNCH_CHECK(c);
       k_hist_gram<<<nb, 256, 0, c->stream>>>(H);
       LAUNCH_CHECK(c);

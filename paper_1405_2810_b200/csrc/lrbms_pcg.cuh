@@ -2,10 +2,11 @@
 //
 // 1. k_block_chol (warp per subdomain): B_EE = L_E L_E^T (in-register Cholesky), L_E^-1, and the
 //    transformed coarse vector zh_E = L_E^T zc_E.
-// 2. k_transform (warp per coupling block): Bh_{E,E'} = L_E^-1 B_{E,E'} L_E'^-T, in place.
+// 2. k_transform_h (two warps per coupling block): Bh_{E,E'} = L_E^-1 B_{E,E'} L_E'^-T, in place.
 //    The block-Jacobi-scaled system  Bh y = L^-1 r,  c = L^-T y  has an IDENTITY diagonal block:
 //    the SpMV reads only the coupling blocks and the block-Jacobi preconditioner costs nothing.
-// 3. k_pcg: one cooperative persistent kernel per solve, warp per subdomain (lane k <-> coefficient
+// 3. k_pcg (the L2-streaming variant, onchip = 0; the default is k_pcg_tm, lrbms_pcg_tm.cuh):
+//    one cooperative persistent kernel per solve, warp per subdomain (lane k <-> coefficient
 //    k, N <= 32).  Preconditioned CG (Hestenes-Stiefel) on Bh with the coarse correction
 //    M^-1 = I + Zh B_c^-1 Zh^T (B_c = Zh^T Bh Zh = Z^T B Z, the Galerkin operator on the subdomain
 //    indicators, inverted every few steps), warm-started from the (extrapolated) previous solution,
@@ -122,26 +123,14 @@ __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
 
 // ============================================================================ factorisation + transform
 
-#ifndef CHOL_SMEM_INV
-#define CHOL_SMEM_INV 1   // L^-1 by forward substitution from L staged in shared memory (the register
-                          // Cholesky's column array is dead by then): ~100 instead of 255 registers,
-                          // 16 instead of 8 warps per SM, one wave for C5
-#endif
-
 // Warp per subdomain.  Lane j holds column j of the (padded-to-32 with identity) block.
 #ifndef CHOL_MINB
 #define CHOL_MINB 4
 #endif
-#if CHOL_SMEM_INV
 __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
                                                       const double* __restrict__ zc, double* __restrict__ zh,
                                                       int* flags, double* __restrict__ Es) {
   __shared__ double Ls[4][32 * 33];
-#else
-__global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
-                                                   const double* __restrict__ zc, double* __restrict__ zh,
-                                                   int* flags, double* __restrict__ Es) {
-#endif
   const int lane = threadIdx.x & 31;
   const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (E >= g.n_s) return;
@@ -179,7 +168,6 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
   double zhat = 0.0;   // (L^T zc)[lane] = sum_i L[i][lane] zc[i]
 #pragma unroll
   for (int i = 0; i < 32; ++i) zhat += m[i] * __shfl_sync(FULL, zk, i);
-#if CHOL_SMEM_INV
   // lane holds column lane of L in m[]: L[i][lane] = m[i] -> Ls[i][lane]
   double* ls = Ls[threadIdx.x >> 5];
 #pragma unroll
@@ -206,27 +194,6 @@ __global__ void __launch_bounds__(128) k_block_chol(Geo g, double* __restrict__ 
       if (i < N) Li[i * N + lane] = x[i];
     zh[E * N + lane] = zhat;
   }
-#else
-  // L^-1 by forward substitution, one column per lane: L x = e_lane
-  double x[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double acc = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k) acc -= __shfl_sync(FULL, m[i], k) * x[k];
-    x[i] = acc * (1.0 / __shfl_sync(FULL, m[i], i));
-  }
-  if (lane < N) {
-    double* Li = Linv + (size_t)E * N * N;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < N) {
-        Bd[i * N + lane] = m[i];   // L in the diagonal slot
-        Li[i * N + lane] = x[i];
-      }
-    zh[E * N + lane] = zhat;
-  }
-#endif
   if (Es) {   // coarse operator diagonal zc^T B_EE zc = |L^T zc|^2; the side slots are set by k_transform
     const double d = warp_sum(lane < N ? zhat * zhat : 0.0);
     if (lane < 8) Es[(size_t)E * 8 + lane] = lane == 0 ? d : 0.0;
@@ -239,227 +206,12 @@ __device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double 
                : "d"(a), "d"(b));
 }
 
-// CTA (8 warps) per subdomain E: Bh_{E,E+a} = L_E^-1 U L_{E+a}^-T in place for its upper couplings,
-// two 32x32x32 products on the fp64 tensor cores (DMMA) through shared memory (rows padded to 36).
-//
-// For the deflation preconditioner it also forms Y_{E,F} = Bh_{E,F} zh_F for the neighbours F of E
-// (Yd[E][a] for F = E + e_a, Yd[E][3 + a] for F = E - e_a; Yd == nullptr: not needed).
-__global__ void __launch_bounds__(256) k_transform(Geo g, double* __restrict__ blocks,
-                                                  const double* __restrict__ Linv,
-                                                  const double* __restrict__ zh, double* __restrict__ Yd,
-                                                  double* __restrict__ Es) {
-  constexpr int LDX = 36;
-  __shared__ double XE[32 * LDX], Us[32 * LDX], XN[32 * LDX], T1[32 * LDX];
-  const int E = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int N = g.N, NN = N * N;
-  const int fr = lane >> 2, fc = lane & 3;
-  int C[3];
-  sub_xyz(g, E, C);
-  auto load = [&](double* dst, const double* src) {
-    for (int t = tid; t < 32 * 32; t += blockDim.x) {
-      const int i = t >> 5, j = t & 31;
-      dst[i * LDX + j] = (i < N && j < N) ? src[i * N + j] : 0.0;
-    }
-  };
-  load(XE, Linv + (size_t)E * NN);
-  for (int a = 0; a < g.dim; ++a) {
-    if (C[a] + 1 >= g.S[a]) continue;
-    double* U = blocks + ((size_t)E * (1 + g.dim) + 1 + a) * NN;
-    load(Us, U);
-    load(XN, Linv + (size_t)(E + g.Estride[a]) * NN);
-    __syncthreads();
-    // T1 = X_E U : warp -> tiles (warp, warp + 8) of the 4 x 4 tile grid
-    for (int t = warp; t < 16; t += 8) {
-      const int ti = t >> 2, tj = t & 3;
-      double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-        dmma_t(c0, c1, XE[(8 * ti + fr) * LDX + 4 * ks + fc], Us[(4 * ks + fc) * LDX + 8 * tj + fr]);
-      T1[(8 * ti + fr) * LDX + 8 * tj + 2 * fc] = c0;
-      T1[(8 * ti + fr) * LDX + 8 * tj + 2 * fc + 1] = c1;
-    }
-    __syncthreads();
-    // Bh = T1 X_N^T
-    for (int t = warp; t < 16; t += 8) {
-      const int ti = t >> 2, tj = t & 3;
-      double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-        dmma_t(c0, c1, T1[(8 * ti + fr) * LDX + 4 * ks + fc], XN[(8 * tj + fr) * LDX + 4 * ks + fc]);
-      const int i = 8 * ti + fr, j = 8 * tj + 2 * fc;
-      if (i < N) {
-        if (j < N) U[i * N + j] = c0;
-        if (j + 1 < N) U[i * N + j + 1] = c1;
-      }
-      Us[i * LDX + j] = c0;   // Bh (zero beyond N: X_E and X_N are zero padded)
-      Us[i * LDX + j + 1] = c1;
-    }
-    if (Es) {
-      __syncthreads();
-      const int En = E + g.Estride[a];
-      if (warp == 0) {   // Y_{E,E+a} = Bh zh_{E+a}; coarse coupling zc_E^T B_{E,E+a} zc_{E+a} = zh_E . Y
-        double acc = 0.0;
-        const double zn = lane < N ? zh[(size_t)En * N + lane] : 0.0;
-        for (int j = 0; j < N; ++j) acc += Us[lane * LDX + j] * __shfl_sync(FULL, zn, j);
-        if (Yd && lane < N) Yd[((size_t)E * 6 + a) * N + lane] = acc;
-        const double o = warp_sum(lane < N ? acc * zh[(size_t)E * N + lane] : 0.0);
-        if (lane == 0) {
-          Es[(size_t)E * 8 + 1 + a] = o;
-          Es[(size_t)En * 8 + 4 + a] = o;
-        }
-      } else if (warp == 1 && Yd) {   // Y_{E+a,E} = Bh^T zh_E
-        double acc = 0.0;
-        const double ze = lane < N ? zh[(size_t)E * N + lane] : 0.0;
-        for (int i = 0; i < N; ++i) acc += Us[i * LDX + lane] * __shfl_sync(FULL, ze, i);
-        if (lane < N) Yd[((size_t)En * 6 + 3 + a) * N + lane] = acc;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-#ifndef TRW_MINB
-#define TRW_MINB 1
-#endif
-// Warp per coupling block (E, a): Bh_{E,E+a} = X_E U X_{E+a}^T (X = L^-1) in place, as k_transform,
-// without shared memory or CTA barriers: both 32x32x32 products on DMMA with operand fragments read
-// straight from L2, the intermediate T1 = X_E U re-laid out from the accumulator layout into A
-// fragments by quad shuffles.  Y_{E,E+a} = Bh zh_{E+a}, Y_{E+a,E} = Bh^T zh_E and the coarse coupling
-// zh_E . Y from the accumulator layout (quad / column reductions).  Grid: n_s * dim warps.
-__global__ void __launch_bounds__(256, TRW_MINB) k_transform_w(Geo g, double* __restrict__ blocks,
-                                                    const double* __restrict__ Linv,
-                                                    const double* __restrict__ zh, double* __restrict__ Yd,
-                                                    double* __restrict__ Es) {
-  const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= g.n_s * g.dim) return;
-  const int E = t / g.dim, a = t - E * g.dim;
-  int C[3];
-  sub_xyz(g, E, C);
-  if (C[a] + 1 >= g.S[a]) return;   // no upper neighbour along a (warp-uniform)
-  const int N = g.N, NN = N * N, En = E + g.Estride[a];
-  double* U = blocks + ((size_t)E * (1 + g.dim) + 1 + a) * NN;
-  const double* XE = Linv + (size_t)E * NN;
-  const double* XN = Linv + (size_t)En * NN;
-  const int fr = lane >> 2, q = lane & 3;
-  auto ld = [&](const double* M, int r, int c) -> double { return (r < N && c < N) ? M[r * N + c] : 0.0; };
-  // T1 = X_E U: tile (ti, tj) accumulators c[ti][tj][2] (row 8 ti + fr, columns 8 tj + 2 q + {0, 1})
-  double t1[4][4][2];
-#pragma unroll
-  for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-    for (int tj = 0; tj < 4; ++tj) t1[ti][tj][0] = t1[ti][tj][1] = 0.0;
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-    double af[4], bf[4];
-#pragma unroll
-    for (int ti = 0; ti < 4; ++ti) af[ti] = ld(XE, 8 * ti + fr, 4 * ks + q);
-#pragma unroll
-    for (int tj = 0; tj < 4; ++tj) bf[tj] = ld(U, 4 * ks + q, 8 * tj + fr);
-#pragma unroll
-    for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-      for (int tj = 0; tj < 4; ++tj) dmma_t(t1[ti][tj][0], t1[ti][tj][1], af[ti], bf[tj]);
-  }
-  // Bh = T1 X_N^T: A fragment (ti, ks) = T1[8 ti + fr][4 ks + q], held by quad lane 2 (ks % 2) + q / 2
-  // in register q % 2 of tile (ti, ks / 2)
-  double bh[4][4][2];
-#pragma unroll
-  for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-    for (int tj = 0; tj < 4; ++tj) bh[ti][tj][0] = bh[ti][tj][1] = 0.0;
-  const int src_lo = (lane & ~3) + (q >> 1), src_hi = (lane & ~3) + 2 + (q >> 1);
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-    const int src = (ks & 1) ? src_hi : src_lo;
-    double af[4], bf[4];
-#pragma unroll
-    for (int ti = 0; ti < 4; ++ti) {
-      const double v0 = __shfl_sync(FULL, t1[ti][ks >> 1][0], src);
-      const double v1 = __shfl_sync(FULL, t1[ti][ks >> 1][1], src);
-      af[ti] = (q & 1) ? v1 : v0;
-    }
-#pragma unroll
-    for (int tj = 0; tj < 4; ++tj) bf[tj] = ld(XN, 8 * tj + fr, 4 * ks + q);   // X_N^T[4 ks + q][8 tj + fr]
-#pragma unroll
-    for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-      for (int tj = 0; tj < 4; ++tj) dmma_t(bh[ti][tj][0], bh[ti][tj][1], af[ti], bf[tj]);
-  }
-  // store Bh in place (zero beyond N by construction)
-#pragma unroll
-  for (int ti = 0; ti < 4; ++ti)
-#pragma unroll
-    for (int tj = 0; tj < 4; ++tj) {
-      const int i = 8 * ti + fr, j = 8 * tj + 2 * q;
-      if (i < N) {
-        if (j < N) U[i * N + j] = bh[ti][tj][0];
-        if (j + 1 < N) U[i * N + j + 1] = bh[ti][tj][1];
-      }
-    }
-  if (!Es) return;
-  // Y_{E,E+a}[i] = sum_j Bh[i][j] zh_N[j]: per lane over its columns, then over the quad
-  const double* zN = zh + (size_t)En * N;
-  const double* zE = zh + (size_t)E * N;
-  double yr[4], yc[4];
-#pragma unroll
-  for (int ti = 0; ti < 4; ++ti) {
-    double v = 0.0;
-#pragma unroll
-    for (int tj = 0; tj < 4; ++tj) {
-      const int j = 8 * tj + 2 * q;
-      v = fma(bh[ti][tj][0], j < N ? zN[j] : 0.0, v);
-      v = fma(bh[ti][tj][1], j + 1 < N ? zN[j + 1] : 0.0, v);
-    }
-    v += __shfl_xor_sync(FULL, v, 1);
-    v += __shfl_xor_sync(FULL, v, 2);
-    yr[ti] = v;   // row 8 ti + fr (all lanes of the quad)
-  }
-  // Y_{E+a,E}[j] = sum_i Bh[i][j] zh_E[i]: per lane over its rows, then over fr (lane bits 2..4)
-#pragma unroll
-  for (int tj = 0; tj < 4; ++tj) {
-    double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-    for (int ti = 0; ti < 4; ++ti) {
-      const int i = 8 * ti + fr;
-      const double z = i < N ? zE[i] : 0.0;
-      v0 = fma(bh[ti][tj][0], z, v0);
-      v1 = fma(bh[ti][tj][1], z, v1);
-    }
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      v0 += __shfl_xor_sync(FULL, v0, o);
-      v1 += __shfl_xor_sync(FULL, v1, o);
-    }
-    yc[tj] = (fr & 1) ? v1 : v0;   // lanes with fr odd report column 8 tj + 2 q + 1
-  }
-  double o = 0.0;
-#pragma unroll
-  for (int ti = 0; ti < 4; ++ti) {
-    const int i = 8 * ti + fr;
-    if (q == 0 && i < N) {
-      if (Yd) Yd[((size_t)E * 6 + a) * N + i] = yr[ti];
-      o = fma(yr[ti], zE[i], o);
-    }
-  }
-  // lanes fr in {0, 1}, q: columns 8 tj + 2 q + fr
-  if (Yd && fr < 2) {
-#pragma unroll
-    for (int tj = 0; tj < 4; ++tj) {
-      const int j = 8 * tj + 2 * q + fr;
-      if (j < N) Yd[((size_t)En * 6 + 3 + a) * N + j] = yc[tj];
-    }
-  }
-  o = warp_sum(o);
-  if (lane == 0) {
-    Es[(size_t)E * 8 + 1 + a] = o;
-    Es[(size_t)En * 8 + 4 + a] = o;
-  }
-}
-
-// As k_transform_w with TWO warps per coupling block, each owning 16 rows of Bh: rows of
-// Bh = (X_E U) X_N^T depend only on the same rows of X_E U, so the halves are independent; half the
-// accumulators per lane (~128 registers, 16 warps per SM instead of 8).  The column sums of
+// Bh_{E,E+a} = X_E U X_{E+a}^T (X = L^-1) in place, TWO warps per coupling block, each owning 16
+// rows of Bh (both 32x32x32 products on DMMA with operand fragments read from L2, the intermediate
+// T1 = X_E U re-laid out from the accumulator layout into A fragments by quad shuffles): rows of
+// Bh = (X_E U) X_N^T depend only on the same rows of X_E U, so the halves are independent
+// (128 registers, 16 warps per SM).  Y_{E,E+a} = Bh zh_{E+a}, Y_{E+a,E} = Bh^T zh_E and the coarse
+// coupling zh_E . Y from the accumulator layout.  The column sums of
 // Y_{E+a,E} and the coarse coupling combine the two halves through shared memory in a fixed order.
 // CTA = 4 blocks x 2 halves.
 __global__ void __launch_bounds__(256, 2) k_transform_h(Geo g, double* __restrict__ blocks,
@@ -917,57 +669,6 @@ __global__ void __launch_bounds__(128) k_hist_transform(HistArgs A) {
     if (act) rbk += ts[lane * 33 + k] * bkk;
   }
   if (act) A.rb[E * N + lane] = rbk;
-}
-
-// warp per subdomain: V_j = W_j + sum_a U_a W_{E+a,j} (own part); U_a^T W_{E,j} -> TH[j][E+a][a]
-__global__ void __launch_bounds__(128) k_hist_spmv(HistArgs A) {
-  __shared__ double tile[4][32 * 33];
-  const Geo& g = A.g;
-  const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int E = blockIdx.x * 4 + warp;
-  if (E >= g.n_s) return;
-  const bool act = lane < N;
-  const size_t R = (size_t)g.n_s * N;
-  double* ts = tile[warp];
-  int C[3];
-  sub_xyz(g, E, C);
-  const double* Bd = A.blocks + (size_t)E * (1 + g.dim) * N * N;
-  double wE[8], v[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    wE[j] = (j < A.nh && act) ? A.W[j * R + E * N + lane] : 0.0;
-    v[j] = wE[j];
-  }
-  for (int a = 0; a < g.dim; ++a) {
-    if (C[a] + 1 >= g.S[a]) continue;
-    const int En = E + g.Estride[a];
-    const double* U = Bd + (size_t)(1 + a) * N * N;
-    __syncwarp();
-    for (int k = 0; k < N; ++k)
-      if (act) ts[k * 33 + lane] = U[k * N + lane];
-    double wN[8], tT[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      wN[j] = (j < A.nh && act) ? A.W[j * R + En * N + lane] : 0.0;
-      tT[j] = 0.0;
-    }
-    __syncwarp();
-    for (int k = 0; k < N; ++k) {
-      const double col = act ? ts[k * 33 + lane] : 0.0;   // U[k][lane]
-      const double row = act ? ts[lane * 33 + k] : 0.0;   // U[lane][k]
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        tT[j] += col * __shfl_sync(FULL, wE[j], k);
-        v[j] += row * __shfl_sync(FULL, wN[j], k);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < A.nh && act) A.TH[((size_t)j * g.n_s * 3 + (size_t)En * 3 + a) * N + lane] = tT[j];
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < A.nh && act) A.V[j * R + E * N + lane] = v[j];
 }
 
 // complete V (lower hand-overs), Gram partials G_ij = W_i.V_j (i <= j) and g_i = W_i.rb per CTA

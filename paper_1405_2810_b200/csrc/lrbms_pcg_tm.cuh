@@ -25,21 +25,6 @@
 #pragma once
 #include "lrbms_pcg.cuh"
 
-#ifndef TM_BAR
-#define TM_BAR 1     // grid reductions: 1 = release reduction on the counter (no fence pair), 0 = grid_reduce
-#endif
-#ifndef TM_G6
-#define TM_G6 1      // coarse rhs contributions side-major [6][n_pad] (coalesced float4 gather), 0 = [n_pad][8]
-#endif
-#ifndef TM_BARB
-#define TM_BARB 1    // the barrier after the r update carries no reduction (r.r is not needed: rz detects NaN / exact)
-#endif
-#ifndef TM_ASYNC_STAGE
-#define TM_ASYNC_STAGE 1   // 1: cp.async staging of the coarse rows / shared-memory blocks / Y during the TMEM fill
-#endif
-#ifndef TM_GEMV
-#define TM_GEMV 0    // coarse product sliced by columns over the CTA's warps (rows read once), 0 = row per warp
-#endif
 
 namespace lrbms {
 
@@ -145,7 +130,6 @@ __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
 // GPU-scope fence per CTA and barrier instead of two (tools/mb_gridreduce.cu: 2.84 vs 3.16 us).
 __device__ __forceinline__ double grid_reduce_rel(double v, double* red16, double* partials, unsigned* bar,
                                                   unsigned& epoch, double* bc) {
-#if TM_BAR
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, G = gridDim.x;
   if (lane == 0) red16[warp] = v;
   __syncthreads();
@@ -169,9 +153,6 @@ __device__ __forceinline__ double grid_reduce_rel(double v, double* red16, doubl
   }
   __syncthreads();
   return *bc;
-#else
-  return grid_reduce(v, red16, partials, bar, epoch, bc);
-#endif
 }
 
 // Grid barrier without a reduction (release arrival on the same counter / epoch as grid_reduce_rel).
@@ -250,10 +231,9 @@ __global__ void __launch_bounds__(128) k_hist_spmv_t(HistArgs A) {
     if (j < nh && act) A.V[j * R + E * N + lane] = v[j];
 }
 
-// Sums of the k_hist_gram partials and the nh x nh Galerkin system for the history weights
+// The nh x nh Galerkin system for the history weights from the sums of the k_hist_gram partials
 // (every thread solves it redundantly; the same arithmetic as pcg_initial_guess).
 __device__ __noinline__ void hist_weights(const PcgArgs& A, double* sh, double (&alpha_h)[8]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nh = A.nh;
 #pragma unroll
   for (int j = 0; j < 8; ++j) alpha_h[j] = 0.0;
@@ -365,10 +345,6 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
   double* yd = reinterpret_cast<double*>(dsm + L.yd) + (size_t)warp * 6 * 32;
   float* gs = reinterpret_cast<float*>(dsm + L.gs);
   float* bs = reinterpret_cast<float*>(dsm + L.bs) + (size_t)warp * A.n_pad;
-#if TM_GEMV
-  float* bs0 = reinterpret_cast<float*>(dsm + L.bs);
-  float* cr = reinterpret_cast<float*>(dsm + L.cr);
-#endif
   const int n4 = A.n_pad >> 2;   // float4 chunks of a coarse row
   const int tm_ncols = TM_COLS;
 
@@ -394,7 +370,6 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     lo[a] = own && a < dim && C[a] > 0;
   }
   const int ra = (lane >> 2) * 4, cb = lane & 3;
-#if TM_ASYNC_STAGE
   // Staging: the rows of the coarse inverse, the shared-memory coupling blocks and the deflation
   // vectors are copied with cp.async (no registers: they stream in the background) while the
   // TMEM-resident blocks go through registers and tcgen05.st.
@@ -447,46 +422,6 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
-#else
-  {
-    const double* Bd = A.blocks + (size_t)(own ? E : 0) * (1 + dim) * N * N;
-#pragma unroll 1
-    for (int a = 0; a < dim; ++a) {
-      if (!up[a]) continue;
-      const double* U = Bd + (size_t)(1 + a) * N * N;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t v[32];
-#pragma unroll
-        for (int ii = 0; ii < 2; ++ii)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int r = ra + 2 * h + ii, c = cb + 4 * j;
-            const double x = (r < N && c < N) ? U[r * N + c] : 0.0;
-            if (a < a_ov) {
-              v[2 * (ii * 8 + j)] = (uint32_t)__double2loint(x);
-              v[2 * (ii * 8 + j) + 1] = (uint32_t)__double2hiint(x);
-            } else {
-              ov[(size_t)(a - a_ov) * 1024 + (size_t)(16 * h + ii * 8 + j) * 32 + lane] = x;
-            }
-          }
-        if (a < a_ov) tm_st32(tcol + 64u * a + 32u * h, v);
-      }
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-  }
-#pragma unroll
-  for (int s = 0; s < 6; ++s) {
-    double v = 0.0;
-    if (A.use_coarse == 2 && act && side_exists(g, C, s)) v = A.Yd[((size_t)E * 6 + s) * N + lane];
-    yd[s * 32 + lane] = v;
-  }
-  if (A.use_coarse) {
-    const float4* src = reinterpret_cast<const float4*>(A.Binv + (size_t)(own ? E : 0) * A.n_pad);
-    float4* dst = reinterpret_cast<float4*>(bs);
-    for (int q = lane; q < (A.n_pad >> 2); q += 32) dst[q] = own ? __ldcs(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-#endif
   const double zh = act ? A.zh[E * N + lane] : 0.0;
   TM_SSTAMP(1);
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -511,71 +446,12 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(FULL, e, o);
     return e;
   };
-#if TM_GEMV
-  // The coarse product of all the CTA's rows sliced by COLUMNS: warp v takes a contiguous slice of
-  // the float4 chunks of gs and runs it against all W rows, so every row is read from shared memory
-  // once and gs once per CTA (C5: 120 KB per SM instead of 224 KB with a row per warp).  Lane
-  // partials -> 16-value reduce-scatter (lane l holds row l % 16) -> per-warp slots -> fixed-order
-  // sum over the warps.  Replaces coarse_dot in the iteration; CTA-uniform call (one barrier).
-  auto coarse_gemv = [&]() -> float {
-    const int n4c = A.n_pad >> 2;
-    const int q0 = (warp * n4c) / W, q1 = ((warp + 1) * n4c) / W;
-    const float4* g4 = reinterpret_cast<const float4*>(gs);
-    float acc[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc[k] = 0.f;
-    for (int q = q0 + lane; q < q1; q += 32) {
-      const float4 a = g4[q];
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < W) {
-          const float4 m = reinterpret_cast<const float4*>(bs0 + (size_t)j * A.n_pad)[q];
-          acc[j] = fmaf(m.w, a.w, fmaf(m.z, a.z, fmaf(m.y, a.y, fmaf(m.x, a.x, acc[j]))));
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const bool hi = lane & 8;
-      const float send = hi ? acc[i] : acc[i + 8];
-      const float keep = hi ? acc[i + 8] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(FULL, send, 8);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const bool hi = lane & 4;
-      const float send = hi ? acc[i] : acc[i + 4];
-      const float keep = hi ? acc[i + 4] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(FULL, send, 4);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const bool hi = lane & 2;
-      const float send = hi ? acc[i] : acc[i + 2];
-      const float keep = hi ? acc[i + 2] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(FULL, send, 2);
-    }
-    {
-      const bool hi = lane & 1;
-      const float send = hi ? acc[0] : acc[1];
-      const float keep = hi ? acc[1] : acc[0];
-      acc[0] = keep + __shfl_xor_sync(FULL, send, 1);
-    }
-    acc[0] += __shfl_xor_sync(FULL, acc[0], 16);
-    if (lane < 16) cr[warp * 32 + lane] = acc[0];
-    __syncthreads();
-    float t = 0.f;
-    for (int v = 0; v < W; ++v) t += cr[v * 32 + warp];
-    return t;
-  };
-#else
   auto coarse_gemv = [&]() -> float { return coarse_dot(); };
-#endif
   auto stage_wc = [&]() {
     for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) gs[i] = i < g.n_s ? (float)__ldcg(A.wc + i) : 0.f;
     __syncthreads();
   };
   auto stage_g = [&]() {   // Zh^T (I - Bh) r = -(sum of the six neighbour contributions), fixed order
-#if TM_G6
     const float* cw = A.cont_tm;   // [6][n_pad], coalesced float4 over F
     for (int q = threadIdx.x; q < (A.n_pad >> 2); q += blockDim.x) {
       float4 c[6];
@@ -588,17 +464,6 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
       v.w = -(((((c[0].w + c[1].w) + c[2].w) + c[3].w) + c[4].w) + c[5].w);
       reinterpret_cast<float4*>(gs)[q] = v;
     }
-#else
-    for (int i = threadIdx.x; i < A.n_pad; i += blockDim.x) {
-      float v = 0.f;
-      if (i < g.n_s) {
-        const float4 c0 = __ldcg(reinterpret_cast<const float4*>(A.cont + (size_t)i * 8));
-        const float4 c1 = __ldcg(reinterpret_cast<const float4*>(A.cont + (size_t)i * 8 + 4));
-        v = -(((((c0.x + c0.y) + c0.z) + c0.w) + c1.x) + c1.y);
-      }
-      gs[i] = v;
-    }
-#endif
     __syncthreads();
   };
   // contributions Y_{E,F} . r_E to the coarse rhs of the neighbours F (as defl_scatter)
@@ -630,11 +495,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     d[0] += __shfl_xor_sync(FULL, d[0], 2);
     d[0] += __shfl_xor_sync(FULL, d[0], 1);
     const int s = lane >> 2;
-#if TM_G6
     if (own && (lane & 3) == 0 && s < 6 && side_exists(g, C, s)) A.cont_tm[(size_t)s * A.n_pad + side_nb(g, E, s)] = (float)d[0];
-#else
-    if (own && (lane & 3) == 0 && s < 6 && side_exists(g, C, s)) A.cont[(size_t)side_nb(g, E, s) * 8 + s] = (float)d[0];
-#endif
   };
 
   unsigned epoch = 0;
@@ -776,16 +637,9 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
         if (lane == 0) A.wc[E] = w;
       }
       TM_STAMP(3);
-#if TM_BARB
       grid_barrier_rel(A.gbar, epoch);
-#else
-      rr = grid_reduce_rel(own ? warp_sum(r * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
-#endif
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
       TM_STAMP(4);
-#if !TM_BARB
-      if (!(rr > 0.0)) break;
-#endif
       // ---------------- C: z = M^-1 r, r.z
       if (A.use_coarse == 2) stage_g();
       else if (A.use_coarse == 1) stage_wc();
@@ -797,10 +651,8 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
       const double rz_new = grid_reduce_rel(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
       if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
       TM_STAMP(7);
-#if TM_BARB
       rr = rz_new;
       if (!(rz_new == rz_new)) break;   // NaN (flagged below)
-#endif
       if (rz_new <= tol2) break;
       beta = rz_new / rz;
       rz = rz_new;
