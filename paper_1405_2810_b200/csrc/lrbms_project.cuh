@@ -285,47 +285,37 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
     A.rhs[E * N + tid] = rr;
   }
 
-  // 5. coupling blocks B_{E,E+a}[i][j] = -sum_f w_f Phi_E[i][a_f] Phi_{E+a}[j][b_f]; every warp
-  //    interleaves up to three 8x8 output tiles (independent DMMA accumulator chains)
-  const int ntask = g.dim * T * T;
-  for (int t0 = warp; t0 < ntask; t0 += 3 * nwarp) {
-    const double* pe[3];
-    const double* pn[3];
-    const int* fca[3];
-    const double* wa[3];
-    double cc[3][2];
-    bool live[3];
+  // 5. coupling blocks B_{E,E+a}[i][j] = -sum_f w_f Phi_E[i][a_f] Phi_{E+a}[j][b_f]; a warp owns a
+  //    row of output tiles (a, ti) and its T accumulator chains share every A fragment (the gathered,
+  //    weighted own-face row), so each k-step loads 1 + T fragments for T DMMAs
+  const int ntask = g.dim * T;
+  for (int t = warp; t < ntask; t += nwarp) {
+    const int a = t / T, ti = t - a * T;
+    const bool live = has[a];
+    const double* pe = Phs + (size_t)(8 * ti + fr) * LD;
+    const int* fca = fcell + a * nfp;
+    const double* wa = wi + a * nfp;
+    const double* pn = PhN + (size_t)a * NP * LDN + (size_t)fr * LDN;
+    double cc[4][2];
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int t = t0 + u * nwarp;
-      cc[u][0] = cc[u][1] = 0.0;
-      live[u] = false;
-      pe[u] = Phs; pn[u] = PhN; fca[u] = fcell; wa[u] = wi;
-      if (t < ntask) {
-        const int a = t / (T * T), tt = t - a * T * T, ti = tt / T, tj = tt - ti * T;
-        live[u] = has[a];
-        pn[u] = PhN + (size_t)a * NP * LDN + (size_t)(8 * tj + fr) * LDN;
-        pe[u] = Phs + (size_t)(8 * ti + fr) * LD;
-        fca[u] = fcell + a * nfp;
-        wa[u] = wi + a * nfp;
+    for (int tj = 0; tj < 4; ++tj) cc[tj][0] = cc[tj][1] = 0.0;
+    if (live) {
+      for (int ks = 0; ks < nfp / 4; ++ks) {
+        const int f = 4 * ks + fc;
+        const double av = pe[fca[f]] * wa[f];
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj)
+          if (tj < T) dmma(cc[tj][0], cc[tj][1], av, pn[(size_t)8 * tj * LDN + f]);
       }
     }
-    for (int ks = 0; ks < nfp / 4; ++ks) {
-      const int f = 4 * ks + fc;
+    double* BEN = BEE + (size_t)(1 + a) * N * N;
+    const int i = 8 * ti + fr;
 #pragma unroll
-      for (int u = 0; u < 3; ++u)
-        if (live[u]) dmma(cc[u][0], cc[u][1], pe[u][fca[u][f]] * wa[u][f], pn[u][f]);
-    }
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int t = t0 + u * nwarp;
-      if (t >= ntask) continue;
-      const int a = t / (T * T), tt = t - a * T * T, ti = tt / T, tj = tt - ti * T;
-      double* BEN = BEE + (size_t)(1 + a) * N * N;
-      const int i = 8 * ti + fr, j0 = 8 * tj + 2 * fc;
-      if (i < N) {
-        if (j0 < N) BEN[i * N + j0] = -cc[u][0];
-        if (j0 + 1 < N) BEN[i * N + j0 + 1] = -cc[u][1];
+    for (int tj = 0; tj < 4; ++tj) {
+      const int j0 = 8 * tj + 2 * fc;
+      if (tj < T && i < N) {
+        if (j0 < N) BEN[i * N + j0] = -cc[tj][0];
+        if (j0 + 1 < N) BEN[i * N + j0 + 1] = -cc[tj][1];
       }
     }
   }
