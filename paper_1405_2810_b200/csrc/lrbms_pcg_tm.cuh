@@ -12,7 +12,7 @@
 //     b = dim m + a; slots b < 8 are TMEM columns 64 b .. +63, read back with tcgen05.ld every
 //     iteration (~300 B/SM-cycle measured, tools/mb_tmem.cu, vs ~127 B/cycle for shared memory);
 //   the overflow slots b >= 8 (3D, more than two warps per quadrant) -> shared memory,
-//     element-interleaved over lanes (bank-conflict free).  C5 (14 warps): 46 blocks in TMEM, 10 in
+//     element-interleaved over lanes (bank-conflict free).  C5 (14 warps): 32 blocks in TMEM (all 512 columns), 10 in
 //     shared memory;
 //   deflation vectors Y_{E,F} (6 per subdomain) and the fp32 rows of the coarse inverse B_c^-1 of
 //     the CTA's subdomains -> shared memory (C5: 221 KB in all).
