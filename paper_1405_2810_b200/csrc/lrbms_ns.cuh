@@ -23,7 +23,7 @@
 
 namespace lrbms {
 
-constexpr int NS_TM = 128, NS_TK = 32, NS_STAGES = 4;
+constexpr int NS_TM = 128, NS_TK = 32, NS_STAGES = 6;   // 6-stage TMA ring: 30 vs 33 us with 4
 constexpr int NS_TILE_BYTES = NS_TM * NS_TK * 4;                  // 16 KB per operand and stage
 constexpr int NS_TC_SMEM = 2 * NS_STAGES * NS_TILE_BYTES + 1024;  // + 1 KB alignment slack
 
