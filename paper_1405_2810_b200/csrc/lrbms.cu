@@ -752,7 +752,7 @@ struct lrbms_ctx {
   size_t proj_smem = 0;
   // workspace layout
   Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
-      Binv32, Binv32b, RTb, Es, Yd, cont, pflags, e0, partials, scal, gbar, gjrk, gjbar,
+      Binv32, Binv32b, RTb, Es, Yd, cont, e0, partials, scal, gbar, gjrk, gjbar,
       flags,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
   size_t ws_bytes = 0;
@@ -1041,8 +1041,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->RTb, (size_t)c->n_pad * c->n_pad * 4);
   alloc(c->Es, (size_t)g.n_s * 8 * 8);
   alloc(c->Yd, R * 6 * 8);
-  alloc(c->cont, (size_t)c->n_pad * (8 + 2 * 16) * 4);   // k_pcg [n_pad][8], then k_pcg_tm [2][n_pad][16]
-  alloc(c->pflags, 32 * (size_t)g.n_s * 4);
+  alloc(c->cont, (size_t)c->n_pad * (8 + 6) * 4);   // k_pcg [n_pad][8], then k_pcg_tm side-major [6][n_pad]
   alloc(c->e0, (size_t)c->n_pad * 8);
   alloc(c->gjbar, 256);
   alloc(c->flags, 4 * 16);
@@ -1159,7 +1158,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
       CUDA_TRY(c, cudaFuncSetAttribute(k_ns_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, NS_TC_SMEM));
   }
   // coarse-rhs contribution slots of absent neighbours are never written: zero them once
-  CUDA_TRY(c, cudaMemsetAsync(c->at<float>(c->cont), 0, (size_t)c->n_pad * (8 + 2 * 16) * 4, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<float>(c->cont), 0, (size_t)c->n_pad * (8 + 6) * 4, c->stream));
   CUDA_TRY(c, cudaFuncSetAttribute(k_ns_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    NS_SMEM));
   // link tables
@@ -1453,6 +1452,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     H.hist = c->at<double>(c->hist); H.W = c->at<double>(c->Wh); H.V = c->at<double>(c->Vh);
     H.TH = c->at<double>(c->TH); H.rb = c->at<double>(c->rbv); H.gpart = c->at<double>(c->gpart);
     H.nh = A.nh;
+    H.gbar_reset = c->at<unsigned>(c->gbar);
     for (int j = 0; j < 8; ++j) H.hslot[j] = ((c->hist_head - j) % KHIST + KHIST) % KHIST;
     const int nb = cdiv(g.n_s, 8);
     k_hist_transform<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
@@ -1481,12 +1481,9 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.gbar = c->at<unsigned>(c->gbar);
   A.Yd = c->at<double>(c->Yd); A.cont = c->at<float>(c->cont); A.cont_tm = A.cont + (size_t)c->n_pad * 8; A.e0 = c->at<double>(c->e0);
   StageScope sc_(c, 4);
-  CUDA_TRY(c, cudaMemsetAsync(A.gbar, 0, 256, c->stream));
-  void* args[] = {&A};
-  A.pflags = c->at<unsigned>(c->pflags);
+  void* args[] = {&A};   // A.gbar was zeroed by k_hist_transform
   if (forked) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->join_ev, 0));
   if (c->opts.onchip && c->tm_W > 0) {
-    CUDA_TRY(c, cudaMemsetAsync(A.pflags, 0, 32 * sizeof(unsigned) * g.n_s, c->stream));
     CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg_tm, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,
                                             c->stream));
   } else {

@@ -66,8 +66,7 @@ struct PcgArgs {
   const double* Yd;       // [n_s][6][N] deflation vectors Y_{E,F} = Bh_{E,F} zh_F (k_transform), mode 2
   float* cont;            // [n_pad][8] contributions Y_{E,F}.r_E to the coarse rhs of F, by side
   double* e0;             // [n_pad] coarse correction of the starting vector
-  float* cont_tm;         // k_pcg_tm coarse-rhs data: [n_pad][8] (r), then per parity [6][n_pad] (w) + [n_pad] (g(r))
-  unsigned* pflags;       // [2][n_s][32] k_pcg_tm neighbour flags (one 128-byte line each) (u published, hand-overs published), zeroed per launch
+  float* cont_tm;         // k_pcg_tm coarse-rhs contributions, side-major [6][n_pad]
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -627,12 +626,14 @@ struct HistArgs {
   double* gpart;          // [44][gridDim] Gram / rhs partials
   int nh;
   int hslot[8];
+  unsigned* gbar_reset;   // the PCG's grid-barrier counter, zeroed here (saves a memset per solve)
 };
 
 // warp per subdomain; each warp stages 32x32 blocks in its own padded shared tile
 __global__ void __launch_bounds__(128) k_hist_transform(HistArgs A) {
   __shared__ double tile[4][32 * 33];
   const Geo& g = A.g;
+  if (A.gbar_reset && blockIdx.x == 0 && threadIdx.x == 0) *A.gbar_reset = 0u;
   const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int E = blockIdx.x * 4 + warp;
   if (E >= g.n_s) return;
