@@ -129,9 +129,13 @@ __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
 __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
                                                       const double* __restrict__ zc, double* __restrict__ zh,
                                                       int* flags, double* __restrict__ Es) {
-  __shared__ double Ls[4][32 * 33];
-  const int lane = threadIdx.x & 31;
-  const int E = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // Lt[k][i] = L[i][k] (column k of L, published at step k by the lanes that hold it), rows padded
+  // to 34 doubles so that row starts stay 16-byte aligned (vector broadcast loads); rinv[k] = 1/L[k][k]
+  __shared__ __align__(16) double Lt[4][32 * 34];
+  __shared__ double rinv[4][32];
+  __shared__ double dg[4][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int E = blockIdx.x * (blockDim.x >> 5) + w;
   if (E >= g.n_s) return;
   const int N = g.N;
   double* Bd = blocks + (size_t)E * (1 + g.dim) * N * N;
@@ -139,52 +143,55 @@ __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __
 #pragma unroll
   for (int i = 0; i < 32; ++i) m[i] = (lane < N && i < N) ? Bd[i * N + lane] : (i == lane ? 1.0 : 0.0);
   bool bad = false;
-  const double d0 = lane < N ? Bd[lane * N + lane] : 1.0;   // original diagonal entry of this lane's column
-  // right-looking Cholesky on the full symmetric trailing matrix: lane j's m[k] = M[k][j] = M[j][k].
+  dg[w][lane] = lane < N ? Bd[lane * N + lane] : 1.0;   // original diagonal entries
+  double* lt = Lt[w];
+  // Right-looking Cholesky on the full symmetric trailing matrix: lane j's m[k] = M[k][j] = M[j][k],
+  // so at step k lane j >= k holds L[j][k] L[k][k] and publishes L[j][k] to row k of Lt; the rank-1
+  // update then reads column k back with broadcast loads, scaled by L[lane][k] on the trailing lanes
+  // and by 0 on the finished ones (no per-entry selects).  Lanes < k publish values nobody reads.
   // A pivot below 1e-13 of its original diagonal entry means a numerically rank-deficient Phi_E.
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     const double dkk = __shfl_sync(FULL, m[k], k);
-    bad |= !(dkk > 1e-13 * __shfl_sync(FULL, d0, k));
-    const double d = sqrt(dkk), rd = 1.0 / d;
+    bad |= !(dkk > 1e-13 * dg[w][k]);
+    const double rd = rsqrt(dkk);
     const double ljk = m[k] * rd;          // L[lane][k] for lane >= k
+    lt[k * 34 + lane] = ljk;
+    if (lane == 0) rinv[w][k] = rd;
+    __syncwarp();
+    const double lm = lane > k ? ljk : 0.0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (i <= k) continue;
-      const double ci = __shfl_sync(FULL, m[i], k) * rd;   // L[i][k]
-      if (lane > k) m[i] -= ci * ljk;
-      else if (lane == k) m[i] = ci;
-    }
-    if (lane == k) {
-      m[k] = d;
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (i < k) m[i] = 0.0;
-    }
+    for (int i = 0; i < 32; ++i)
+      if (i > k) m[i] = fma(-lt[k * 34 + i], lm, m[i]);
   }
   if (bad && lane == 0) atomicOr(flags, FLAG_PIVOT);
+  __syncwarp();
+  // column lane of L: L[i][lane] = Lt[lane][i] for i >= lane
   const double zk = lane < N ? zc[E * N + lane] : 0.0;
+  dg[w][lane] = zk;
+  __syncwarp();
   double zhat = 0.0;   // (L^T zc)[lane] = sum_i L[i][lane] zc[i]
 #pragma unroll
-  for (int i = 0; i < 32; ++i) zhat += m[i] * __shfl_sync(FULL, zk, i);
-  // lane holds column lane of L in m[]: L[i][lane] = m[i] -> Ls[i][lane]
-  double* ls = Ls[threadIdx.x >> 5];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) ls[i * 33 + lane] = m[i];
+  for (int i = 0; i < 32; ++i) {
+    m[i] = i >= lane ? lt[lane * 34 + i] : 0.0;
+    zhat = fma(m[i], dg[w][i], zhat);
+  }
   if (lane < N) {
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      if (i < N) Bd[i * N + lane] = m[i];   // L in the diagonal slot
+      if (i < N) Bd[i * N + lane] = m[i];   // L in the diagonal slot (read by k_hist_transform)
   }
-  __syncwarp();
-  // L^-1 by forward substitution, one column per lane: L x = e_lane, L rows read from shared memory
+  // L^-1 by column-oriented forward substitution, one column per lane: L x = e_lane; column k of L
+  // is row k of Lt (vector broadcast loads)
   double x[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double acc = (i == lane) ? 1.0 : 0.0;
+  for (int i = 0; i < 32; ++i) x[i] = i == lane ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = 0; k < i; ++k) acc -= ls[i * 33 + k] * x[k];
-    x[i] = acc * (1.0 / ls[i * 33 + i]);
+  for (int k = 0; k < 32; ++k) {
+    x[k] *= rinv[w][k];
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i > k) x[i] = fma(-lt[k * 34 + i], x[k], x[i]);
   }
   if (lane < N) {
     double* Li = Linv + (size_t)E * N * N;
