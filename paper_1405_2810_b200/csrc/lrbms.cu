@@ -1401,12 +1401,22 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   const Geo& g = c->g;
   const int mode = (c->opts.use_coarse && g.n_s > 1) ? c->opts.use_coarse : 0;
   const bool coarse = mode > 0;
+  const size_t R = (size_t)g.n_s * g.N;
+  // inputs of the Galerkin initial guess; W = L^T c^{n-j} and rb = L^-1 b are formed by k_block_chol
+  HistArgs H;
+  H.g = g;
+  H.blocks = c->at<double>(c->blocks); H.Linv = c->at<double>(c->Linv); H.rhs = c->at<double>(c->rhs);
+  H.hist = c->at<double>(c->hist); H.W = c->at<double>(c->Wh); H.V = c->at<double>(c->Vh);
+  H.TH = c->at<double>(c->TH); H.rb = c->at<double>(c->rbv); H.gpart = c->at<double>(c->gpart);
+  H.nh = std::min(c->hist_count, c->opts.history);
+  H.gbar_reset = c->at<unsigned>(c->gbar);
+  for (int j = 0; j < 8; ++j) H.hslot[j] = ((c->hist_head - j) % KHIST + KHIST) % KHIST;
   {
     StageScope sc_(c, 2);   // block Cholesky + scaling of the couplings: Bh = L^-1 B L^-T (+ coarse stencil)
     double* es = coarse ? c->at<double>(c->Es) : nullptr;
     k_block_chol<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
                                                          c->at<double>(c->zc), c->at<double>(c->zh),
-                                                         c->at<int>(c->flags), es);
+                                                         c->at<int>(c->flags), es, H);
     LAUNCH_CHECK(c);
     k_transform_h<<<cdiv(g.n_s * g.dim, 4), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
                                                                 c->at<double>(c->zh),
@@ -1439,24 +1449,13 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.rhs = c->at<double>(c->rhs); A.zh = c->at<double>(c->zh);
   A.Binv = coarse_x(c, c->xcur);
   A.x = c->at<double>(c->c); A.y = c->at<double>(c->yv);
-  const size_t R = (size_t)g.n_s * g.N;
-  A.nh = std::min(c->hist_count, c->opts.history);
+  A.nh = H.nh;
   const int out_slot = (c->hist_head + 1) % KHIST;
   A.hist_out = c->at<double>(c->hist) + (size_t)out_slot * R;
   A.W = c->at<double>(c->Wh); A.V = c->at<double>(c->Vh); A.rb = c->at<double>(c->rbv);
   {
     StageScope sh_(c, 3);
-    HistArgs H;
-    H.g = g;
-    H.blocks = c->at<double>(c->blocks); H.Linv = c->at<double>(c->Linv); H.rhs = c->at<double>(c->rhs);
-    H.hist = c->at<double>(c->hist); H.W = c->at<double>(c->Wh); H.V = c->at<double>(c->Vh);
-    H.TH = c->at<double>(c->TH); H.rb = c->at<double>(c->rbv); H.gpart = c->at<double>(c->gpart);
-    H.nh = A.nh;
-    H.gbar_reset = c->at<unsigned>(c->gbar);
-    for (int j = 0; j < 8; ++j) H.hslot[j] = ((c->hist_head - j) % KHIST + KHIST) % KHIST;
     const int nb = cdiv(g.n_s, 8);
-    k_hist_transform<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
-    LAUNCH_CHECK(c);
     if (H.nh > 0) {
       k_hist_spmv_t<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
       LAUNCH_CHECK(c);
@@ -1481,7 +1480,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   A.gbar = c->at<unsigned>(c->gbar);
   A.Yd = c->at<double>(c->Yd); A.cont = c->at<float>(c->cont); A.cont_tm = A.cont + (size_t)c->n_pad * 8; A.e0 = c->at<double>(c->e0);
   StageScope sc_(c, 4);
-  void* args[] = {&A};   // A.gbar was zeroed by k_hist_transform
+  void* args[] = {&A};   // A.gbar was zeroed by k_block_chol
   if (forked) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->join_ev, 0));
   if (c->opts.onchip && c->tm_W > 0) {
     CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg_tm, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,

@@ -120,6 +120,23 @@ __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
   return w[0];
 }
 
+// Inputs of the Galerkin initial guess (below): the history ring buffer and its transformed copies.
+struct HistArgs {
+  Geo g;
+  const double* blocks;   // scaled couplings in slots 1..dim
+  const double* Linv;
+  const double* rhs;
+  const double* hist;     // [KH][R] ring buffer
+  double* W;              // [KH][R]
+  double* V;              // [KH][R]
+  double* TH;             // [KH][n_s][3][N]
+  double* rb;             // [R]  L^-1 b
+  double* gpart;          // [44][gridDim] Gram / rhs partials
+  int nh;
+  int hslot[8];
+  unsigned* gbar_reset;   // the PCG's grid-barrier counter, zeroed by k_block_chol (saves a memset per solve)
+};
+
 // ============================================================================ factorisation + transform
 
 // Warp per subdomain.  Lane j holds column j of the (padded-to-32 with identity) block.
@@ -128,13 +145,15 @@ __device__ __forceinline__ double reduce_scatter32(double (&w)[32], int lane) {
 #endif
 __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
                                                       const double* __restrict__ zc, double* __restrict__ zh,
-                                                      int* flags, double* __restrict__ Es) {
+                                                      int* flags, double* __restrict__ Es, const HistArgs H) {
   // Lt[k][i] = L[i][k] (column k of L, published at step k by the lanes that hold it), rows padded
   // to 34 doubles so that row starts stay 16-byte aligned (vector broadcast loads); rinv[k] = 1/L[k][k]
   __shared__ __align__(16) double Lt[4][32 * 34];
   __shared__ double rinv[4][32];
   __shared__ double dg[4][32];
+  __shared__ __align__(16) double xs[4][32 * 8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (H.gbar_reset && blockIdx.x == 0 && threadIdx.x == 0) *H.gbar_reset = 0u;
   const int E = blockIdx.x * (blockDim.x >> 5) + w;
   if (E >= g.n_s) return;
   const int N = g.N;
@@ -176,11 +195,6 @@ __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __
     m[i] = i >= lane ? lt[lane * 34 + i] : 0.0;
     zhat = fma(m[i], dg[w][i], zhat);
   }
-  if (lane < N) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < N) Bd[i * N + lane] = m[i];   // L in the diagonal slot (read by k_hist_transform)
-  }
   // L^-1 by column-oriented forward substitution, one column per lane: L x = e_lane; column k of L
   // is row k of Lt (vector broadcast loads)
   double x[32];
@@ -199,6 +213,35 @@ __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __
     for (int i = 0; i < 32; ++i)
       if (i < N) Li[i * N + lane] = x[i];
     zh[E * N + lane] = zhat;
+  }
+  // the initial guess's inputs (fused: L and L^-1 are at hand here)
+  //   rb = L^-1 b: row lane of L^-1 from shared memory (x[] holds column lane), b broadcast;
+  //   W_j = L^T c^{n-j}, j < nh: W_j[lane] = sum_i L[i][lane] c_j[i], c_j[i] broadcast as xs[i][j].
+  const size_t R = (size_t)g.n_s * N;
+  const bool act = lane < N;
+  __syncwarp();   // every lane is done reading Lt
+#pragma unroll
+  for (int i = 0; i < 32; ++i) lt[i * 34 + lane] = x[i];
+  dg[w][lane] = act ? H.rhs[E * N + lane] : 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    xs[w][lane * 8 + j] = (j < H.nh && act) ? H.hist[(size_t)H.hslot[j] * R + E * N + lane] : 0.0;
+  __syncwarp();
+  double rbk = 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) rbk = fma(lt[lane * 34 + k], dg[w][k], rbk);
+  if (act) H.rb[E * N + lane] = rbk;
+  if (H.nh > 0) {
+    double wk[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) wk[j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) wk[j] = fma(m[i], xs[w][i * 8 + j], wk[j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < H.nh && act) H.W[j * R + E * N + lane] = wk[j];
   }
   if (Es) {   // coarse operator diagonal zc^T B_EE zc = |L^T zc|^2; the side slots are set by k_transform
     const double d = warp_sum(lane < N ? zhat * zhat : 0.0);
@@ -620,64 +663,6 @@ __device__ __forceinline__ double grid_total(const double* partials, int slot) {
 // Three small kernels (W and rb; V = Bh W with one read of every coupling block; Gram partials)
 // precede k_pcg, which solves the nh x nh system redundantly in every thread.
 
-struct HistArgs {
-  Geo g;
-  const double* blocks;   // L in slot 0, scaled couplings
-  const double* Linv;
-  const double* rhs;
-  const double* hist;     // [KH][R] ring buffer
-  double* W;              // [KH][R]
-  double* V;              // [KH][R]
-  double* TH;             // [KH][n_s][3][N]
-  double* rb;             // [R]  L^-1 b
-  double* gpart;          // [44][gridDim] Gram / rhs partials
-  int nh;
-  int hslot[8];
-  unsigned* gbar_reset;   // the PCG's grid-barrier counter, zeroed here (saves a memset per solve)
-};
-
-// warp per subdomain; each warp stages 32x32 blocks in its own padded shared tile
-__global__ void __launch_bounds__(128) k_hist_transform(HistArgs A) {
-  __shared__ double tile[4][32 * 33];
-  const Geo& g = A.g;
-  if (A.gbar_reset && blockIdx.x == 0 && threadIdx.x == 0) *A.gbar_reset = 0u;
-  const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int E = blockIdx.x * 4 + warp;
-  if (E >= g.n_s) return;
-  const bool act = lane < N;
-  const size_t R = (size_t)g.n_s * N;
-  double* ts = tile[warp];
-  const double* L = A.blocks + (size_t)E * (1 + g.dim) * N * N;
-  for (int k = 0; k < N; ++k)
-    if (act) ts[k * 33 + lane] = L[k * N + lane];
-  double xk[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) xk[j] = (j < A.nh && act) ? A.hist[(size_t)A.hslot[j] * R + E * N + lane] : 0.0;
-  __syncwarp();
-  double wk[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) wk[j] = 0.0;
-  for (int i = 0; i < N; ++i) {   // W_j[lane] = sum_i L[i][lane] x_j[i]
-    const double lil = act ? ts[i * 33 + lane] : 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) wk[j] += lil * __shfl_sync(FULL, xk[j], i);
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if (j < A.nh && act) A.W[j * R + E * N + lane] = wk[j];
-  __syncwarp();
-  const double* Li = A.Linv + (size_t)E * N * N;
-  for (int k = 0; k < N; ++k)
-    if (act) ts[k * 33 + lane] = Li[k * N + lane];
-  const double bk = act ? A.rhs[E * N + lane] : 0.0;
-  __syncwarp();
-  double rbk = 0.0;   // (L^-1 b)[lane] = sum_k Linv[lane][k] b[k]
-  for (int k = 0; k < N; ++k) {
-    const double bkk = __shfl_sync(FULL, bk, k);
-    if (act) rbk += ts[lane * 33 + k] * bkk;
-  }
-  if (act) A.rb[E * N + lane] = rbk;
-}
 
 // complete V (lower hand-overs), Gram partials G_ij = W_i.V_j (i <= j) and g_i = W_i.rb per CTA
 __global__ void __launch_bounds__(256) k_hist_gram(HistArgs A) {
