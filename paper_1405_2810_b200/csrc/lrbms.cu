@@ -620,7 +620,10 @@ __device__ __forceinline__ size_t face_index(const Geo& g, int i, int j, int k, 
 }
 
 // a5: Q_i = max(sum of outflow, sum of inflow); dt = cfl min phi V / (f'max Q)   (R4)
-__global__ void __launch_bounds__(512) k_flux_cfl(FluxArgs A) {
+#ifndef FLUX_MINB
+#define FLUX_MINB 3
+#endif
+__global__ void __launch_bounds__(512, FLUX_MINB) k_flux_cfl(FluxArgs A) {
   extern __shared__ double sm[];
   const Geo& g = A.g;
   const int E = blockIdx.x, nl = g.n_loc;

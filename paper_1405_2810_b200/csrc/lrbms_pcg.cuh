@@ -263,7 +263,10 @@ __device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double 
 // coupling zh_E . Y from the accumulator layout.  The column sums of
 // Y_{E+a,E} and the coarse coupling combine the two halves through shared memory in a fixed order.
 // CTA = 4 blocks x 2 halves.
-__global__ void __launch_bounds__(256, 2) k_transform_h(Geo g, double* __restrict__ blocks,
+#ifndef TRANSFORM_MINB
+#define TRANSFORM_MINB 2
+#endif
+__global__ void __launch_bounds__(256, TRANSFORM_MINB) k_transform_h(Geo g, double* __restrict__ blocks,
                                                     const double* __restrict__ Linv,
                                                     const double* __restrict__ zh, double* __restrict__ Yd,
                                                     double* __restrict__ Es) {
