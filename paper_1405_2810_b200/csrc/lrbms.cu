@@ -263,10 +263,11 @@ __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restric
       nb[1 + s] = j;
     }
   }
-#pragma unroll 8
-  for (int r = 0; r < RT_ROWS; ++r) {   // unrolled: the 7 loads of several rows in flight at once
+  // n (n_pad) is a multiple of 32, so all RT_ROWS rows exist: no exit inside the unrolled loop, the
+  // loads of every row are independent and issue back to back
+#pragma unroll
+  for (int r = 0; r < RT_ROWS; ++r) {
     const int i = i0 + r;
-    if (i >= n) break;
     const float* xi = X + (size_t)i * n;
     float v = __ldg(xi + nb[0]) * e[0];
 #pragma unroll
