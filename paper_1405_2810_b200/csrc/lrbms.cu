@@ -235,7 +235,16 @@ __global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* flags)
 // RT = I - X E = (I - E X)^T for symmetric X (the tensor-core update keeps X exactly symmetric):
 // RT[i][j] = delta_ij - sum_{G in {j} + nb(j)} X[i][G] E_{jG}; j >= n_s: identity padding of E.
 // Row-wise, coalesced over j.  Its rows are the K-major B operand of k_ns_gemm_tc.
-constexpr int RT_ROWS = 16;   // rows of RT per CTA (the column's stencil is loaded once per CTA)
+#ifndef RT_ROWS_V
+#define RT_ROWS_V 16
+#endif
+#ifndef RT_BATCH_V
+#define RT_BATCH_V 8
+#endif
+constexpr int RT_ROWS = RT_ROWS_V;     // rows of RT per CTA (the column's stencil is loaded once per CTA)
+constexpr int RT_BATCH = RT_BATCH_V;   // rows whose loads are in flight together
+static_assert(32 % RT_ROWS == 0, "n_pad is a multiple of 32: every CTA's rows exist");
+static_assert(RT_ROWS % RT_BATCH == 0, "whole batches");
 __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restrict__ X, const double* __restrict__ Es,
                                                    float* __restrict__ RT, int n) {
   // thread <-> column j: its stencil (coefficients, neighbour columns) in registers, reused for
@@ -263,16 +272,26 @@ __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restric
       nb[1 + s] = j;
     }
   }
-  // n (n_pad) is a multiple of 32, so all RT_ROWS rows exist: no exit inside the unrolled loop, the
-  // loads of every row are independent and issue back to back
+  // n (n_pad) is a multiple of 32, so all RT_ROWS rows exist.  The 7 loads of RT_BATCH rows are
+  // issued before any of them is used (explicit batches: left to itself the compiler works row by
+  // row at 40 registers, one memory round trip per row)
 #pragma unroll
-  for (int r = 0; r < RT_ROWS; ++r) {
-    const int i = i0 + r;
-    const float* xi = X + (size_t)i * n;
-    float v = __ldg(xi + nb[0]) * e[0];
+  for (int r0 = 0; r0 < RT_ROWS; r0 += RT_BATCH) {
+    float xv[RT_BATCH][7];
 #pragma unroll
-    for (int s = 1; s < 7; ++s) v = fmaf(__ldg(xi + nb[s]), e[s], v);
-    RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+    for (int r = 0; r < RT_BATCH; ++r) {
+      const float* xi = X + (size_t)(i0 + r0 + r) * n;
+#pragma unroll
+      for (int s = 0; s < 7; ++s) xv[r][s] = __ldg(xi + nb[s]);
+    }
+#pragma unroll
+    for (int r = 0; r < RT_BATCH; ++r) {
+      const int i = i0 + r0 + r;
+      float v = xv[r][0] * e[0];
+#pragma unroll
+      for (int s = 1; s < 7; ++s) v = fmaf(xv[r][s], e[s], v);
+      RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+    }
   }
 }
 
