@@ -153,6 +153,27 @@ lrbms_status lrbms_set_profiles(lrbms_ctx *ctx, const double *s_profiles, int32_
 lrbms_status lrbms_set_online(lrbms_ctx *ctx, int32_t affine);
 lrbms_status lrbms_stage_theta(lrbms_ctx *ctx, double *theta);
 
+/* NEXT-2: the fine-scale reference scheme on the GPU -- alg:highDimTwoPhaseFlow
+ * at k = 0, i.e. the online step with Phi_E = I: per step the fine pressure
+ * system of def:pressureDG, A(lambda) p = b(lambda) with A = sum_F w_F (e_a - e_b)
+ * (e_a - e_b)^T + sum_L g_L e_a e_a^T and b = sum_L g_L p_L e_a (reading R2 weights), solved by a
+ * Jacobi-preconditioned CG (cooperative kernel, deterministic reductions) warm-started from the
+ * current pressure and stopped when r.D^-1 r <= rtol^2 b.D^-1 b; then the same fluxes, CFL step
+ * and upwind transport as lrbms_run.  The paper's comparison run (speed-up).
+ *
+ * lrbms_fine_bytes: size of the caller-owned fine workspace (10 n doubles + 6 n int32 + scratch).
+ * lrbms_run_fine: n_steps, cfl, dt_fixed, dt_log as lrbms_run; ws (dev, 256-byte aligned, >= the
+ * size above, owned by the caller, used only during the call); rtol > 0, max_iters > 0 per solve;
+ * iters_total (host, NULL = skip) receives the CG iterations summed over the steps.  Needs
+ * set_medium and set_saturation (not set_basis); the pressure of the last step is what
+ * lrbms_get_state returns afterwards.  The reduced solver's history is not updated.  Errors: CONFIG
+ * (arguments, workspace), STATE, NUMERICAL (non-convergence within max_iters, breakdown, NaN,
+ * no flow), CUDA.  Synchronises the stream once at the end. */
+size_t       lrbms_fine_bytes(const lrbms_ctx *ctx);
+lrbms_status lrbms_run_fine(lrbms_ctx *ctx, int32_t n_steps, double cfl, double dt_fixed,
+                            double *dt_log, void *ws, size_t bytes, double rtol, int32_t max_iters,
+                            int64_t *iters_total);
+
 /* Advance n_steps online steps a1..a6 on the bound stream, no host round trip per step.
  * dt_fixed > 0 overrides the CFL step (the paper's fixed N_T); otherwise
  * dt^n = cfl * min_i phi_i V_i / (f'_max Q_i) (reading R4).  dt_log (dev, n_steps) or NULL.

@@ -30,6 +30,7 @@
 #include "lrbms_project.cuh"
 #include "lrbms_ns.cuh"
 #include "lrbms_affine.cuh"
+#include "lrbms_fine.cuh"
 
 using namespace lrbms;
 
@@ -784,6 +785,7 @@ struct lrbms_ctx {
   bool bound = false, have_medium = false, have_phi = false, have_basis = false, have_sat = false;
   bool poisoned = false;
   bool have_blocks = false;
+  bool p_valid = false;        // the pressure buffer holds a pressure (warm start of the fine solve)
   int cur = 0;                 // which s buffer is current
   int64_t steps = 0, total_iters = 0, launches = 0, solves = 0;
   int hist_count = 0, hist_head = KHIST - 1;   // ring buffer of previous solutions (initial guess)
@@ -1526,6 +1528,7 @@ static lrbms_status launch_recon(lrbms_ctx* c) {
   k_recon<<<g.n_s, nt, 0, c->stream>>>(g, c->at<double>(c->Phi), c->at<double>(c->c), c->at<double>(c->p),
                                        (unsigned long long*)c->at<double>(c->scal));
   LAUNCH_CHECK(c);
+  c->p_valid = true;
   return LRBMS_OK;
 }
 
@@ -1744,6 +1747,79 @@ lrbms_status lrbms_stage_theta(lrbms_ctx* c, double* theta) {
   if (theta) CUDA_TRY(c, cudaMemcpyAsync(theta, th, 8 * (size_t)c->prof_M, cudaMemcpyDeviceToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return LRBMS_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-2: fine-scale reference run
+static void fine_layout(const lrbms_ctx* c, size_t* offs, size_t* total) {
+  const size_t n = c->g.n;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  for (int k = 0; k < 10; ++k) offs[k] = take(n * 8);   // r z p0 p1 q diag rhs w[3]
+  offs[10] = take(6 * n * 4);                             // nbr
+  offs[11] = take(8 * 4 * 4096);                          // partials (G <= 4096)
+  offs[12] = take(256);                                   // barrier counter, iteration counters
+  *total = off;
+}
+
+size_t lrbms_fine_bytes(const lrbms_ctx* c) {
+  if (!c) return 0;
+  size_t offs[13], total;
+  fine_layout(c, offs, &total);
+  return total;
+}
+
+lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt_fixed, double* dt_log, void* ws,
+                            size_t bytes, double rtol, int32_t max_iters, int64_t* iters_total) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!c->have_medium || !c->have_sat) return fail(c, LRBMS_E_STATE, "set_medium and set_saturation must precede the fine run");
+  if (n_steps < 0) return fail(c, LRBMS_E_CONFIG, "n_steps < 0");
+  if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
+  if (!(rtol > 0) || max_iters <= 0) return fail(c, LRBMS_E_CONFIG, "fine solve needs rtol > 0 and max_iters > 0");
+  size_t offs[13], total;
+  fine_layout(c, offs, &total);
+  if (!ws || bytes < total || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(c, LRBMS_E_CONFIG, "fine workspace missing, smaller than lrbms_fine_bytes or not 256-byte aligned");
+  const Geo& g = c->g;
+  char* b = static_cast<char*>(ws);
+  FineArgs F;
+  F.g = g; F.L = links_of(c);
+  F.fc = c->at<double2>(c->fc);
+  F.x = c->at<double>(c->p);
+  double* v[10];
+  for (int k = 0; k < 10; ++k) v[k] = reinterpret_cast<double*>(b + offs[k]);
+  F.r = v[0]; F.z = v[1]; F.p0 = v[2]; F.p1 = v[3]; F.q = v[4]; F.diag = v[5]; F.rhs = v[6]; F.w = v[7];
+  F.nbr = reinterpret_cast<int*>(b + offs[10]);
+  F.partials = reinterpret_cast<double*>(b + offs[11]);
+  F.bar = reinterpret_cast<unsigned*>(b + offs[12]);
+  F.iters = reinterpret_cast<int*>(b + offs[12] + 128);
+  F.flags = c->at<int>(c->flags);
+  F.rtol = rtol; F.max_iters = max_iters;
+  F.dt_bits = (unsigned long long*)c->at<double>(c->scal);
+  int per_sm = 0;
+  CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fine_pcg, 256, 0));
+  const int G = std::min(4096, std::max(1, per_sm) * c->sms);
+  const int nt = std::min(512, cdiv(g.n_loc, 32) * 32);
+  if (16 * (size_t)g.n_loc > 48 * 1024) return fail(c, LRBMS_E_CONFIG, "fine run: subdomain too large (n_loc > 3072)");
+  if (!c->p_valid) CUDA_TRY(c, cudaMemsetAsync(F.x, 0, 8 * (size_t)g.n, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(F.iters, 0, 8, c->stream));
+  for (int k = 0; k < n_steps; ++k) {
+    F.lam = c->lam_cur();
+    F.build_nbr = k == 0;
+    k_fine_setup<<<g.n_s, nt, 16 * (size_t)g.n_loc, c->stream>>>(F);
+    LAUNCH_CHECK(c);
+    CUDA_TRY(c, cudaMemsetAsync(F.bar, 0, 4, c->stream));
+    void* args[] = {&F};
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_fine_pcg, dim3(G), dim3(256), args, 0, c->stream));
+    c->launches++;
+    c->p_valid = true;
+    if ((st = launch_transport(c, cfl, dt_fixed, dt_log, k, nullptr, nullptr))) return st;
+  }
+  int it[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(it, F.iters, 8, cudaMemcpyDeviceToHost, c->stream));
+  st = finish(c, n_steps);
+  if (iters_total) *iters_total = it[1];
+  return st;
 }
 
 lrbms_status lrbms_stage_project(lrbms_ctx* c, double* blocks, double* r) {

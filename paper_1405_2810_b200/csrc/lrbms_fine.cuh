@@ -1,0 +1,182 @@
+// lrbms_fine.cuh -- NEXT-2: the fine-scale reference scheme on the GPU.
+//
+//   alg:highDimTwoPhaseFlow at k = 0: per step the fine pressure system
+//   A(lambda(s^n)) p = b(lambda(s^n)) of def:pressureDG (at k = 0 the operator of
+//   eq:swipBilP reduces to A = sum_F w_F (e_a - e_b)(e_a - e_b)^T + sum_L g_L e_a e_a^T,
+//   b = sum_L g_L p_L e_a with the face weights of reading R2), then the same fluxes, CFL step and
+//   upwind transport as the reduced scheme (k_flux_cfl, k_transport).  This is the paper's
+//   comparison run (the speed-up of P:1300-1302), i.e. the LRBMS step with Phi_E = I.
+//
+// Kernels:
+//   k_fine_setup (CTA per subdomain, thread per cell): the static neighbour table (first call),
+//     the + face weights w[a][i] = T_F (tau_a lambda_i + tau_b lambda_nb), the diagonal
+//     d_i = sum of the weights of the faces of i + sum of its link weights, and b (links in the
+//     subdomain's link order, by one thread: deterministic).
+//   k_fine_pcg (cooperative, grid-stride over cells): Jacobi-preconditioned CG, warm-started from
+//     the previous pressure, two grid reductions per iteration (p.Ap; r.z), the search direction
+//     p_new = z + beta p formed on the fly for the neighbours inside the SpMV (double-buffered p);
+//     stop when r.z <= rtol^2 b.D^-1 b.  Deterministic (fixed-order per-CTA partials).
+#pragma once
+#include "lrbms_kernels.cuh"
+
+namespace lrbms {
+
+struct FineArgs {
+  Geo g;
+  Links L;
+  const double2* fc;   // [n][3] static face coefficients (T tau_a, T tau_b) of the + face per axis
+  const double* lam;   // [n] lambda_t(s^n)
+  double* x;           // [n] pressure (warm start in, solution out): the context's p
+  double* r;
+  double* z;
+  double* p0;          // search direction, double buffered
+  double* p1;
+  double* q;           // A p
+  double* diag;        // [n]
+  double* rhs;         // [n]
+  double* w;           // [3][n] + face weight of cell i along axis a (0 without a + neighbour)
+  int* nbr;            // [6][n] neighbour of cell i on side d = 2 a + (dir > 0), -1 outside
+  double* partials;    // [4][gridDim]
+  unsigned* bar;       // grid-barrier counter (zeroed before the launch)
+  int* iters;          // [0]: iterations of the last solve, [1]: running total
+  int* flags;
+  double rtol;
+  int max_iters;
+  int build_nbr;       // 1: k_fine_setup fills nbr (first call of a run)
+  unsigned long long* dt_bits;   // the step's dt minimum (reset here, as k_recon does for the reduced step)
+};
+
+__global__ void __launch_bounds__(512) k_fine_setup(FineArgs A) {
+  extern __shared__ double fsm[];
+  double* dg = fsm;                // [n_loc] diagonal
+  double* bl = fsm + A.g.n_loc;    // [n_loc] right-hand side
+  const Geo& g = A.g;
+  const int E = blockIdx.x, nl = g.n_loc;
+  const size_t n = g.n;
+  int C[3];
+  sub_xyz(g, E, C);
+  const size_t base = (size_t)E * nl;
+  if (E == 0 && threadIdx.x == 0) *A.dt_bits = 0x7ff0000000000000ull;   // +inf
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    int c[3];
+    local_xyz(g, l, c);
+    const size_t gl = base + l;
+    const double ll = A.lam[gl];
+    double d = 0.0;
+    for (int a = 0; a < 3; ++a)
+      for (int t = 0; t < 2; ++t) {
+        const int dir = t ? 1 : -1;
+        const int nb = a < g.dim ? neighbour(g, E, C, l, c, a, dir) : -1;
+        if (A.build_nbr) A.nbr[(size_t)(2 * a + t) * n + gl] = nb;
+        if (nb < 0) {
+          if (t) A.w[(size_t)a * n + gl] = 0.0;
+          continue;
+        }
+        // the face between this cell and nb: T1 = the lower cell along a (eq:upwind orientation)
+        const double wf = t ? face_w(A.fc[gl * 3 + a], ll, A.lam[nb]) : face_w(A.fc[(size_t)nb * 3 + a], A.lam[nb], ll);
+        if (t) A.w[(size_t)a * n + gl] = wf;
+        d += wf;
+      }
+    dg[l] = d;
+    bl[l] = 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int qi = A.L.sub_start[E]; qi < A.L.sub_start[E + 1]; ++qi) {
+      const int l = A.L.local[qi];
+      const double gL = A.L.gK[qi] * A.lam[base + l];
+      dg[l] += gL;
+      bl[l] += gL * A.L.p[qi];
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    A.diag[base + l] = dg[l];
+    A.rhs[base + l] = bl[l];
+  }
+}
+
+// (A v)_i = d_i v_i - sum over the faces of i of w_F v_nb, with v_j = vz[j] + beta * vp[j] for
+// every j (beta = 0, vp = nullptr: v = vz)
+__device__ __forceinline__ double fine_apply(const FineArgs& A, size_t i, const double* vz, const double* vp,
+                                             double beta, double vi) {
+  const size_t n = A.g.n;
+  double acc = A.diag[i] * vi;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) {
+    const int j = A.nbr[(size_t)d * n + i];
+    if (j < 0) continue;
+    const double wf = (d & 1) ? A.w[(size_t)(d >> 1) * n + i] : A.w[(size_t)(d >> 1) * n + j];
+    const double vj = vp ? fma(beta, vp[j], vz[j]) : vz[j];
+    acc = fma(-wf, vj, acc);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) k_fine_pcg(FineArgs A) {
+  __shared__ double red16[16];
+  __shared__ double bc[1];
+  unsigned epoch = 0;
+  const size_t n = A.g.n;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // r = b - A x, z = D^-1 r
+  double prz = 0.0, pbb = 0.0;
+  for (size_t i = i0; i < n; i += stride) {
+    const double ri = A.rhs[i] - fine_apply(A, i, A.x, nullptr, 0.0, A.x[i]);
+    const double zi = ri / A.diag[i];
+    A.r[i] = ri;
+    A.z[i] = zi;
+    prz = fma(ri, zi, prz);
+    pbb = fma(A.rhs[i], A.rhs[i] / A.diag[i], pbb);
+  }
+  double rz = grid_reduce_rel(warp_sum(prz), red16, A.partials, A.bar, epoch, &bc[0]);
+  const double bb = grid_reduce_rel(warp_sum(pbb), red16, A.partials, A.bar, epoch, &bc[0]);
+  const double tol2 = A.rtol * A.rtol * bb;
+  double beta = 0.0;
+  int it = 0;
+  bool ok = true;
+  while (rz > tol2 && it < A.max_iters) {
+    // phase A: p_new = z + beta p (p = the previous direction, absent in the first iteration),
+    // q = A p_new with the neighbours' p_new formed on the fly
+    const double* pold = it == 0 ? nullptr : ((it & 1) ? A.p0 : A.p1);
+    double* pnew = (it & 1) ? A.p1 : A.p0;
+    double ppq = 0.0;
+    for (size_t i = i0; i < n; i += stride) {
+      const double pi = pold ? fma(beta, pold[i], A.z[i]) : A.z[i];
+      const double qi = fine_apply(A, i, A.z, pold, beta, pi);
+      pnew[i] = pi;
+      A.q[i] = qi;
+      ppq = fma(pi, qi, ppq);
+    }
+    const double pq = grid_reduce_rel(warp_sum(ppq), red16, A.partials, A.bar, epoch, &bc[0]);
+    if (!(pq > 0.0)) {
+      ok = false;
+      break;
+    }
+    const double alpha = rz / pq;
+    // phase B: x += alpha p, r -= alpha q, z = D^-1 r, r.z
+    prz = 0.0;
+    for (size_t i = i0; i < n; i += stride) {
+      A.x[i] = fma(alpha, pnew[i], A.x[i]);
+      const double ri = fma(-alpha, A.q[i], A.r[i]);
+      const double zi = ri / A.diag[i];
+      A.r[i] = ri;
+      A.z[i] = zi;
+      prz = fma(ri, zi, prz);
+    }
+    const double rz_new = grid_reduce_rel(warp_sum(prz), red16, A.partials, A.bar, epoch, &bc[0]);
+    beta = rz_new / rz;
+    rz = rz_new;
+    ++it;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.iters[0] = it;
+    A.iters[1] += it;
+    if (!ok) atomicOr(A.flags, FLAG_BREAKDOWN);
+    else if (rz > tol2) atomicOr(A.flags, FLAG_NOCONV);
+    if (!(rz == rz)) atomicOr(A.flags, FLAG_NAN);
+  }
+}
+
+}  // namespace lrbms

@@ -23,7 +23,8 @@ EXPORTS = ["lrbms_create", "lrbms_workspace_bytes", "lrbms_bind", "lrbms_set_med
            "lrbms_set_saturation", "lrbms_set_solver", "lrbms_run", "lrbms_run_host", "lrbms_get_state",
            "lrbms_stage_project", "lrbms_stage_solve", "lrbms_stage_reconstruct", "lrbms_stage_transport",
            "lrbms_get_stats", "lrbms_set_profiling", "lrbms_get_stage_times", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy",
-           "lrbms_profiles_bytes", "lrbms_set_profiles", "lrbms_set_online", "lrbms_stage_theta"]
+           "lrbms_profiles_bytes", "lrbms_set_profiles", "lrbms_set_online", "lrbms_stage_theta",
+           "lrbms_fine_bytes", "lrbms_run_fine"]
 
 
 class LrbmsError(RuntimeError):
@@ -99,6 +100,8 @@ def load_library(path: str = LIB_PATH):
         "lrbms_set_profiles": (st, [P, P, I, P, ctypes.c_size_t]),
         "lrbms_set_online": (st, [P, I]),
         "lrbms_stage_theta": (st, [P, P]),
+        "lrbms_fine_bytes": (ctypes.c_size_t, [P]),
+        "lrbms_run_fine": (st, [P, I, D, D, P, P, ctypes.c_size_t, D, I, ctypes.POINTER(ctypes.c_int64)]),
         "lrbms_get_stage_times": (st, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), I]),
         "lrbms_last_error": (ctypes.c_char_p, [P]),
         "lrbms_version": (ctypes.c_char_p, []),
@@ -251,6 +254,24 @@ class LrbmsContext:
         self._profiles_dev = self.dev(sp.reshape(M, -1))
         self.n_profiles = M
         self._check(self.L.lrbms_set_profiles(self.h, _ptr(self._profiles_dev), M, ctypes.c_void_p(ptr), nbytes))
+
+    def run_fine(self, n_steps, cfl=None, dt_fixed=0.0, log_dt=False, rtol=1e-12, max_iters=100000):
+        """NEXT-2: n_steps of the fine-scale reference scheme (Phi_E = I; lrbms_run_fine) from the
+        current state; allocates the caller-owned fine workspace once (marshalling only).
+        Returns (dt_log or None, CG iterations summed over the steps)."""
+        torch = self.torch
+        cfl = self.sc.cfl if cfl is None else cfl
+        nbytes = self.L.lrbms_fine_bytes(self.h)
+        if getattr(self, "fine_ws", None) is None or self.fine_ws.numel() < nbytes + 256:
+            with torch.cuda.device(self.device):
+                self.fine_ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        ptr = (self.fine_ws.data_ptr() + 255) // 256 * 256
+        dt_log = self.empty(max(n_steps, 1)) if log_dt else None
+        iters = ctypes.c_int64(0)
+        self._check(self.L.lrbms_run_fine(self.h, int(n_steps), float(cfl), float(dt_fixed), _ptr(dt_log),
+                                          ctypes.c_void_p(ptr), nbytes, float(rtol), int(max_iters),
+                                          ctypes.byref(iters)))
+        return (dt_log[:n_steps] if log_dt else None), int(iters.value)
 
     def set_online(self, affine: bool):
         self._check(self.L.lrbms_set_online(self.h, 1 if affine else 0))
