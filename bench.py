@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--rtol", type=float, default=None)
     ap.add_argument("--profile-steps", type=int, default=100,
                     help="steps of the separate profiled pass that gives the per-stage times")
+    ap.add_argument("--fine-steps", type=int, default=5,
+                    help="steps timed in the fine-scale reference scheme (NEXT-2, Phi_E = I; 0 = skip)")
     ap.add_argument("--affine-steps", type=int, default=50,
                     help="steps timed in the paper's affine online variant (NEXT-1; 0 = skip)")
     return ap.parse_args()
@@ -330,6 +332,34 @@ def run_ours(args, rank, local, world):
                           "sum_q theta_q b_q, d_q; NEXT-1), continuing the trajectory above; "
                           "the north-star metric is the direct-projection line"}
 
+    # ---- NEXT-2: the fine-scale reference scheme (the paper's comparison run) on the
+    #      same workload, continuing the trajectory: fine Jacobi-PCG pressure + the same transport
+    fine = None
+    if args.fine_steps > 0:
+        ctx.run_fine(1, rtol=1e-12)   # workspace allocation, neighbour table, warm start
+        barrier(world)
+        torch.cuda.synchronize()
+        e6 = torch.cuda.Event(enable_timing=True)
+        e7 = torch.cuda.Event(enable_timing=True)
+        e6.record(stream)
+        _, fit = ctx.run_fine(args.fine_steps, rtol=1e-12)
+        e7.record(stream)
+        torch.cuda.synchronize()
+        ms_f = max_over_ranks(e6.elapsed_time(e7), world, device)
+        # algorithmic bytes of one CG iteration per cell: phase A reads z, p, 6 neighbour indices,
+        # 3 face weights, d and writes p_new, q (88 B); phase B reads x, p_new, q, r, d and writes
+        # x, r, z (64 B)
+        fbytes = 152.0 * sc.n * fit
+        fine = {"value": world * args.fine_steps / (ms_f / 1e3), "unit": "steps/s",
+                "ms_per_step": ms_f / args.fine_steps, "steps": args.fine_steps,
+                "cg_iters_per_step": fit / args.fine_steps, "rtol": 1e-12,
+                "achieved_gbs": fbytes / (ms_f / 1e3) / 1e9,
+                "lrbms_speedup": value / (world * args.fine_steps / (ms_f / 1e3)),
+                "note": "the fine k = 0 scheme on the GPU (alg:highDimTwoPhaseFlow at Phi_E = I; NEXT-2): "
+                        "Jacobi-preconditioned CG in one cooperative kernel, then the same fluxes and "
+                        "transport; lrbms_speedup = the headline steps/s over these steps/s (the paper's "
+                        "online-vs-fine comparison, P:1300-1302)"}
+
     if rank != 0:
         return 0
 
@@ -390,6 +420,7 @@ def run_ours(args, rank, local, world):
         "stage_us_per_step": stage_us,
         "pcg_iters_per_step": iters,
         "affine_variant": affine,
+        "fine_reference": fine,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
