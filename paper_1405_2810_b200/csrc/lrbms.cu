@@ -778,7 +778,7 @@ struct lrbms_ctx {
   Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
       Binv32, Binv32b, RTb, Es, Yd, cont, e0, partials, scal, gbar, gjrk, gjbar,
       flags,
-      iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp;
+      iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp, tmp2;
   size_t ws_bytes = 0;
   char* ws = nullptr;
   cudaStream_t stream = nullptr;
@@ -807,6 +807,10 @@ struct lrbms_ctx {
   // initial-guess kernels (both only need the scaled operator; the PCG needs both)
   cudaStream_t side = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // lrbms_run_host: the last step's pressure is converted and copied out on a high-priority copy
+  // stream while the fluxes and the transport run
+  cudaStream_t cpy = nullptr;
+  cudaEvent_t p_ev = nullptr, cpy_ev = nullptr;
   std::vector<std::pair<int, int>> ev_pending;  // (stage, index of start event in pool)
   size_t ev_used = 0;
   double stage_ms[LRBMS_N_STAGES] = {0};
@@ -1041,6 +1045,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->K, n * 8); alloc(c->fc, n * 3 * 16); alloc(c->l_gK, 8 * (size_t)nl); alloc(c->phiV, n * 8); alloc(c->s0, n * 8); alloc(c->s1, n * 8); alloc(c->p, n * 8);
   alloc(c->tmp, n * 8);
   alloc(c->netw, n * 8);
+  alloc(c->tmp2, n * 8);
   alloc(c->lam0, n * 8); alloc(c->lam1, n * 8); alloc(c->fw0, n * 8); alloc(c->fw1, n * 8);
   alloc(c->Phi, (size_t)g.n_s * g.N * g.n_loc * 8);
   alloc(c->zc, R * 8);
@@ -1095,6 +1100,9 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->cpy, cudaStreamNonBlocking, prio_hi));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->p_ev, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->cpy_ev, cudaEventDisableTiming));
   }
   // occupancy-limited cooperative grids
   int dev = 0, sms = 148;
@@ -1618,6 +1626,8 @@ lrbms_status lrbms_run_host(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
                             double* s_out, double* p_out) {
   lrbms_status st = ready(c);
   if (st) return st;
+  if (n_steps < 0) return fail(c, LRBMS_E_CONFIG, "n_steps < 0");
+  if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
   const Geo& g = c->g;
   double* tmp = c->at<double>(c->tmp);
   const int nb = cdiv(g.n, 256);
@@ -1628,20 +1638,38 @@ lrbms_status lrbms_run_host(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
     k_mobility<<<nb, 256, 0, c->stream>>>(g, c->f, c->s_cur(), c->lam_cur(), c->fw_cur());
     LAUNCH_CHECK(c);
   }
-  st = lrbms_run(c, n_steps, cfl, dt_fixed, nullptr);
-  if (st) return st;
+  bool p_forked = false;
+  for (int k = 0; k < n_steps; ++k) {
+    if ((st = launch_project(c))) return st;
+    if ((st = launch_solve(c))) return st;
+    if ((st = launch_recon(c))) return st;
+    if (k == n_steps - 1 && p_out && c->cpy) {
+      // the pressure is final after the reconstruction: convert and copy it out on the copy stream
+      // while the fluxes and the transport run
+      CUDA_TRY(c, cudaEventRecord(c->p_ev, c->stream));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->cpy, c->p_ev, 0));
+      double* tmp2 = c->at<double>(c->tmp2);
+      k_to_natural<<<nb, 256, 0, c->cpy>>>(g, c->at<double>(c->p), tmp2);
+      LAUNCH_CHECK(c);
+      CUDA_TRY(c, cudaMemcpyAsync(p_out, tmp2, 8 * (size_t)g.n, cudaMemcpyDeviceToHost, c->cpy));
+      CUDA_TRY(c, cudaEventRecord(c->cpy_ev, c->cpy));
+      p_forked = true;
+    }
+    if ((st = launch_transport(c, cfl, dt_fixed, nullptr, k, nullptr, nullptr))) return st;
+    c->steps++;
+  }
   if (s_out) {
     k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->s_cur(), tmp);
     LAUNCH_CHECK(c);
     CUDA_TRY(c, cudaMemcpyAsync(s_out, tmp, 8 * (size_t)g.n, cudaMemcpyDeviceToHost, c->stream));
   }
-  if (p_out) {
+  if (p_out && !p_forked) {
     k_to_natural<<<nb, 256, 0, c->stream>>>(g, c->at<double>(c->p), tmp);
     LAUNCH_CHECK(c);
     CUDA_TRY(c, cudaMemcpyAsync(p_out, tmp, 8 * (size_t)g.n, cudaMemcpyDeviceToHost, c->stream));
   }
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  return LRBMS_OK;
+  if (p_forked) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->cpy_ev, 0));
+  return finish(c, n_steps);
 }
 
 lrbms_status lrbms_get_state(lrbms_ctx* c, double* s, double* p, double* cc) {
@@ -1933,6 +1961,9 @@ void lrbms_destroy(lrbms_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->join_ev) cudaEventDestroy(c->join_ev);
+  if (c->cpy) cudaStreamDestroy(c->cpy);
+  if (c->p_ev) cudaEventDestroy(c->p_ev);
+  if (c->cpy_ev) cudaEventDestroy(c->cpy_ev);
   delete c;
 }
 
