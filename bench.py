@@ -164,6 +164,28 @@ def stage_bytes(sc, iters_per_step):
     }
 
 
+def stage_flops(sc):
+    """fp64 flops per STEP of the stages with dense contractions: the projection
+    (Y = A_EE Phi_E^T with the (2 dim + 1)-point stencil, B_EE = Phi_E Y, the couplings over the
+    interface faces), the scaling transform (two N^3 products per coupling block) and the
+    reconstruction (p = Phi c)."""
+    n, ns, N, nl, dim = sc.n, sc.n_s, sc.N, sc.n_loc, sc.dim
+    iface_faces = ns * sum(nl // s for s in (sc.sx, sc.sy, sc.sz)[:dim])
+    return {"project": ns * (2.0 * N * N * nl + 2.0 * N * (2 * dim + 1) * nl) + 2.0 * N * N * iface_faces,
+            "scale": 4.0 * N ** 3 * ns * dim + 2.0 * N ** 3 / 3 * ns * 2,
+            "recon": 2.0 * N * n}
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+    if os.path.exists(p):
+        d, _ = json.JSONDecoder().raw_decode(open(p).read())   # the tool's output: a JSON object, then its status line
+        for k in ("dmma_tflops", "DMMA_tflops", "dmma"):
+            if k in d:
+                return float(d[k]), "measured (profiles/r01_fp64_peaks.json, DMMA)"
+    return 37.1, "fallback: the DMMA peak measured in round 1 (tools/fp64_peaks.cu)"
+
+
 # measured cost of one deterministic grid-wide reduction fused with a grid barrier (147 CTAs x 448
 # threads, a neighbour store + load before each; tools/mb_gridreduce.cu, release-reduction arrival)
 GRID_REDUCE_US = 2.84
@@ -378,6 +400,9 @@ def run_ours(args, rank, local, world):
         traffic = json.load(open(tp)).get(args.config, {}).get(dom)
     # whole-step view: every stage's algorithmic bytes once per step
     step_bytes = sum(sb[k] for k in sb if k in stages)
+    sf = stage_flops(sc)
+    p64, p64_src = fp64_peak()
+    t_roof_us = sum(max(sb[k] / (peak * 1e9), sf.get(k, 0.0) / (p64 * 1e12)) for k in sb if k in stages) * 1e6
     step_ms = ms / K
     ms_prof = sum(v[0] for v in stages.values())
     stage_share = {k: round(v[0] / max(ms_prof, 1e-9), 4) for k, v in stages.items()}
@@ -415,7 +440,11 @@ def run_ours(args, rank, local, world):
         "profiled_pass": {"steps": Kp, "pcg_iters_per_step": iters_p,
                           "note": "stage times, roofline and sync_roofline come from this separate pass"},
         "step_roofline": {"algorithmic_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (step_ms / 1e3) / 1e9,
-                          "frac": step_bytes / (step_ms / 1e3) / 1e9 / peak},
+                          "frac": step_bytes / (step_ms / 1e3) / 1e9 / peak,
+                          "t_roof_us": t_roof_us, "frac_time": t_roof_us / (1e3 * step_ms),
+                          "fp64_peak_tflops": p64, "fp64_peak_source": p64_src,
+                          "note": "t_roof = sum over stages of max(algorithmic bytes / HBM peak, fp64 flops / "
+                                  "DMMA peak) (SURVEY 8(d)); frac_time = t_roof / measured step time"},
         "stage_share": stage_share,
         "stage_us_per_step": stage_us,
         "pcg_iters_per_step": iters,
