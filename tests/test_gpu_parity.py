@@ -170,6 +170,24 @@ def test_run_host_matches_device_path():
     assert np.array_equal(s_h, np_(s_d)) and np.array_equal(p_h, np_(p_d))
 
 
+def test_run_host_pinned_overlapped_copies():
+    """e2e path with pinned buffers, as bench.py drives it: the last step's pressure is copied out on
+    the copy stream while the transport runs; s and p must equal the device path bitwise, also with
+    several steps per call and s_in == s_out."""
+    sc = inputs.make_scenario("C2")
+    ctx = ctx_for(sc)
+    s_pin = torch.from_numpy(sc.s0.copy()).pin_memory()
+    p_pin = torch.empty(sc.n, dtype=torch.float64).pin_memory()
+    for _ in range(3):
+        ctx.run_host_ptr(2, s_pin.data_ptr(), s_pin.data_ptr(), p_pin.data_ptr())
+    ctx2 = ctx_for(sc)
+    ctx2.run(6)
+    s_d, p_d, _ = ctx2.get_state()
+    assert np.array_equal(s_pin.numpy(), np_(s_d)) and np.array_equal(p_pin.numpy(), np_(p_d))
+    ctx.close()
+    ctx2.close()
+
+
 def test_determinism_bitwise():
     sc = inputs.make_scenario("C2", n_steps=10)
     outs = []
