@@ -368,10 +368,10 @@ def run_ours(args, rank, local, world):
         e7.record(stream)
         torch.cuda.synchronize()
         ms_f = max_over_ranks(e6.elapsed_time(e7), world, device)
-        # algorithmic bytes of one CG iteration per cell: phase A reads z, p, 6 neighbour indices,
-        # 3 face weights, d and writes p_new, q (88 B); phase B reads x, p_new, q, r, d and writes
-        # x, r, z (64 B)
-        fbytes = 152.0 * sc.n * fit
+        # algorithmic bytes of one CG iteration per cell: phase A reads z, p, the 2-byte neighbour
+        # code, 3 face weights, d and writes p_new, q (66 B); phase B reads x, p_new, q, r, d and
+        # writes x, r, z (64 B)
+        fbytes = 130.0 * sc.n * fit
         fine = {"value": world * args.fine_steps / (ms_f / 1e3), "unit": "steps/s",
                 "ms_per_step": ms_f / args.fine_steps, "steps": args.fine_steps,
                 "cg_iters_per_step": fit / args.fine_steps, "rtol": 1e-12,

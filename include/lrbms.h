@@ -161,7 +161,7 @@ lrbms_status lrbms_stage_theta(lrbms_ctx *ctx, double *theta);
  * current pressure and stopped when r.D^-1 r <= rtol^2 b.D^-1 b; then the same fluxes, CFL step
  * and upwind transport as lrbms_run.  The paper's comparison run (speed-up).
  *
- * lrbms_fine_bytes: size of the caller-owned fine workspace (10 n doubles + 6 n int32 + scratch).
+ * lrbms_fine_bytes: size of the caller-owned fine workspace (10 n doubles + 2 n bytes + scratch).
  * lrbms_run_fine: n_steps, cfl, dt_fixed, dt_log as lrbms_run; ws (dev, 256-byte aligned, >= the
  * size above, owned by the caller, used only during the call); rtol > 0, max_iters > 0 per solve;
  * iters_total (host, NULL = skip) receives the CG iterations summed over the steps.  Needs

@@ -1783,7 +1783,7 @@ static void fine_layout(const lrbms_ctx* c, size_t* offs, size_t* total) {
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
   for (int k = 0; k < 10; ++k) offs[k] = take(n * 8);   // r z p0 p1 q diag rhs w[3]
-  offs[10] = take(6 * n * 4);                             // nbr
+  offs[10] = take(n * 2);                                 // neighbour codes
   offs[11] = take(8 * 4 * 4096);                          // partials (G <= 4096)
   offs[12] = take(256);                                   // barrier counter, iteration counters
   *total = off;
@@ -1817,7 +1817,13 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
   double* v[10];
   for (int k = 0; k < 10; ++k) v[k] = reinterpret_cast<double*>(b + offs[k]);
   F.r = v[0]; F.z = v[1]; F.p0 = v[2]; F.p1 = v[3]; F.q = v[4]; F.diag = v[5]; F.rhs = v[6]; F.w = v[7];
-  F.nbr = reinterpret_cast<int*>(b + offs[10]);
+  F.nbr = reinterpret_cast<unsigned short*>(b + offs[10]);
+  for (int a = 0; a < 3; ++a)
+    for (int t = 0; t < 2; ++t) {
+      const int dir = t ? 1 : -1, d = 2 * a + t;
+      F.ioff[d] = a < g.dim ? dir * g.lstride[a] : 0;
+      F.xoff[d] = a < g.dim ? dir * (g.Estride[a] * g.n_loc - (g.s[a] - 1) * g.lstride[a]) : 0;
+    }
   F.partials = reinterpret_cast<double*>(b + offs[11]);
   F.bar = reinterpret_cast<unsigned*>(b + offs[12]);
   F.iters = reinterpret_cast<int*>(b + offs[12] + 128);

@@ -35,7 +35,10 @@ struct FineArgs {
   double* diag;        // [n]
   double* rhs;         // [n]
   double* w;           // [3][n] + face weight of cell i along axis a (0 without a + neighbour)
-  int* nbr;            // [6][n] neighbour of cell i on side d = 2 a + (dir > 0), -1 outside
+  unsigned short* nbr; // [n] neighbour code of cell i: bit d (side d = 2 a + (dir > 0)) = the neighbour
+                       // exists, bit 6 + d = it lies in the adjacent subdomain; its index is then
+                       // i + xoff[d], else i + ioff[d]
+  int ioff[6], xoff[6];
   double* partials;    // [4][gridDim]
   unsigned* bar;       // grid-barrier counter (zeroed before the launch)
   int* iters;          // [0]: iterations of the last solve, [1]: running total
@@ -63,11 +66,15 @@ __global__ void __launch_bounds__(512) k_fine_setup(FineArgs A) {
     const size_t gl = base + l;
     const double ll = A.lam[gl];
     double d = 0.0;
+    unsigned code = 0;
     for (int a = 0; a < 3; ++a)
       for (int t = 0; t < 2; ++t) {
         const int dir = t ? 1 : -1;
         const int nb = a < g.dim ? neighbour(g, E, C, l, c, a, dir) : -1;
-        if (A.build_nbr) A.nbr[(size_t)(2 * a + t) * n + gl] = nb;
+        if (nb >= 0) {
+          code |= 1u << (2 * a + t);
+          if (c[a] + dir < 0 || c[a] + dir >= g.s[a]) code |= 1u << (6 + 2 * a + t);
+        }
         if (nb < 0) {
           if (t) A.w[(size_t)a * n + gl] = 0.0;
           continue;
@@ -77,6 +84,7 @@ __global__ void __launch_bounds__(512) k_fine_setup(FineArgs A) {
         if (t) A.w[(size_t)a * n + gl] = wf;
         d += wf;
       }
+    if (A.build_nbr) A.nbr[gl] = (unsigned short)code;
     dg[l] = d;
     bl[l] = 0.0;
   }
@@ -102,10 +110,11 @@ __device__ __forceinline__ double fine_apply(const FineArgs& A, size_t i, const 
                                              double beta, double vi) {
   const size_t n = A.g.n;
   double acc = A.diag[i] * vi;
+  const unsigned code = A.nbr[i];
 #pragma unroll
   for (int d = 0; d < 6; ++d) {
-    const int j = A.nbr[(size_t)d * n + i];
-    if (j < 0) continue;
+    if (!((code >> d) & 1u)) continue;
+    const size_t j = i + (((code >> (6 + d)) & 1u) ? A.xoff[d] : A.ioff[d]);
     const double wf = (d & 1) ? A.w[(size_t)(d >> 1) * n + i] : A.w[(size_t)(d >> 1) * n + j];
     const double vj = vp ? fma(beta, vp[j], vz[j]) : vz[j];
     acc = fma(-wf, vj, acc);
