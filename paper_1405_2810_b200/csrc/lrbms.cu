@@ -296,6 +296,57 @@ __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restric
   }
 }
 
+// The same RT with the CTA's RT_SROWS rows of X staged in shared memory by cp.async first (every
+// row is read from DRAM once at full bandwidth instead of by 7 dependent gathers per element).
+constexpr int RT_SROWS = 8;
+__global__ void __launch_bounds__(256) k_coarse_rt_s(Geo g, const float* __restrict__ X, const double* __restrict__ Es,
+                                                     float* __restrict__ RT, int n) {
+  extern __shared__ __align__(16) float xs[];   // [RT_SROWS][n]
+  const int i0 = blockIdx.x * RT_SROWS;
+  {
+    const float4* src = reinterpret_cast<const float4*>(X + (size_t)i0 * n);
+    const int n4 = RT_SROWS * n / 4;   // n is a multiple of 32
+    for (int k = threadIdx.x; k < n4; k += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(xs + 4 * k)),
+                   "l"(src + k)
+                   : "memory");
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    float e[7];
+    int nb[7];
+    nb[0] = j;
+    if (j < g.n_s) {
+      int C[3];
+      sub_xyz(g, j, C);
+      e[0] = (float)Es[(size_t)j * 8];
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        const bool ex = side_exists(g, C, s);
+        e[1 + s] = ex ? (float)Es[(size_t)j * 8 + 1 + s] : 0.f;
+        nb[1 + s] = ex ? side_nb(g, j, s) : j;
+      }
+    } else {
+      e[0] = 1.f;
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        e[1 + s] = 0.f;
+        nb[1 + s] = j;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RT_SROWS; ++r) {
+      const float* xr = xs + (size_t)r * n;
+      float v = xr[nb[0]] * e[0];
+#pragma unroll
+      for (int s = 1; s < 7; ++s) v = fmaf(xr[nb[s]], e[s], v);
+      const int i = i0 + r;
+      RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+    }
+  }
+}
+
 // R = I - E X for the Newton-Schulz update of the coarse inverse (X is not exactly symmetric:
 // using (I - X E)^T instead would double X's antisymmetric part every step):
 // R[k][j] = delta_kj - sum_{G in {k} + nb(k)} E_{kG} X[G][j]; rows k >= n_s are the identity padding
@@ -1168,6 +1219,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   }
   CUDA_TRY(c, cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_coarse_rt_s, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   {  // TMA descriptors (128 x 32 fp32 boxes, 128-byte swizzle) for the tensor-core Newton-Schulz GEMM
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -1413,8 +1465,12 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
     float* X = coarse_x(c, c->xcur);
     float* Xn = coarse_x(c, 1 - c->xcur);
     if (c->have_tmaps) {   // tcgen05 (TF32, TMEM accumulators), upper-triangular tiles, symmetric output
-      k_coarse_rt<<<dim3(cdiv(n, 256), cdiv(n, RT_ROWS)), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es),
-                                                                              c->at<float>(c->RTb), n);
+      if ((size_t)RT_SROWS * n * 4 <= 96 * 1024)
+        k_coarse_rt_s<<<n / RT_SROWS, 256, (size_t)RT_SROWS * n * 4, c->stream>>>(g, X, c->at<double>(c->Es),
+                                                                                  c->at<float>(c->RTb), n);
+      else
+        k_coarse_rt<<<dim3(cdiv(n, 256), cdiv(n, RT_ROWS)), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es),
+                                                                                c->at<float>(c->RTb), n);
       LAUNCH_CHECK(c);
       const int nbt = cdiv(n, NS_TM);
       k_ns_gemm_tc<<<nbt * (nbt + 1) / 2, 128, NS_TC_SMEM, c->stream>>>(c->tmX[c->xcur], c->tmRT, X, Xn, n);
