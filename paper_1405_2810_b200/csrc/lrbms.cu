@@ -296,9 +296,12 @@ __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restric
   }
 }
 
-// The same RT with the CTA's RT_SROWS rows of X staged in shared memory by cp.async first (every
+// The same RT with the CTA's RT_SROWS (16) rows of X staged in shared memory by cp.async first (every
 // row is read from DRAM once at full bandwidth instead of by 7 dependent gathers per element).
-constexpr int RT_SROWS = 8;
+#ifndef RT_SROWS_V
+#define RT_SROWS_V 16
+#endif
+constexpr int RT_SROWS = RT_SROWS_V;
 __global__ void __launch_bounds__(256) k_coarse_rt_s(Geo g, const float* __restrict__ X, const double* __restrict__ Es,
                                                      float* __restrict__ RT, int n) {
   extern __shared__ __align__(16) float xs[];   // [RT_SROWS][n]
@@ -1219,7 +1222,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   }
   CUDA_TRY(c, cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
-  CUDA_TRY(c, cudaFuncSetAttribute(k_coarse_rt_s, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_coarse_rt_s, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   {  // TMA descriptors (128 x 32 fp32 boxes, 128-byte swizzle) for the tensor-core Newton-Schulz GEMM
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -1465,7 +1468,7 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
     float* X = coarse_x(c, c->xcur);
     float* Xn = coarse_x(c, 1 - c->xcur);
     if (c->have_tmaps) {   // tcgen05 (TF32, TMEM accumulators), upper-triangular tiles, symmetric output
-      if ((size_t)RT_SROWS * n * 4 <= 96 * 1024)
+      if ((size_t)RT_SROWS * n * 4 <= 200 * 1024)
         k_coarse_rt_s<<<n / RT_SROWS, 256, (size_t)RT_SROWS * n * 4, c->stream>>>(g, X, c->at<double>(c->Es),
                                                                                   c->at<float>(c->RTb), n);
       else
