@@ -157,11 +157,14 @@ lrbms_status lrbms_stage_theta(lrbms_ctx *ctx, double *theta);
  * at k = 0, i.e. the online step with Phi_E = I: per step the fine pressure
  * system of def:pressureDG, A(lambda) p = b(lambda) with A = sum_F w_F (e_a - e_b)
  * (e_a - e_b)^T + sum_L g_L e_a e_a^T and b = sum_L g_L p_L e_a (reading R2 weights), solved by a
- * Jacobi-preconditioned CG (cooperative kernel, deterministic reductions) warm-started from the
- * current pressure and stopped when r.D^-1 r <= rtol^2 b.D^-1 b; then the same fluxes, CFL step
+ * CG (cooperative kernel, deterministic reductions) preconditioned by Jacobi plus an additive coarse
+ * correction on the subdomain indicators (E = Z^T A Z inverted each step by the reduced solver's
+ * Gauss-Jordan kernel, when that kernel fits the configuration), warm-started from the current
+ * pressure and stopped when r.M^-1 r <= rtol^2 b.D^-1 b; then the same fluxes, CFL step
  * and upwind transport as lrbms_run.  The paper's comparison run (speed-up).
  *
- * lrbms_fine_bytes: size of the caller-owned fine workspace (10 n doubles + 2 n bytes + scratch).
+ * lrbms_fine_bytes: size of the caller-owned fine workspace (10 n doubles + 2 n bytes + the coarse
+ * stencil and its fp32 inverse, n_pad^2 floats + scratch).
  * lrbms_run_fine: n_steps, cfl, dt_fixed, dt_log as lrbms_run; ws (dev, 256-byte aligned, >= the
  * size above, owned by the caller, used only during the call); rtol > 0, max_iters > 0 per solve;
  * iters_total (host, NULL = skip) receives the CG iterations summed over the steps.  Needs

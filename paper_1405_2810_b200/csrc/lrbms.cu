@@ -1845,12 +1845,15 @@ static void fine_layout(const lrbms_ctx* c, size_t* offs, size_t* total) {
   offs[10] = take(n * 2);                                 // neighbour codes
   offs[11] = take(8 * 4 * 4096);                          // partials (G <= 4096)
   offs[12] = take(256);                                   // barrier counter, iteration counters
+  offs[13] = take(8 * 8 * (size_t)c->g.n_s);              // coarse stencil Z^T A Z
+  offs[14] = take(4 * (size_t)c->n_pad * c->n_pad);       // its inverse (fp32)
+  offs[15] = take(8 * (size_t)c->n_pad);                  // Z^T r
   *total = off;
 }
 
 size_t lrbms_fine_bytes(const lrbms_ctx* c) {
   if (!c) return 0;
-  size_t offs[13], total;
+  size_t offs[16], total;
   fine_layout(c, offs, &total);
   return total;
 }
@@ -1863,7 +1866,7 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
   if (n_steps < 0) return fail(c, LRBMS_E_CONFIG, "n_steps < 0");
   if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
   if (!(rtol > 0) || max_iters <= 0) return fail(c, LRBMS_E_CONFIG, "fine solve needs rtol > 0 and max_iters > 0");
-  size_t offs[13], total;
+  size_t offs[16], total;
   fine_layout(c, offs, &total);
   if (!ws || bytes < total || (reinterpret_cast<uintptr_t>(ws) & 255))
     return fail(c, LRBMS_E_CONFIG, "fine workspace missing, smaller than lrbms_fine_bytes or not 256-byte aligned");
@@ -1888,6 +1891,15 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
   F.iters = reinterpret_cast<int*>(b + offs[12] + 128);
   F.flags = c->at<int>(c->flags);
   F.rtol = rtol; F.max_iters = max_iters;
+#ifndef FINE_COARSE
+#define FINE_COARSE 1
+#endif
+  // two-level preconditioner when the row-resident fp32 Gauss-Jordan inverse is available
+  F.coarse = FINE_COARSE && c->gj32_G > 0 && g.n_s > 1;
+  double* es_f = reinterpret_cast<double*>(b + offs[13]);
+  F.Xc = reinterpret_cast<const float*>(b + offs[14]);
+  F.wc = reinterpret_cast<double*>(b + offs[15]);
+  F.n_pad = c->n_pad;
   F.dt_bits = (unsigned long long*)c->at<double>(c->scal);
   int per_sm = 0;
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fine_pcg, 256, 0));
@@ -1901,6 +1913,22 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
     F.build_nbr = k == 0;
     k_fine_setup<<<g.n_s, nt, 16 * (size_t)g.n_loc, c->stream>>>(F);
     LAUNCH_CHECK(c);
+    if (F.coarse) {   // E = Z^T A Z and its inverse (the reduced solver's Gauss-Jordan kernel)
+      k_fine_coarse_stencil<<<g.n_s, 256, 0, c->stream>>>(F, es_f);
+      LAUNCH_CHECK(c);
+      Geo gg = g;
+      const double* es = es_f;
+      float* out = const_cast<float*>(F.Xc);
+      float* rk = c->at<float>(c->gjrk);
+      unsigned* gbar = c->at<unsigned>(c->gjbar);
+      int* bad = reinterpret_cast<int*>(gbar + 16);
+      int np = c->n_pad;
+      CUDA_TRY(c, cudaMemsetAsync(gbar, 0, 256, c->stream));
+      void* gargs[] = {&gg, &es, &out, &rk, &np, &gbar, &bad};
+      CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), gargs,
+                                              c->gj32_smem, c->stream));
+      c->launches++;
+    }
     CUDA_TRY(c, cudaMemsetAsync(F.bar, 0, 4, c->stream));
     void* args[] = {&F};
     CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_fine_pcg, dim3(G), dim3(256), args, 0, c->stream));

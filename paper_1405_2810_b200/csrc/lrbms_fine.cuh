@@ -46,6 +46,11 @@ struct FineArgs {
   double rtol;
   int max_iters;
   int build_nbr;       // 1: k_fine_setup fills nbr (first call of a run)
+  // two-level preconditioner M^-1 = D^-1 + Z E^-1 Z^T (Z = subdomain indicators, E = Z^T A Z)
+  int coarse;          // 0: Jacobi only
+  const float* Xc;     // [n_pad][n_pad] E^-1 (fp32: it only steers the iteration)
+  double* wc;          // [n_s] Z^T r
+  int n_pad;
   unsigned long long* dt_bits;   // the step's dt minimum (reset here, as k_recon does for the reduced step)
 };
 
@@ -104,6 +109,90 @@ __global__ void __launch_bounds__(512) k_fine_setup(FineArgs A) {
   }
 }
 
+// E = Z^T A Z on the subdomain indicators, as the 7-point stencil Es[E][0..7] of the reduced
+// solver's coarse level (0: diagonal, 1 + a: coupling to E + e_a, 4 + a: coupling to E - e_a):
+// E_EE = sum over the cells of E of (d_i - the weights of their faces inside E), E_EE' = - the sum
+// of the weights of the faces between E and E'.  CTA per subdomain, fixed-order block sums.
+__global__ void __launch_bounds__(256) k_fine_coarse_stencil(FineArgs A, double* __restrict__ Es) {
+  __shared__ double red[8][7];
+  const Geo& g = A.g;
+  const int E = blockIdx.x, nl = g.n_loc;
+  const size_t n = g.n;
+  double v[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) v[k] = 0.0;
+  for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+    const size_t i = (size_t)E * nl + l;
+    const unsigned code = A.nbr[i];
+    double dsum = A.diag[i];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+      if (!((code >> d) & 1u)) continue;
+      const int a = d >> 1;
+      const bool cross = (code >> (6 + d)) & 1u;
+      const size_t j = i + (cross ? A.xoff[d] : A.ioff[d]);
+      const double wf = (d & 1) ? A.w[(size_t)a * n + i] : A.w[(size_t)a * n + j];
+      if (cross) v[1 + ((d & 1) ? a : 3 + a)] -= wf;
+      else dsum -= wf;
+    }
+    v[0] += dsum;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const double t = warp_sum(v[k]);
+    if (lane == 0) red[warp][k] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double t = 0.0;
+    if (threadIdx.x < 7)
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w][threadIdx.x];
+    Es[(size_t)E * 8 + threadIdx.x] = t;
+  }
+}
+
+// fixed-order block sum (every thread gets the same value)
+__device__ __forceinline__ double fine_block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+  __syncthreads();
+  return t;
+}
+
+// two-level part, CTA per subdomain: wc[E] = sum of r over E (r already updated), then after a grid
+// barrier z = D^-1 r + e_E with e = E^-1 wc; returns this thread's part of r.z
+__device__ __forceinline__ double fine_coarse_z(const FineArgs& A, double* sh, unsigned& epoch) {
+  const Geo& g = A.g;
+  const int nl = g.n_loc;
+  for (int E = blockIdx.x; E < g.n_s; E += gridDim.x) {
+    double ws = 0.0;
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) ws += A.r[(size_t)E * nl + l];
+    ws = fine_block_sum(ws, sh);
+    if (threadIdx.x == 0) A.wc[E] = ws;
+  }
+  grid_barrier_rel(A.bar, epoch);
+  double prz = 0.0;
+  for (int E = blockIdx.x; E < g.n_s; E += gridDim.x) {
+    double ep = 0.0;
+    const float* row = A.Xc + (size_t)E * A.n_pad;
+    for (int F = threadIdx.x; F < g.n_s; F += blockDim.x) ep = fma((double)row[F], __ldcg(A.wc + F), ep);
+    const double e = fine_block_sum(ep, sh);
+    for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+      const size_t i = (size_t)E * nl + l;
+      const double ri = A.r[i];
+      const double zi = ri / A.diag[i] + e;
+      A.z[i] = zi;
+      prz = fma(ri, zi, prz);
+    }
+  }
+  return prz;
+}
+
 // (A v)_i = d_i v_i - sum over the faces of i of w_F v_nb, with v_j = vz[j] + beta * vp[j] for
 // every j (beta = 0, vp = nullptr: v = vz)
 __device__ __forceinline__ double fine_apply(const FineArgs& A, size_t i, const double* vz, const double* vp,
@@ -139,6 +228,11 @@ __global__ void __launch_bounds__(256) k_fine_pcg(FineArgs A) {
     prz = fma(ri, zi, prz);
     pbb = fma(A.rhs[i], A.rhs[i] / A.diag[i], pbb);
   }
+  __shared__ double shb[8];
+  if (A.coarse) {   // r was written grid-stride: a barrier before the per-subdomain sums
+    grid_barrier_rel(A.bar, epoch);
+    prz = fine_coarse_z(A, shb, epoch);
+  }
   double rz = grid_reduce_rel(warp_sum(prz), red16, A.partials, A.bar, epoch, &bc[0]);
   const double bb = grid_reduce_rel(warp_sum(pbb), red16, A.partials, A.bar, epoch, &bc[0]);
   const double tol2 = A.rtol * A.rtol * bb;
@@ -166,13 +260,25 @@ __global__ void __launch_bounds__(256) k_fine_pcg(FineArgs A) {
     const double alpha = rz / pq;
     // phase B: x += alpha p, r -= alpha q, z = D^-1 r, r.z
     prz = 0.0;
-    for (size_t i = i0; i < n; i += stride) {
-      A.x[i] = fma(alpha, pnew[i], A.x[i]);
-      const double ri = fma(-alpha, A.q[i], A.r[i]);
-      const double zi = ri / A.diag[i];
-      A.r[i] = ri;
-      A.z[i] = zi;
-      prz = fma(ri, zi, prz);
+    if (A.coarse) {   // x, r updated per subdomain, then the coarse correction (one more barrier)
+      const int nl = A.g.n_loc;
+      for (int E = blockIdx.x; E < A.g.n_s; E += gridDim.x)
+        for (int l = threadIdx.x; l < nl; l += blockDim.x) {
+          const size_t i = (size_t)E * nl + l;
+          A.x[i] = fma(alpha, pnew[i], A.x[i]);
+          A.r[i] = fma(-alpha, A.q[i], A.r[i]);
+        }
+      __syncthreads();
+      prz = fine_coarse_z(A, shb, epoch);
+    } else {
+      for (size_t i = i0; i < n; i += stride) {
+        A.x[i] = fma(alpha, pnew[i], A.x[i]);
+        const double ri = fma(-alpha, A.q[i], A.r[i]);
+        const double zi = ri / A.diag[i];
+        A.r[i] = ri;
+        A.z[i] = zi;
+        prz = fma(ri, zi, prz);
+      }
     }
     const double rz_new = grid_reduce_rel(warp_sum(prz), red16, A.partials, A.bar, epoch, &bc[0]);
     beta = rz_new / rz;
