@@ -12,10 +12,13 @@
 //     the + face weights w[a][i] = T_F (tau_a lambda_i + tau_b lambda_nb), the diagonal
 //     d_i = sum of the weights of the faces of i + sum of its link weights, and b (links in the
 //     subdomain's link order, by one thread: deterministic).
-//   k_fine_pcg (cooperative, grid-stride over cells): Jacobi-preconditioned CG, warm-started from
-//     the previous pressure, two grid reductions per iteration (p.Ap; r.z), the search direction
-//     p_new = z + beta p formed on the fly for the neighbours inside the SpMV (double-buffered p);
-//     stop when r.z <= rtol^2 b.D^-1 b.  Deterministic (fixed-order per-CTA partials).
+//   k_fine_coarse_stencil (CTA per subdomain): E = Z^T A Z on the subdomain indicators, inverted
+//     each step by the reduced solver's Gauss-Jordan kernel (k_coarse_gj32, fp32).
+//   k_fine_pcg (cooperative, grid-stride over cells): CG warm-started from the previous pressure,
+//     preconditioned by M^-1 = D^-1 + Z E^-1 Z^T (Jacobi only when no coarse inverse is available);
+//     the search direction p_new = z + beta p formed on the fly for the neighbours inside the SpMV
+//     (double-buffered p); grid synchronisations per iteration: p.Ap, the coarse barrier (two-level
+//     only), r.z; stop when r.M^-1 r <= rtol^2 b.D^-1 b.  Deterministic (fixed-order partials).
 #pragma once
 #include "lrbms_kernels.cuh"
 
