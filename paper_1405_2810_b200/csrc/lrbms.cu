@@ -1845,8 +1845,8 @@ static void fine_layout(const lrbms_ctx* c, size_t* offs, size_t* total) {
   offs[10] = take(n * 2);                                 // neighbour codes
   offs[11] = take(8 * 4 * 4096);                          // partials (G <= 4096)
   offs[12] = take(256);                                   // barrier counter, iteration counters
-  offs[13] = take(8 * 8 * (size_t)c->g.n_s);              // coarse stencil Z^T A Z
-  offs[14] = take(4 * (size_t)c->n_pad * c->n_pad);       // its inverse (fp32)
+  offs[13] = offs[14] = 0;                                // (the coarse stencil and inverse use the
+                                                          //  context's coarse-level buffers)
   offs[15] = take(8 * (size_t)c->n_pad);                  // Z^T r
   *total = off;
 }
@@ -1894,10 +1894,12 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
 #ifndef FINE_COARSE
 #define FINE_COARSE 1
 #endif
-  // two-level preconditioner when the row-resident fp32 Gauss-Jordan inverse is available
-  F.coarse = FINE_COARSE && c->gj32_G > 0 && g.n_s > 1;
-  double* es_f = reinterpret_cast<double*>(b + offs[13]);
-  F.Xc = reinterpret_cast<const float*>(b + offs[14]);
+  // two-level preconditioner: E = Z^T A Z goes through the context's coarse level (stencil buffer,
+  // a full inverse on the first step of the call, then one Newton-Schulz update per step); the
+  // reduced solver's coarse inverse is rebuilt at its next step
+  F.coarse = FINE_COARSE && g.n_s > 1 && c->opts.use_coarse == 2;
+  if (F.coarse) c->have_x = false;
+  F.Xc = nullptr;
   F.wc = reinterpret_cast<double*>(b + offs[15]);
   F.n_pad = c->n_pad;
   F.dt_bits = (unsigned long long*)c->at<double>(c->scal);
@@ -1913,21 +1915,11 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
     F.build_nbr = k == 0;
     k_fine_setup<<<g.n_s, nt, 16 * (size_t)g.n_loc, c->stream>>>(F);
     LAUNCH_CHECK(c);
-    if (F.coarse) {   // E = Z^T A Z and its inverse (the reduced solver's Gauss-Jordan kernel)
-      k_fine_coarse_stencil<<<g.n_s, 256, 0, c->stream>>>(F, es_f);
+    if (F.coarse) {   // E = Z^T A Z, then its inverse kept current by the coarse level
+      k_fine_coarse_stencil<<<g.n_s, 256, 0, c->stream>>>(F, c->at<double>(c->Es));
       LAUNCH_CHECK(c);
-      Geo gg = g;
-      const double* es = es_f;
-      float* out = const_cast<float*>(F.Xc);
-      float* rk = c->at<float>(c->gjrk);
-      unsigned* gbar = c->at<unsigned>(c->gjbar);
-      int* bad = reinterpret_cast<int*>(gbar + 16);
-      int np = c->n_pad;
-      CUDA_TRY(c, cudaMemsetAsync(gbar, 0, 256, c->stream));
-      void* gargs[] = {&gg, &es, &out, &rk, &np, &gbar, &bad};
-      CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), gargs,
-                                              c->gj32_smem, c->stream));
-      c->launches++;
+      if ((st = launch_coarse(c))) return st;
+      F.Xc = coarse_x(c, c->xcur);
     }
     CUDA_TRY(c, cudaMemsetAsync(F.bar, 0, 4, c->stream));
     void* args[] = {&F};
@@ -1936,6 +1928,7 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
     c->p_valid = true;
     if ((st = launch_transport(c, cfl, dt_fixed, dt_log, k, nullptr, nullptr))) return st;
   }
+  if (F.coarse) c->have_x = false;   // the coarse buffers hold the fine E^-1 now
   int it[2] = {0, 0};
   CUDA_TRY(c, cudaMemcpyAsync(it, F.iters, 8, cudaMemcpyDeviceToHost, c->stream));
   st = finish(c, n_steps);

@@ -152,3 +152,21 @@ def test_fine_errors():
     with pytest.raises(LrbmsError):
         ctx.run_fine(1, rtol=1e-14, max_iters=2)   # cannot converge in 2 iterations: NUMERICAL
     ctx.close()
+
+
+def test_reduced_steps_after_fine_steps():
+    """The fine run borrows the context's coarse level (E = Z^T A Z and its inverse): reduced steps
+    that follow on the same context must still match the oracle (the coarse inverse is rebuilt)."""
+    sc = inputs.make_scenario("C2")
+    fp = O.fprime_max(sc)
+    s = sc.s0.copy()
+    for _ in range(3):
+        s = O.fine_step(sc, s, fpmax=fp)["s"]
+    for _ in range(4):
+        s = O.lrbms_step(sc, s, fpmax=fp)["s"]
+    ctx = ctx_for(sc)
+    ctx.run_fine(3, rtol=1e-14)
+    ctx.run(4)
+    sg, _, _ = ctx.get_state()
+    assert np.max(np.abs(np_(sg) - s)) <= 1e-10
+    ctx.close()
