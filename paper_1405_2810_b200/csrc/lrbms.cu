@@ -1510,9 +1510,14 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
                                                          c->at<double>(c->zc), c->at<double>(c->zh),
                                                          c->at<int>(c->flags), es, H);
     LAUNCH_CHECK(c);
-    k_transform_h<<<cdiv(g.n_s * g.dim, 4), 256, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
-                                                                c->at<double>(c->zh),
-                                                                mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
+    if (g.N == 32)
+      k_transform_h<32><<<cdiv(g.n_s * g.dim, 4), 256, 0, c->stream>>>(
+          g, c->at<double>(c->blocks), c->at<double>(c->Linv), c->at<double>(c->zh),
+          mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
+    else
+      k_transform_h<0><<<cdiv(g.n_s * g.dim, 4), 256, 0, c->stream>>>(
+          g, c->at<double>(c->blocks), c->at<double>(c->Linv), c->at<double>(c->zh),
+          mode == 2 ? c->at<double>(c->Yd) : nullptr, es);
     LAUNCH_CHECK(c);
   }
   // The coarse update (Newton-Schulz: non-cooperative kernels) goes to the side stream, forked

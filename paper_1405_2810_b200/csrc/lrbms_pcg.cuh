@@ -266,6 +266,7 @@ __device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double 
 #ifndef TRANSFORM_MINB
 #define TRANSFORM_MINB 2
 #endif
+template <int NFIX>   // NFIX = 32: N known at compile time (no bounds predicates, constant strides)
 __global__ void __launch_bounds__(256, TRANSFORM_MINB) k_transform_h(Geo g, double* __restrict__ blocks,
                                                     const double* __restrict__ Linv,
                                                     const double* __restrict__ zh, double* __restrict__ Yd,
@@ -285,14 +286,16 @@ __global__ void __launch_bounds__(256, TRANSFORM_MINB) k_transform_h(Geo g, doub
     live = C[a] + 1 < g.S[a];
     En = live ? E + g.Estride[a] : E;
   }
-  const int N = g.N, NN = N * N;
+  const int N = NFIX ? NFIX : g.N, NN = N * N;
   const int fr = lane >> 2, q = lane & 3;
   double bh[2][4][2];
   if (live) {
     double* U = blocks + ((size_t)E * (1 + g.dim) + 1 + a) * NN;
     const double* XE = Linv + (size_t)E * NN;
     const double* XN = Linv + (size_t)En * NN;
-    auto ld = [&](const double* M, int r, int c) -> double { return (r < N && c < N) ? M[r * N + c] : 0.0; };
+    auto ld = [&](const double* M, int r, int c) -> double {
+      return NFIX ? M[r * N + c] : ((r < N && c < N) ? M[r * N + c] : 0.0);
+    };
     double t1[2][4][2];
 #pragma unroll
     for (int ti = 0; ti < 2; ++ti)
