@@ -1506,9 +1506,14 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   {
     StageScope sc_(c, 2);   // block Cholesky + scaling of the couplings: Bh = L^-1 B L^-T (+ coarse stencil)
     double* es = coarse ? c->at<double>(c->Es) : nullptr;
-    k_block_chol<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
-                                                         c->at<double>(c->zc), c->at<double>(c->zh),
-                                                         c->at<int>(c->flags), es, H);
+    if (g.N == 32)
+      k_block_chol<32><<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
+                                                               c->at<double>(c->zc), c->at<double>(c->zh),
+                                                               c->at<int>(c->flags), es, H);
+    else
+      k_block_chol<0><<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(g, c->at<double>(c->blocks), c->at<double>(c->Linv),
+                                                              c->at<double>(c->zc), c->at<double>(c->zh),
+                                                              c->at<int>(c->flags), es, H);
     LAUNCH_CHECK(c);
     if (g.N == 32)
       k_transform_h<32><<<cdiv(g.n_s * g.dim, 4), 256, 0, c->stream>>>(
@@ -1554,7 +1559,8 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     StageScope sh_(c, 3);
     const int nb = cdiv(g.n_s, 8);
     if (H.nh > 0) {
-      k_hist_spmv_t<<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
+      if (g.N == 32) k_hist_spmv_t<32><<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
+      else k_hist_spmv_t<0><<<cdiv(g.n_s, 4), 128, 0, c->stream>>>(H);
       LAUNCH_CHECK(c);
       k_hist_gram<<<nb, 256, 0, c->stream>>>(H);
       LAUNCH_CHECK(c);

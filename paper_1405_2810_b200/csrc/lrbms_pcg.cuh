@@ -143,6 +143,7 @@ struct HistArgs {
 #ifndef CHOL_MINB
 #define CHOL_MINB 4
 #endif
+template <int NFIX>   // NFIX = 32: N known at compile time
 __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __restrict__ blocks, double* __restrict__ Linv,
                                                       const double* __restrict__ zc, double* __restrict__ zh,
                                                       int* flags, double* __restrict__ Es, const HistArgs H) {
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __
   if (H.gbar_reset && blockIdx.x == 0 && threadIdx.x == 0) *H.gbar_reset = 0u;
   const int E = blockIdx.x * (blockDim.x >> 5) + w;
   if (E >= g.n_s) return;
-  const int N = g.N;
+  const int N = NFIX ? NFIX : g.N;
   double* Bd = blocks + (size_t)E * (1 + g.dim) * N * N;
   double m[32];
 #pragma unroll

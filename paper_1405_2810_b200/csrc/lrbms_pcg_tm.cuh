@@ -173,9 +173,10 @@ __device__ __forceinline__ void grid_barrier_rel(unsigned* bar, unsigned& epoch)
 // subdomain.  Each coupling block is read once into the 4 x 8 register tiling of the PCG SpMV and
 // applied to all nh vectors; the vector operands come through L1 (read-only) instead of 2 x 32
 // shuffles per block column, so the kernel is FMA-bound instead of shuffle-bound.
+template <int NFIX>   // NFIX = 32: N known at compile time
 __global__ void __launch_bounds__(128) k_hist_spmv_t(HistArgs A) {
   const Geo& g = A.g;
-  const int N = g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int N = NFIX ? NFIX : g.N, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int E = blockIdx.x * 4 + warp;
   if (E >= g.n_s) return;
   const bool act = lane < N;
