@@ -819,6 +819,7 @@ struct lrbms_ctx {
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
   int sms = 148;   // SM count of the device (wave size of the one-CTA-per-SM kernels)
   int tm_W = 0, tm_G = 0;   // on-chip PCG (k_pcg_tm) launch; tm_W = 0: not usable
+  const void* tm_fn = nullptr;   // the k_pcg_tm instance (compile-time N = 32, or the general one)
   size_t tm_smem = 0;
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
   int xcur = 0;            // which of Binv32 / Binv32b holds the current coarse inverse
@@ -1193,9 +1194,10 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
       if (Ls.total <= 227 * 1024 - 1024) {
         // at least 116 KB so that no two CTAs share an SM (each allocates all 512 TMEM columns)
         const size_t smem = std::max<size_t>(Ls.total, 116 * 1024);
-        CUDA_TRY(c, cudaFuncSetAttribute(k_pcg_tm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        c->tm_fn = c->g.N == 32 ? (const void*)k_pcg_tm<32> : (const void*)k_pcg_tm<0>;
+        CUDA_TRY(c, cudaFuncSetAttribute(c->tm_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ_tm = 0;
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tm, (const void*)k_pcg_tm, 32 * W, smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tm, c->tm_fn, 32 * W, smem));
         if (occ_tm == 1 && G <= sms) {
           c->tm_W = W; c->tm_G = G; c->tm_smem = smem;
         }
@@ -1586,7 +1588,7 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   void* args[] = {&A};   // A.gbar was zeroed by k_block_chol
   if (forked) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->join_ev, 0));
   if (c->opts.onchip && c->tm_W > 0) {
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg_tm, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,
+    CUDA_TRY(c, cudaLaunchCooperativeKernel(c->tm_fn, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,
                                             c->stream));
   } else {
     CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(c->pcg_G), dim3(32 * c->pcg_W), args, c->pcg_smem,

@@ -328,6 +328,7 @@ __host__ __device__ inline TmLayout tm_layout(int W, int dim, int n_pad) {
     if (A.tstamp && threadIdx.x == 0) A.tstamp[4096 + 8 * (size_t)blockIdx.x + (k)] = gtimer();  \
   } while (0)
 
+template <int NFIX>   // NFIX = 32: N known at compile time (the lane predicates fold away)
 __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ uint32_t tbase_s;
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
   __shared__ double bc[4];
   __shared__ double sh46[46];
   const Geo& g = A.g;
-  const int N = g.N, dim = g.dim;
+  const int N = NFIX ? NFIX : g.N, dim = g.dim;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int E = blockIdx.x * W + warp;
   const bool own = E < g.n_s;

@@ -59,7 +59,7 @@ def _sass_of(fn):
 def test_onchip_pcg_uses_tensor_memory():
     """k_pcg_tm keeps the scaled couplings in tensor memory: tcgen05.st at staging (STTM), tcgen05.ld
     every iteration (LDTM), cp.async staging (LDGSTS) and release reductions for its grid barriers."""
-    sass = _sass_of("_ZN5lrbms8k_pcg_tmENS_7PcgArgsE")
+    sass = _sass_of("_ZN5lrbms8k_pcg_tmILi32EEEvNS_7PcgArgsE")
     for op in ("LDTM", "STTM", "LDGSTS", "REDG.E.ADD.STRONG.GPU"):
         assert op in sass, op
 
