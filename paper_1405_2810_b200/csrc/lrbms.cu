@@ -1222,7 +1222,8 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
       }
     }
   }
-  CUDA_TRY(c, cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_project<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_project<32, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
   CUDA_TRY(c, cudaFuncSetAttribute(k_coarse_rt_s, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   {  // TMA descriptors (128 x 32 fp32 boxes, 128-byte swizzle) for the tensor-core Newton-Schulz GEMM
@@ -1387,7 +1388,10 @@ static lrbms_status launch_project_to(lrbms_ctx* c, const double* lam, double* b
   A.fc = c->at<double2>(c->fc); A.lam = lam;
   A.blocks = blocks; A.rhs = rhs;
   A.tstamp = c->debug_tstamp;
-  k_project<<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
+  if (c->g.N == 32 && c->g.n_loc == 512)
+    k_project<32, 512><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
+  else
+    k_project<0, 0><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
   return LRBMS_OK;
 }

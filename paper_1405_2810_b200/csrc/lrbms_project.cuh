@@ -59,10 +59,11 @@ __device__ __forceinline__ int pair_tj(int p) {
   return p < 4 ? p : p < 7 ? p - 3 : p < 9 ? p - 5 : 3;
 }
 
+template <int NFIX, int NLFIX>   // compile-time N and n_loc (C5: 32, 512), 0 = runtime
 __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   extern __shared__ __align__(16) double sm[];
   const Geo& g = A.g;
-  const int N = g.N, nl = g.n_loc, E = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int N = NFIX ? NFIX : g.N, nl = NLFIX ? NLFIX : g.n_loc, E = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   const int nb1 = 1 + g.dim, LD = A.LD, NP = A.NP, T = NP / 8, nfp = A.nfp, LDN = A.LDN;
   double* Phs = sm;                               // [NP][LD]
