@@ -72,6 +72,83 @@ def test_fprime_max_closed_form_equal_viscosity_corey2():
     assert O.fprime_max(sc) == pytest.approx(2.0, rel=1e-14)
 
 
+# ---------------------------------------------------------------- residual saturations (R5)
+
+@pytest.mark.parametrize("swr,sor", [(0.1, 0.2), (0.25, 0.05), (0.0, 0.3)])
+def test_effective_saturation_residuals_closed_forms(swr, sor):
+    """S_e = (s - Swr)/(1 - Swr - Sor) (R5), pinned by values the Corey law fixes without S_e:
+    k_rw(Swr) = 0 and k_ro(1 - Sor) = 0 (the residual saturations are immobile), so
+    lambda_t(Swr) = 1/mu_o and lambda_t(1 - Sor) = 1/mu_w; at the mobile midpoint
+    s = (Swr + 1 - Sor)/2 the effective saturation is 1/2, so Corey 2 gives
+    lambda_t = (1/4)/mu_w + (1/4)/mu_o; at the mobile quarter point it gives (1/16)/mu_w + (9/16)/mu_o.
+    (A slip such as dividing by 1 - Swr moves the midpoint value.)"""
+    mu_w, mu_o = 0.7, 5.0
+    sc = inputs.custom_scenario(4, 4, 1, 2, 2, 1, 2, mu_w=mu_w, mu_o=mu_o, swr=swr, sor=sor)
+    mid = 0.5 * (swr + 1.0 - sor)
+    quarter = swr + 0.25 * (1.0 - swr - sor)
+    s = np.array([swr, 1.0 - sor, mid, quarter, swr - 0.05, 1.0 - sor + 0.05])
+    lw, ln = O.phase_mobilities(s, sc)
+    assert lw[0] == 0.0 and ln[1] == 0.0
+    lam = lw + ln
+    assert lam[0] == pytest.approx(1.0 / mu_o, rel=1e-15)
+    assert lam[1] == pytest.approx(1.0 / mu_w, rel=1e-15)
+    assert lam[2] == pytest.approx(0.25 / mu_w + 0.25 / mu_o, rel=1e-14)
+    assert lam[3] == pytest.approx(1.0 / 16.0 / mu_w + 9.0 / 16.0 / mu_o, rel=1e-14)
+    # outside the mobile range the law is clamped at its end values (A8)
+    assert lam[4] == lam[0] and lam[5] == lam[1]
+    f = O.fractional_flow(s, sc)
+    assert f[0] == 0.0 and f[1] == 1.0
+    assert f[2] == pytest.approx((0.25 / mu_w) / (0.25 / mu_w + 0.25 / mu_o), rel=1e-14)
+
+
+def _fprime_max_corey2_exact(m_ratio, digits=40):
+    """max_S f'(S) for Corey 2 with m = mu_w/mu_o, derived by hand independently of the oracle:
+    f = S^2/(S^2 + m(1-S)^2)  =>  f'(S) = 2 m S (1-S) / D^2,  D = S^2 + m (1-S)^2.
+    d/dS [S(1-S)/D^2] = 0  <=>  h(S) = (1-2S) D - 2 S (1-S) D' = 0, D' = 2S - 2m(1-S):
+    a cubic with a single root in (0, 1) at the maximum of f'; found by bisection in 40-digit
+    arithmetic (mpmath), then f' evaluated there in the same precision."""
+    import mpmath as mp
+    mp.mp.dps = digits
+    m = mp.mpf(m_ratio)
+
+    def D(S):
+        return S * S + m * (1 - S) ** 2
+
+    def h(S):
+        return (1 - 2 * S) * D(S) - 2 * S * (1 - S) * (2 * S - 2 * m * (1 - S))
+
+    lo, hi = mp.mpf("1e-30"), 1 - mp.mpf("1e-30")
+    assert h(lo) > 0 > h(hi)
+    for _ in range(200):
+        mid = (lo + hi) / 2
+        if h(mid) > 0:
+            lo = mid
+        else:
+            hi = mid
+    S = (lo + hi) / 2
+    return float(2 * m * S * (1 - S) / D(S) ** 2)
+
+
+@pytest.mark.parametrize("mu_o", [1.0, 5.0, 10.0])
+def test_fprime_max_corey2_exact_maximiser(mu_o):
+    """f'_max for the configs' fluids (Corey 2, mu_o/mu_w = 1, 5, 10) against the exact maximiser of
+    f' (root of its derivative's numerator in 40-digit arithmetic): <= 1e-13 relative."""
+    sc = inputs.custom_scenario(4, 4, 1, 2, 2, 1, 2, mu_w=1.0, mu_o=mu_o)
+    exact = _fprime_max_corey2_exact(1.0 / mu_o)
+    assert O.fprime_max(sc) == pytest.approx(exact, rel=1e-13)
+    if mu_o == 1.0:
+        assert exact == pytest.approx(2.0, rel=1e-15)
+
+
+@pytest.mark.parametrize("swr,sor", [(0.1, 0.2), (0.2, 0.0)])
+def test_fprime_max_residual_scaling(swr, sor):
+    """With residual saturations f(s) = F((s - Swr)/(1 - Swr - Sor)), so by the chain rule
+    f'_max = F'_max / (1 - Swr - Sor), F'_max the exact Corey-2 maximum above."""
+    sc = inputs.custom_scenario(4, 4, 1, 2, 2, 1, 2, mu_w=1.0, mu_o=5.0, swr=swr, sor=sor)
+    exact = _fprime_max_corey2_exact(1.0 / 5.0) / (1.0 - swr - sor)
+    assert O.fprime_max(sc) == pytest.approx(exact, rel=1e-13)
+
+
 # ---------------------------------------------------------------- SPEC per-operation examples
 
 def test_face_weight_mean_and_harmonic_penalty():
