@@ -143,7 +143,11 @@ __device__ __forceinline__ void tile_load(double (*T)[33], const double* A, int 
     T[i][j] = A[(size_t)(I * 32 + i) * n + J * 32 + j];
   }
 }
-__global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* flags) {
+// fp64 Gauss-Jordan inverse of the dense coarse matrix (n_pad too large for k_coarse_gj32).  A
+// non-positive pivot (a singular coarse matrix, e.g. zc_E = 0 for a basis orthogonal to 1_E) sets
+// *bad, and k_to_f32 then zeroes the inverse (block-Jacobi fallback), as k_coarse_gj32 does; it is
+// not FLAG_PIVOT, which is reserved for the block Cholesky of B.
+__global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* bad) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double P[32][33], T[32][33], F[32][33];
   __shared__ double rowk[32], colk[32];
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(256) k_coarse_gj(double* A, int n, int* flags)
           rowk[tid] = ((tid == k) ? 1.0 : P[k][tid]) / pk;
           colk[tid] = P[tid][k];
         }
-        if (tid == 0 && !(pk > 0.0)) atomicOr(flags, FLAG_PIVOT);
+        if (tid == 0 && !(pk > 0.0)) atomicOr(bad, 1);
         __syncthreads();
         for (int t = tid; t < 1024; t += blockDim.x) {
           const int i = t >> 5, j = t & 31;
@@ -246,12 +250,36 @@ constexpr int RT_ROWS = RT_ROWS_V;     // rows of RT per CTA (the column's stenc
 constexpr int RT_BATCH = RT_BATCH_V;   // rows whose loads are in flight together
 static_assert(32 % RT_ROWS == 0, "n_pad is a multiple of 32: every CTA's rows exist");
 static_assert(RT_ROWS % RT_BATCH == 0, "whole batches");
+// Convergence guard of the Newton-Schulz update (both RT kernels): max_ij |RT_ij| (NaN-propagating, as
+// ordered float bits) is accumulated into guard[par]; CTA 0 clears guard[1 - par] for the next step.
+__device__ __forceinline__ void ns_guard_accum(float m, unsigned* guard, int par) {
+  __shared__ unsigned gmax;
+  if (threadIdx.x == 0) gmax = 0u;
+  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    const float t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (t > m || t != t) ? t : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(&gmax, __float_as_uint(m));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicMax(guard + par, gmax);
+    if (blockIdx.x == 0 && blockIdx.y == 0) guard[1 - par] = 0u;
+  }
+}
+__device__ __forceinline__ float nanmax_abs(float m, float v) {
+  const float a = fabsf(v);
+  return (a > m || a != a) ? a : m;
+}
+
 __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restrict__ X, const double* __restrict__ Es,
-                                                   float* __restrict__ RT, int n) {
+                                                   float* __restrict__ RT, int n, unsigned* guard, int par) {
   // thread <-> column j: its stencil (coefficients, neighbour columns) in registers, reused for
   // RT_ROWS rows; the X reads of a warp are contiguous per stencil offset (L1-resident rows)
-  const int j = blockIdx.x * blockDim.x + threadIdx.x, i0 = blockIdx.y * RT_ROWS;
-  if (j >= n) return;
+  const int j0 = blockIdx.x * blockDim.x + threadIdx.x, i0 = blockIdx.y * RT_ROWS;
+  const bool active = j0 < n;
+  const int j = active ? j0 : n - 1;
+  float gm = 0.f;
   float e[7];
   int nb[7];
   nb[0] = j;
@@ -291,9 +319,14 @@ __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restric
       float v = xv[r][0] * e[0];
 #pragma unroll
       for (int s = 1; s < 7; ++s) v = fmaf(xv[r][s], e[s], v);
-      RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+      const float rt = (i == j ? 1.f : 0.f) - v;
+      if (active) {
+        RT[(size_t)i * n + j] = rt;
+        gm = nanmax_abs(gm, rt);
+      }
     }
   }
+  ns_guard_accum(gm, guard, par);
 }
 
 // The same RT with the CTA's RT_SROWS (16) rows of X staged in shared memory by cp.async first (every
@@ -303,7 +336,8 @@ __global__ void __launch_bounds__(256) k_coarse_rt(Geo g, const float* __restric
 #endif
 constexpr int RT_SROWS = RT_SROWS_V;
 __global__ void __launch_bounds__(256) k_coarse_rt_s(Geo g, const float* __restrict__ X, const double* __restrict__ Es,
-                                                     float* __restrict__ RT, int n) {
+                                                     float* __restrict__ RT, int n, unsigned* guard, int par) {
+  float gm = 0.f;
   extern __shared__ __align__(16) float xs[];   // [RT_SROWS][n]
   const int i0 = blockIdx.x * RT_SROWS;
   {
@@ -345,9 +379,12 @@ __global__ void __launch_bounds__(256) k_coarse_rt_s(Geo g, const float* __restr
 #pragma unroll
       for (int s = 1; s < 7; ++s) v = fmaf(xr[nb[s]], e[s], v);
       const int i = i0 + r;
-      RT[(size_t)i * n + j] = (i == j ? 1.f : 0.f) - v;
+      const float rt = (i == j ? 1.f : 0.f) - v;
+      RT[(size_t)i * n + j] = rt;
+      gm = nanmax_abs(gm, rt);
     }
   }
+  ns_guard_accum(gm, guard, par);
 }
 
 // R = I - E X for the Newton-Schulz update of the coarse inverse (X is not exactly symmetric:
@@ -821,6 +858,8 @@ struct lrbms_ctx {
   int tm_W = 0, tm_G = 0;   // on-chip PCG (k_pcg_tm) launch; tm_W = 0: not usable
   const void* tm_fn = nullptr;   // the k_pcg_tm instance (compile-time N = 32, or the general one)
   size_t tm_smem = 0;
+  int ns_par = 0;          // ping-pong word of the Newton-Schulz guard
+  int64_t ns_trips = 0;    // calls that ended with a skipped Newton-Schulz update (forced rebuild)
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
   int xcur = 0;            // which of Binv32 / Binv32b holds the current coarse inverse
   CUtensorMap tmX[2], tmRT;  // TMA descriptors of the coarse inverse buffers and of RT
@@ -1267,6 +1306,13 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   return LRBMS_OK;
 }
 
+// NEXT-1 state (b_q, d_q, the Gram matrix) depends on K and Phi: a new medium or basis drops it; the
+// affine variant then needs set_profiles again (set_online(1) returns STATE until it is called)
+static void invalidate_profiles(lrbms_ctx* c) {
+  c->prof_M = 0;
+  c->affine = false;
+}
+
 lrbms_status lrbms_set_medium(lrbms_ctx* c, const double* K, const double* phi) {
   lrbms_status st = check_ctx(c);
   if (st) return st;
@@ -1301,6 +1347,7 @@ lrbms_status lrbms_set_medium(lrbms_ctx* c, const double* K, const double* phi) 
   }
   c->have_medium = true;
   c->have_blocks = false;
+  invalidate_profiles(c);   // b_q, d_q were projected with the old K
   return LRBMS_OK;
 }
 
@@ -1316,6 +1363,7 @@ lrbms_status lrbms_set_basis(lrbms_ctx* c, const double* Phi) {
   c->have_blocks = false;
   c->last_rebuild_step = -1;
   c->have_x = false;
+  invalidate_profiles(c);   // b_q, d_q were projected onto the old Phi
   return LRBMS_OK;
 }
 
@@ -1398,6 +1446,10 @@ static lrbms_status launch_project_to(lrbms_ctx* c, const double* lam, double* b
 
 static size_t block_len(const lrbms_ctx* c) { return (size_t)c->g.n_s * (1 + c->g.dim) * c->g.N * c->g.N; }
 
+// elements between consecutive profiles' b_q (or d_q): the length rounded up to an even count, so
+// that every profile starts 16-byte aligned for k_affine_combine's double2 loads
+static inline size_t profile_stride(size_t len) { return (len + 1) & ~(size_t)1; }
+
 // a2 of the step: the direct projection of A(lambda(s^n)) (north star, reading R3), or the paper's
 // affine variant (NEXT-1): theta fit + sum_q theta_q b_q, d_q
 static lrbms_status launch_project(lrbms_ctx* c) {
@@ -1417,10 +1469,12 @@ static lrbms_status launch_project(lrbms_ctx* c) {
 #define AFF_GRID 8
 #endif
     k_affine_combine<<<AFF_GRID * c->sms, 256, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_bq), theta,
-                                                        c->prof_M, block_len(c), c->at<double>(c->blocks));
+                                                        c->prof_M, block_len(c), profile_stride(block_len(c)),
+                                                        c->at<double>(c->blocks));
     LAUNCH_CHECK(c);
     k_affine_combine<<<cdiv((int)(R / 2 + 1), 256), 256, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_dq),
-                                                                          theta, c->prof_M, R, c->at<double>(c->rhs));
+                                                                          theta, c->prof_M, R, profile_stride(R),
+                                                                          c->at<double>(c->rhs));
     LAUNCH_CHECK(c);
   } else {
     st = launch_project_to(c, c->lam_cur(), c->at<double>(c->blocks), c->at<double>(c->rhs));
@@ -1460,11 +1514,13 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
       CUDA_TRY(c, cudaMemsetAsync(Bc, 0, c->Binv.bytes, c->stream));
       k_coarse_dense<<<cdiv(n, 256), 256, 0, c->stream>>>(g, c->at<double>(c->Es), Bc, n);
       LAUNCH_CHECK(c);
-      int* fl = c->at<int>(c->flags);
-      void* args[] = {&Bc, &n, &fl};
+      unsigned* bar = c->at<unsigned>(c->gjbar);
+      int* bad = reinterpret_cast<int*>(bar + 16);
+      CUDA_TRY(c, cudaMemsetAsync(bar, 0, 256, c->stream));
+      void* args[] = {&Bc, &n, &bad};
       CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj, dim3(c->gj_G), dim3(256), args, 0, c->stream));
       c->launches++;
-      k_to_f32<<<592, 256, 0, c->stream>>>(Bc, coarse_x(c, c->xcur), (size_t)n * n);
+      k_to_f32<<<592, 256, 0, c->stream>>>(Bc, coarse_x(c, c->xcur), (size_t)n * n, bad);
       LAUNCH_CHECK(c);
     }
     c->rebuilds++;
@@ -1474,16 +1530,20 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
     float* X = coarse_x(c, c->xcur);
     float* Xn = coarse_x(c, 1 - c->xcur);
     if (c->have_tmaps) {   // tcgen05 (TF32, TMEM accumulators), upper-triangular tiles, symmetric output
+      unsigned* guard = reinterpret_cast<unsigned*>(c->at<int>(c->flags) + FLAGW_NSMAX);
+      const int par = c->ns_par;
       if ((size_t)RT_SROWS * n * 4 <= 200 * 1024)
         k_coarse_rt_s<<<n / RT_SROWS, 256, (size_t)RT_SROWS * n * 4, c->stream>>>(g, X, c->at<double>(c->Es),
-                                                                                  c->at<float>(c->RTb), n);
+                                                                                  c->at<float>(c->RTb), n, guard, par);
       else
         k_coarse_rt<<<dim3(cdiv(n, 256), cdiv(n, RT_ROWS)), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es),
-                                                                                c->at<float>(c->RTb), n);
+                                                                                c->at<float>(c->RTb), n, guard, par);
       LAUNCH_CHECK(c);
       const int nbt = cdiv(n, NS_TM);
-      k_ns_gemm_tc<<<nbt * (nbt + 1) / 2, 128, NS_TC_SMEM, c->stream>>>(c->tmX[c->xcur], c->tmRT, X, Xn, n);
+      k_ns_gemm_tc<<<nbt * (nbt + 1) / 2, 128, NS_TC_SMEM, c->stream>>>(c->tmX[c->xcur], c->tmRT, X, Xn, n,
+                                                                         guard + par, c->at<int>(c->flags) + FLAGW_NSTRIP);
       LAUNCH_CHECK(c);
+      c->ns_par ^= 1;
     } else {                 // mma.sync fallback
       k_coarse_r<<<dim3(cdiv(n, 256), n), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es), c->at<float>(c->RTb), n);
       LAUNCH_CHECK(c);
@@ -1667,6 +1727,11 @@ static lrbms_status finish(lrbms_ctx* c, int nsteps_iters_known) {
   resolve_events(c);
   c->last_iters = it[0];
   c->total_iters = it[1];
+  if (hf[FLAGW_NSTRIP]) {   // a Newton-Schulz update was skipped (||I - E X||_max too large): rebuild next call
+    c->have_x = false;
+    c->ns_trips++;
+    CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->flags) + FLAGW_NSTRIP, 0, 4, c->stream));
+  }
   if (hf[0]) {
     std::string m;
     if (hf[0] & FLAG_PIVOT) m += "non-positive pivot (B not SPD: rank-deficient Phi_E or lambda <= 0); ";
@@ -1768,8 +1833,8 @@ static void profile_layout(const lrbms_ctx* c, int M, size_t* offs, size_t* tota
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o += (bytes + 255) / 256 * 256; return r; };
   offs[0] = take(8 * (size_t)M * n);                 // lambda_{t,q}, internal order
-  offs[1] = take(8 * (size_t)M * block_len(c));      // b_q
-  offs[2] = take(8 * (size_t)M * R);                 // d_q
+  offs[1] = take(8 * (size_t)M * profile_stride(block_len(c)));   // b_q
+  offs[2] = take(8 * (size_t)M * profile_stride(R));              // d_q
   offs[3] = take(8 * (size_t)M * M);                 // Gram
   offs[4] = take(8 * (size_t)M * AFF_PGRID * (size_t)c->sms);   // per-CTA partials
   offs[5] = take(8 * AFF_MAXM);                      // theta
@@ -1808,8 +1873,9 @@ lrbms_status lrbms_set_profiles(lrbms_ctx* c, const double* s_profiles, int32_t 
     LAUNCH_CHECK(c);
     k_mobility<<<nb, 256, 0, c->stream>>>(g, c->f, c->at<double>(c->tmp), lamq + (size_t)q * n, scratch);
     LAUNCH_CHECK(c);
-    if ((st = launch_project_to(c, lamq + (size_t)q * n, reinterpret_cast<double*>(c->pws + c->off_bq) + q * block_len(c),
-                                reinterpret_cast<double*>(c->pws + c->off_dq) + q * R)))
+    if ((st = launch_project_to(c, lamq + (size_t)q * n,
+                                reinterpret_cast<double*>(c->pws + c->off_bq) + q * profile_stride(block_len(c)),
+                                reinterpret_cast<double*>(c->pws + c->off_dq) + q * profile_stride(R))))
       return st;
   }
   double* part = reinterpret_cast<double*>(c->pws + c->off_part);
@@ -1944,6 +2010,7 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
     c->launches++;
     c->p_valid = true;
     if ((st = launch_transport(c, cfl, dt_fixed, dt_log, k, nullptr, nullptr))) return st;
+    c->steps++;
   }
   if (F.coarse) c->have_x = false;   // the coarse buffers hold the fine E^-1 now
   int it[2] = {0, 0};
@@ -2013,6 +2080,13 @@ lrbms_status lrbms_get_stats(lrbms_ctx* c, lrbms_stats* o) {
   o->last_iters = it[0];
   o->total_iters = it[1];
   o->coarse_rebuilds = c->rebuilds;
+  o->ns_guard_trips = c->ns_trips;
+  unsigned gw[2] = {0u, 0u};
+  CUDA_TRY(c, cudaMemcpyAsync(gw, c->at<int>(c->flags) + FLAGW_NSMAX, 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float last;
+  memcpy(&last, &gw[1 - c->ns_par], 4);
+  o->ns_resid_max = last;
   o->fprime_max = c->fpmax;
   return LRBMS_OK;
 }

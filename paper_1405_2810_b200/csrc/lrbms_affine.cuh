@@ -107,22 +107,23 @@ __global__ void k_theta_solve(const double* __restrict__ part, int G, int M, con
   for (int q = 0; q < M; ++q) theta[q] = t[q];
 }
 
-// out[i] = sum_q theta_q X[q][i] for i < len (the reduced operator or right-hand side), 16-byte
-// streaming loads (len even) -- one pass over the M precomputed operators
+// out[i] = sum_q theta_q X[q * qstride + i] for i < len (the reduced operator or right-hand side), 16-byte
+// streaming loads -- one pass over the M precomputed operators.  qstride (elements between profiles)
+// is even (profile_stride), so every profile starts 16-byte aligned whatever the parity of len.
 __global__ void __launch_bounds__(256) k_affine_combine(const double* __restrict__ X, const double* __restrict__ theta,
-                                                        int M, size_t len, double* __restrict__ out) {
+                                                        int M, size_t len, size_t qstride, double* __restrict__ out) {
   double th[AFF_MAXM];
 #pragma unroll
   for (int q = 0; q < AFF_MAXM; ++q) th[q] = q < M ? theta[q] : 0.0;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  const size_t h = len >> 1;
+  const size_t h = len >> 1, h2 = qstride >> 1;
   const double2* X2 = reinterpret_cast<const double2*>(X);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < h; i += stride) {
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
     for (int q = 0; q < AFF_MAXM; ++q)
       if (q < M) {
-        const double2 v = __ldcs(X2 + (size_t)q * h + i);
+        const double2 v = __ldcs(X2 + (size_t)q * h2 + i);
         a0 = fma(th[q], v.x, a0);
         a1 = fma(th[q], v.y, a1);
       }
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(256) k_affine_combine(const double* __restrict
   }
   if ((len & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     double a = 0.0;
-    for (int q = 0; q < M; ++q) a = fma(th[q], X[(size_t)q * len + len - 1], a);
+    for (int q = 0; q < M; ++q) a = fma(th[q], X[(size_t)q * qstride + len - 1], a);
     out[len - 1] = a;
   }
 }

@@ -66,7 +66,8 @@ constexpr uint32_t NS_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N
 
 __global__ void __launch_bounds__(128, 1) k_ns_gemm_tc(const __grid_constant__ CUtensorMap mapX,
                                                        const __grid_constant__ CUtensorMap mapRT,
-                                                       const float* __restrict__ X, float* __restrict__ Xn, int n) {
+                                                       const float* __restrict__ X, float* __restrict__ Xn, int n,
+                                                       const unsigned* __restrict__ guard, int* __restrict__ trip) {
   extern __shared__ uint8_t ns_raw[];
   __shared__ __align__(8) uint64_t full[NS_STAGES], empty[NS_STAGES], done;
   __shared__ uint32_t tmem_base;
@@ -138,7 +139,13 @@ __global__ void __launch_bounds__(128, 1) k_ns_gemm_tc(const __grid_constant__ C
   }
   __syncwarp();
 
-  // epilogue: warp w owns TMEM lanes (tile rows) 32 w .. 32 w + 31
+  // epilogue: warp w owns TMEM lanes (tile rows) 32 w .. 32 w + 31.  Guard: if max |I - E X| of this
+  // step (k_coarse_rt*) is >= NS_GUARD_MAX or NaN, the iteration is not converging to E^-1: the
+  // inverse is dropped (Xn = 0, the solve continues as block-Jacobi PCG, which the deflation variant
+  // with a wrong coarse inverse would not) and the context is flagged; it rebuilds at its next call
+  const float gmax = __uint_as_float(__ldcg(guard));
+  const bool keep = gmax < NS_GUARD_MAX;
+  if (!keep && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(trip, 1);
   mbar_wait_parity(&done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const int row = I * NS_TM + 32 * warp + lane;
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(128, 1) k_ns_gemm_tc(const __grid_constant__ C
           for (int q = 0; q < 32; ++q) {
             const int col = col0 + q;
             if (col < row) continue;
-            const float val = X[(size_t)col * n + row] + __uint_as_float(v[q]);
+            const float val = keep ? X[(size_t)col * n + row] + __uint_as_float(v[q]) : 0.f;
             Xn[(size_t)row * n + col] = val;
             Xn[(size_t)col * n + row] = val;
           }
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(128, 1) k_ns_gemm_tc(const __grid_constant__ C
         float val[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q)   // X symmetric: X[row][col] = X[col][row], read coalesced
-          val[q] = (row < n) ? X[(size_t)(col0 + q) * n + row] + __uint_as_float(v[q]) : 0.f;
+          val[q] = (row < n && keep) ? X[(size_t)(col0 + q) * n + row] + __uint_as_float(v[q]) : 0.f;
         if (row < n) {
           float4* dst = reinterpret_cast<float4*>(Xn + (size_t)row * n + col0);
 #pragma unroll

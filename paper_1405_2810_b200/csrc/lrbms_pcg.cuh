@@ -1010,10 +1010,13 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
   }
 }
 
-__global__ void k_to_f32(const double* __restrict__ a, float* __restrict__ b, size_t n) {
+// b = (float) a; with *bad set (a singular coarse matrix met a non-positive pivot) b = 0 instead: the
+// coarse level is dropped and the solve continues as block Jacobi -- the same policy as k_coarse_gj32
+__global__ void k_to_f32(const double* __restrict__ a, float* __restrict__ b, size_t n, const int* __restrict__ bad) {
   size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   const size_t st = (size_t)gridDim.x * blockDim.x;
-  for (; i < n; i += st) b[i] = (float)a[i];
+  const bool zero = bad && __ldcg(bad) != 0;
+  for (; i < n; i += st) b[i] = zero ? 0.f : (float)a[i];
 }
 
 }  // namespace lrbms

@@ -59,7 +59,8 @@ class SolverOpts(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int64), ("t", ctypes.c_double), ("last_dt", ctypes.c_double),
                 ("last_iters", ctypes.c_int32), ("total_iters", ctypes.c_int64),
-                ("coarse_rebuilds", ctypes.c_int32), ("fprime_max", ctypes.c_double)]
+                ("coarse_rebuilds", ctypes.c_int32), ("fprime_max", ctypes.c_double),
+                ("ns_guard_trips", ctypes.c_int64), ("ns_resid_max", ctypes.c_double)]
 
 
 _lib = None

@@ -92,11 +92,12 @@ def test_full_run_small(name, make, onchip):
     ctx = ctx_for(sc, onchip=onchip)
     dts = np_(ctx.run(n, log_dt=True))
     s, p, c = ctx.get_state()
+    st = ctx.stats()
+    print(f"{name}: iters {st['total_iters']}, ns max|I-EX| {st['ns_resid_max']:.3e}, trips {st['ns_guard_trips']}")
     assert rel(dts, ref["dts"]) <= 1e-10
     assert rel(np_(c), ref["cs"][-1]) <= 1e-10
     assert rel(np_(p), ref["ps"][-1]) <= 1e-10
     assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
-    st = ctx.stats()
     assert st["steps"] == n and st["total_iters"] > 0
     ctx.close()
 
@@ -309,6 +310,8 @@ def test_c4_prefix_tight_solver():
 AFFINE = [
     ("C1", lambda: inputs.make_scenario("C1")),
     ("C2", lambda: inputs.make_scenario("C2")),
+    # odd n_s (3 x 3) and odd N: the lengths of b_q (9*3*25) and d_q (45) are odd
+    ("odd_len", lambda: inputs.custom_scenario(15, 15, 1, 5, 5, 1, 5, seed=26, mu_o=5.0)),
     ("ragged3d", lambda: inputs.custom_scenario(9, 6, 4, 3, 3, 2, 11, seed=22, mu_o=10.0, bc="corner_columns_3d",
                                                 hx=0.5, hy=1.5, hz=2.0)),
 ]
@@ -397,3 +400,29 @@ def test_affine_errors():
     with pytest.raises(LrbmsError) as e:
         ctx.set_profiles(np.zeros((17, sc.n)))
     assert e.value.status == LRBMS_E_CONFIG
+    # a new medium or basis invalidates b_q, d_q: the affine variant needs set_profiles again
+    sp = inputs.profile_saturations(sc)
+    for reset in (lambda: ctx.set_medium(sc.K * 2.0), lambda: ctx.set_basis(sc.Phi)):
+        ctx.set_profiles(sp)
+        ctx.set_online(True)
+        reset()
+        with pytest.raises(LrbmsError) as e:
+            ctx.set_online(True)
+        assert e.value.status == LRBMS_E_STATE
+
+
+def test_affine_after_new_medium_matches_oracle():
+    """set_profiles after set_medium recomputes b_q, d_q with the new K."""
+    sc = inputs.make_scenario("C1")
+    sp = inputs.profile_saturations(sc)
+    ctx = ctx_for(sc)
+    ctx.set_profiles(sp)
+    sc.K = sc.K * np.linspace(0.5, 2.0, sc.n)
+    ctx.set_medium(sc.K)
+    ctx.set_profiles(sp)
+    ctx.set_online(True)
+    ref = O.run(sc, n_steps=5, keep=True, s_profiles=sp)
+    ctx.run(5)
+    s, p, c = ctx.get_state()
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
