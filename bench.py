@@ -36,13 +36,16 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--basis", default="poly")
+    ap.add_argument("--basis", default="pod",
+                    help="local bases: pod = the paper's offline recipe (host, offline/recipe.py); poly")
+    ap.add_argument("--reps", type=int, default=5, help="timed repetitions of the window (median reported)")
+    ap.add_argument("--no-small", dest="small", action="store_false",
+                    help="skip the C1-C4 us/step keys")
+    ap.add_argument("--cpu-steps", type=int, default=3, help="oracle steps timed for cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--coarse-refresh", type=int, default=None)
     ap.add_argument("--rtol", type=float, default=None)
-    ap.add_argument("--profile-steps", type=int, default=100,
-                    help="steps of the separate profiled pass that gives the per-stage times")
     ap.add_argument("--fine-steps", type=int, default=5,
                     help="steps timed in the fine-scale reference scheme (NEXT-2, Phi_E = I; 0 = skip)")
     ap.add_argument("--affine-steps", type=int, default=50,
@@ -250,6 +253,56 @@ def run_reference(args, rank, world):
     return 0
 
 
+def timed_window(ctx, sc, W, K, world, device, profile=False):
+    """One repetition of the timed window: from s0 (set_saturation resets the solver history and the
+    coarse inverse, so every repetition does identical work), W untimed steps, then K steps timed with
+    CUDA events on the library's stream, inputs resident in HBM.  Returns (ms max over ranks, PCG
+    iterations per step, kernel launches, stage times or None)."""
+    import torch
+    ctx.set_saturation(sc.s0)
+    ctx.run(W)
+    st0 = ctx.stats()
+    if profile:
+        ctx.set_profiling(True)
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    ctx.run(K)
+    e1.record(ctx.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - l0
+    stages = None
+    if profile:
+        stages = ctx.stage_times()
+        ctx.set_profiling(False)
+    st1 = ctx.stats()
+    barrier(world)
+    return max_over_ranks(ms, world, device), (st1["total_iters"] - st0["total_iters"]) / K, launches, stages
+
+
+def small_configs(args, device):
+    """us per step of the latency-bound configs C1-C4 (paper-recipe bases), median of 3
+    repetitions of a window from s0 (3 untimed steps, then min(steps, 50) timed)."""
+    from paper_1405_2810_b200 import inputs
+    from paper_1405_2810_b200.lrbms import LrbmsContext
+    out = {}
+    for cfg in ("C1", "C2", "C3", "C4"):
+        sc = inputs.make_scenario(cfg, basis=args.basis)
+        ctx = LrbmsContext(sc, device=device)
+        K = min(sc.n_steps, 50)
+        reps = [timed_window(ctx, sc, 3, K, 1, device) for _ in range(3)]
+        ms = statistics.median(r[0] for r in reps)
+        out[cfg] = {"us_per_step": round(1e3 * ms / K, 2), "steps_per_s": round(1e3 * K / ms, 1), "steps": K,
+                    "pcg_iters_per_step": reps[0][1], "launches_per_step": reps[0][2] / K,
+                    "cells": sc.n, "reduced_dofs": sc.n_s * sc.N}
+        ctx.close()
+    return out
+
+
 def run_ours(args, rank, local, world):
     import torch
     from paper_1405_2810_b200 import inputs
@@ -269,43 +322,34 @@ def run_ours(args, rank, local, world):
     stream = ctx.stream
     K, W = args.steps, args.warmup
 
-    # ---- warm-up (untimed), then the timed region on device, inputs resident in HBM
-    ctx.run(W)
-    st0 = ctx.stats()
-    barrier(world)
-    torch.cuda.synchronize()
+    # ---- the headline: median of --reps repetitions of the same window (W untimed + K timed steps
+    #      from s0), clocks sampled during them
+    ctx.run(1)   # first-call costs (TMA descriptors, occupancy queries) outside every window
     clocks = ClockSampler(local)
     clocks.start()
-    l0 = ctx.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    ctx.run(K)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    launches = ctx.launch_count() - l0
+    reps = [timed_window(ctx, sc, W, K, world, device) for _ in range(args.reps)]
     clk = clocks.stop()
-    st1 = ctx.stats()
-    barrier(world)
-    ms_max = max_over_ranks(ms, world, device)
+    rep_ms = [r[0] for r in reps]
+    ms_max = statistics.median(rep_ms)
     value = world * K / (ms_max / 1e3)
-    iters = (st1["total_iters"] - st0["total_iters"]) / K
+    iters = reps[0][1]
+    launches = reps[0][2]
+    ms = ms_max
 
-    # ---- per-stage device times: a separate profiled pass (CUDA events around every stage cost
-    #      ~70 us per step, so they stay out of the timed region above); continues the trajectory
-    Kp = max(1, min(K, args.profile_steps))
-    sp0 = ctx.stats()
-    ctx.set_profiling(True)
-    ctx.run(Kp)
-    stages = ctx.stage_times()
-    ctx.set_profiling(False)
-    iters_p = (ctx.stats()["total_iters"] - sp0["total_iters"]) / Kp
+    # ---- per-stage device times of the SAME window (CUDA events around every stage cost ~70 us per
+    #      step, so this is one extra repetition, not one of the timed ones; deterministic, so the
+    #      iteration count equals the headline's)
+    _, iters_p, _, stages = timed_window(ctx, sc, W, K, world, device, profile=True)
+    Kp = K
+    diag = ctx.diagnostics()   # K6 of the window's last step (off the timed path)
 
-    # ---- e2e: the same metric through the C ABI with HOST buffers (pinned), copies inside
-    Ke = args.e2e_steps or max(1, min(K, 50))
+    # ---- e2e: the same window through the C ABI with HOST buffers (pinned): every step copies s in
+    #      and s, p out inside the timed region
+    Ke = args.e2e_steps or K
     s_pin = torch.empty(sc.n, dtype=torch.float64, pin_memory=True)
     p_pin = torch.empty(sc.n, dtype=torch.float64, pin_memory=True)
+    ctx.set_saturation(sc.s0)
+    ctx.run(W)
     s_dev, _, _ = ctx.get_state()
     s_pin.copy_(s_dev.cpu())
     barrier(world)
@@ -322,6 +366,8 @@ def run_ours(args, rank, local, world):
     ms_e2e = max(e2.elapsed_time(e3), 1e3 * t_wall)
     ms_e2e = max_over_ranks(ms_e2e, world, device)
     e2e_value = world * Ke / (ms_e2e / 1e3)
+
+    small = small_configs(args, device) if (world == 1 and args.small) else None
 
     # ---- NEXT-1: the paper's affine online variant on the same workload (theta fit + sum_q theta_q
     #      b_q instead of the direct projection); reported beside the north-star metric, not as it
@@ -413,15 +459,21 @@ def run_ours(args, rank, local, world):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        ts = oracle_sample(args.config, args.basis, 1)
-        cpu = {"value": 1.0 / sum(ts), "unit": "steps/s", "cores": cpu_threads(), "kind": "oracle",
-               "sample": f"1 oracle online step of {args.config} from s0 ({sum(ts):.1f} s), "
-                         "NumPy/SciPy fp64 oracle as it stands"}
+        from threadpoolctl import threadpool_limits
+        n_cpu = max(1, args.cpu_steps)
+        ts_all = oracle_sample(args.config, args.basis, n_cpu + 1)[1:]
+        with threadpool_limits(1):
+            ts_one = oracle_sample(args.config, args.basis, 2)[1:]
+        cpu = {"value": n_cpu / sum(ts_all), "unit": "steps/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"{n_cpu} oracle online steps of {args.config} after 1 untimed step from s0 "
+                         f"({sum(ts_all):.1f} s) on all host threads; NumPy/SciPy fp64 oracle as it stands",
+               "one_thread": {"value": 1.0 / sum(ts_one), "unit": "steps/s", "cores": 1,
+                              "sample": f"1 oracle step after 1 untimed step, BLAS limited to 1 thread ({sum(ts_one):.1f} s)"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded C5 recipe of DESIGN.md; no dataset)",
+        "dtype": "f64", "data": "synthetic (seeded %s recipe of DESIGN.md section 4, %s bases; no dataset)" % (args.config, args.basis),
         "config": {"workload": args.config, "grid": f"{sc.nx}x{sc.ny}x{sc.nz}",
                    "subdomains": f"{sc.Sx}x{sc.Sy}x{sc.Sz} of {sc.sx}x{sc.sy}x{sc.sz}", "N": sc.N,
                    "cells": sc.n, "reduced_dofs": sc.n_s * sc.N, "basis": args.basis,
@@ -429,7 +481,9 @@ def run_ours(args, rank, local, world):
                    "parallelism": "replicas" if world > 1 else "single GPU"},
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": 8 * sc.n,
-                "d2h_bytes_per_step": 16 * sc.n, "steps": Ke},
+                "d2h_bytes_per_step": 16 * sc.n, "steps": Ke,
+                "note": "lrbms_run_host with pinned host buffers, one step per call (s in, s and p out), "
+                        "the same window as the headline"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_pcg_tm" if dom == "pcg" else dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -440,8 +494,13 @@ def run_ours(args, rank, local, world):
                               "construction; it is bound by the latency of its three grid-wide synchronisations "
                               "per iteration (sync_roofline)") if dom == "pcg" else ""},
         "sync_roofline": sync_roofline(stages, Kp, iters_p),
+        "reps": {"ms_per_window": [round(x, 4) for x in rep_ms], "median_ms": ms_max, "window": f"{W} untimed + {K} timed steps from s0"},
         "profiled_pass": {"steps": Kp, "pcg_iters_per_step": iters_p,
-                          "note": "stage times, roofline and sync_roofline come from this separate pass"},
+                          "note": "stage times, roofline and sync_roofline come from one more repetition of the "
+                                  "same window with per-stage CUDA events (same iterations as the headline)"},
+        "small_configs": small,
+        "diagnostics": dict(diag, note="K6 (lrbms_diagnostics) after the window's last step: mass, s range, "
+                                       "relative mass loss zeta (P:1114-1120), coarse defect, link fluxes"),
         "step_roofline": {"algorithmic_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (step_ms / 1e3) / 1e9,
                           "frac": step_bytes / (step_ms / 1e3) / 1e9 / peak,
                           "t_roof_us": t_roof_us, "frac_time": t_roof_us / (1e3 * step_ms),

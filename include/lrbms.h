@@ -212,6 +212,25 @@ lrbms_status lrbms_stage_transport(lrbms_ctx *ctx, double cfl, double dt_fixed,
 
 lrbms_status lrbms_get_stats(lrbms_ctx *ctx, lrbms_stats *out);
 
+/* K6 diagnostics of the last step (off the timed path; one kernel per subdomain + a
+ * fixed-order sum, deterministic; synchronises the stream).  Needs a step since set_saturation
+ * (STATE otherwise).  zeta is the paper's relative mass loss of the step's velocity,
+ * zeta(T) = |int_dT u.n dS| / max_{x in dT} |u(x)|, with u.n on a face or link its
+ * flux density F/|F| (A27); 0 for the fine scheme, > 0 for reduced bases.
+ * coarse_defect = max_E |sum_{i in E} int_dT_i u.n| (0 when 1_E is in span Phi_E).
+ * mass_balance = |mass - mass_prev + dt water_out| / max(mass, mass_prev) (pin P3: round-off). */
+typedef struct {
+  double mass_prev, mass;      /* sum_i phi_i V_i s_i before / after the last step */
+  double s_min, s_max;         /* range of s after the last step */
+  double zeta_max, zeta_mean;  /* relative mass loss over the cells */
+  double coarse_defect;
+  double water_out;            /* sum over links of F_L f(s_up) (water leaving per unit time) */
+  double q_in, q_out;          /* total link inflow / outflow rates */
+  double dt;                   /* dt of the last step */
+  double mass_balance;
+} lrbms_diag;
+lrbms_status lrbms_diagnostics(lrbms_ctx *ctx, lrbms_diag *out);
+
 /* Per-stage device timing with CUDA events on the bound stream (off by default).
  * Stages: 0 project (a1+a2), 1 coarse-level rebuild, 2 block Cholesky + scaling of the couplings,
  * 3 initial guess from the solution history, 4 PCG (a3), 5 reconstruction (a4), 6 flux + CFL (a5),

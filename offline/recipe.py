@@ -37,6 +37,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 DIRECT_MAX_CELLS = 300_000
+PARALLEL_MIN_CELLS = 50_000     # snapshots of larger problems are solved in worker processes
 
 
 # ----------------------------------------------------------------------------- mobilities (R5)
@@ -283,7 +284,7 @@ def snapshots(sc, LW, LO, mus, p0=None, workers=None):
     with total mobility lambda_w^(j) + lambda_o^(j).  Returns [n_train][n]."""
     lam = mus @ (LW + LO)
     P = np.empty((len(mus), sc.n))
-    if sc.n <= DIRECT_MAX_CELLS:
+    if sc.n <= PARALLEL_MIN_CELLS:
         for j in range(len(mus)):
             P[j] = fine_solve(sc, lam[j])
         return P
@@ -384,6 +385,12 @@ class OfflineResult:
 def pod_recipe(sc, seed, M=8, n_train=None, keep_snapshots=False, workers=None, eps_pca=1e-8):
     """The whole offline recipe for scenario ``sc`` (its K, links, s0, N, n_steps): steps 1-6 above.
     seed: training-set seed (100 + config index for C1..C5)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):   # BLAS reductions in a fixed order: bits independent of the core count
+        return _pod_recipe(sc, seed, M, n_train, keep_snapshots, workers, eps_pca)
+
+
+def _pod_recipe(sc, seed, M, n_train, keep_snapshots, workers, eps_pca):
     N = sc.N
     n_train = 2 * N if n_train is None else n_train
     fl = initial_flow(sc)

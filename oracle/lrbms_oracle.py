@@ -544,3 +544,51 @@ def fine_step(sc, s, fpmax=None, dt_fixed=0.0):
     Ff, Fl = fluxes(sc, p, lam)
     dt = dt_fixed if dt_fixed > 0 else cfl_time_step(sc, Ff, Fl, fpmax)
     return dict(s=transport(sc, s, Ff, Fl, dt), p=p, dt=dt, Ff=Ff, Fl=Fl)
+
+
+# ----------------------------------------------------------------------------
+# diagnostics of a step (the paper's fine-grid mass-conservation measure)
+# ----------------------------------------------------------------------------
+
+
+def total_mass(sc, s):
+    """sum_i phi_i V_i s_i: the water volume (the quantity eq:saturationDG conserves, pin P3)."""
+    phi = np.ones(sc.n) if sc.phi is None else sc.phi
+    return float(np.sum(phi * cell_volume(sc) * s))
+
+
+def face_areas(sc):
+    h = (sc.hx, sc.hy, sc.hz)
+    return np.array([h[(d + 1) % 3] * h[(d + 2) % 3] for d in range(3)])
+
+
+def cell_net_outflow(sc, Ff, Fl):
+    """int_{dT} u.n dS per cell: the outward total flux over the cell's faces and links."""
+    a, b, _ = interior_faces(sc)
+    net = np.zeros(sc.n)
+    np.add.at(net, a, Ff)
+    np.add.at(net, b, -Ff)
+    np.add.at(net, sc.link_cell.astype(np.int64), Fl)
+    return net
+
+
+def relative_mass_loss(sc, Ff, Fl):
+    """zeta(T) = |int_{dT} u.n dS| / max_{x in dT} |u(x)|.  At k = 0 the velocity on a
+    face is represented by its normal flux density F_F/|F|, so the max runs over the cell's faces and
+    links (reading A27)."""
+    a, b, ax = interior_faces(sc)
+    area = face_areas(sc)
+    umax = np.zeros(sc.n)
+    u = np.abs(Ff) / area[ax] if len(ax) else np.zeros(0)
+    np.maximum.at(umax, a, u)
+    np.maximum.at(umax, b, u)
+    lc = sc.link_cell.astype(np.int64)
+    np.maximum.at(umax, lc, np.abs(Fl) / area[sc.link_axis])
+    net = cell_net_outflow(sc, Ff, Fl)
+    return np.where(umax > 0, np.abs(net) / np.where(umax > 0, umax, 1.0), 0.0)
+
+
+def link_water_outflow(sc, s, Fl):
+    """sum_L F_L f(s_up): the water leaving through links in one step (eq:upwind on links)."""
+    s_up = np.where(Fl >= 0.0, s[sc.link_cell.astype(np.int64)], sc.link_s)
+    return float(np.sum(Fl * fractional_flow(s_up, sc)))

@@ -1,15 +1,24 @@
 // lrbms.cu -- B200-native (sm_100a) LRBMS online step behind the C ABI of include/lrbms.h.
 //
-// One online step (alg:fullTwoPhaseScheme, with direct projection R3):
-//   k_project    a1 + a2  one CTA per subdomain: lambda(s) fused into the k = 0 SWIP operator,
-//                         Y = A_EE Phi_E in shared memory, B_EE = Phi_E^T Y, coupling blocks
-//                         B_{E,E+e_d} = -sum_F w_F phi_a phi_b^T, r_E = Phi_E^T b
-//   k_pcg        a3       one cooperative persistent kernel: warp-per-subdomain two-level PCG
-//                         (block-Jacobi + coarse correction), device-side termination
-//   k_recon      a4       p = Phi_E c_E, coalesced streaming read of Phi
-//   k_flux_cfl   a5       face/link fluxes with lambda(s^n), per-cell Q_i, global min dt
-//   k_transport  a6       explicit upwind update
-// plus the coarse level (k_coarse_gj32 / k_coarse_gj inverses, k_coarse_rt + k_ns_gemm updates).
+// One online step (alg:fullTwoPhaseScheme, with direct projection R3), in launch
+// order (DESIGN.md section 5 has the per-kernel roofline table):
+//   k_project        a1 + a2  one CTA per subdomain: face weights of lambda(s^n) (formed by the
+//                             previous transport), B_EE = Phi_E (A_EE Phi_E^T) on DMMA with the
+//                             stencil product formed in registers, couplings on DMMA from staged face
+//                             slabs, r_E = Phi_E^T b (lrbms_project.cuh)
+//   k_block_chol,    a3       B_EE = L L^T per subdomain, L^-1, scaled couplings L^-1 B L^-T, coarse
+//   k_transform_h             stencil E = Z^T B Z, deflation vectors (lrbms_pcg.cuh)
+//   k_coarse_rt_s +  a3       coarse inverse kept current: R^T = I - X E, X += X R on tcgen05 (TF32,
+//   k_ns_gemm_tc              TMA ring, TMEM accumulator) on a side stream (lrbms_ns.cuh); full
+//                             Gauss-Jordan inverse (k_coarse_gj32) at step 0 and every coarse_refresh
+//   k_hist_*         a3       Galerkin initial guess from the last 8 solutions
+//   k_pcg_tm         a3       cooperative deflated PCG (A-DEF2), one warp per subdomain, the scaled
+//                             couplings held in tensor memory / shared memory for the whole solve
+//                             (lrbms_pcg_tm.cuh); k_pcg streams them from L2 (onchip = 0)
+//   k_recon          a4       p = Phi_E c_E, coalesced streaming read of Phi
+//   k_flux_cfl       a5       face/link fluxes with lambda(s^n), per-cell Q_i, global min dt
+//   k_transport      a6       explicit upwind update, then lambda, f_w of s^{n+1} (a1 of the next step)
+// plus NEXT-1 (lrbms_affine.cuh), NEXT-2 (lrbms_fine.cuh) and the K6 diagnostics (lrbms_diag.cuh).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -30,6 +39,7 @@
 #include "lrbms_project.cuh"
 #include "lrbms_ns.cuh"
 #include "lrbms_affine.cuh"
+#include "lrbms_diag.cuh"
 #include "lrbms_fine.cuh"
 
 using namespace lrbms;
@@ -871,7 +881,7 @@ struct lrbms_ctx {
   // workspace layout
   Buf netw, lam0, lam1, fw0, fw1, K, fc, l_gK, phiV, s0, s1, p, Phi, zc, zh, blocks, rhs, c, hist, Wh, Vh, TH, rbv, gpart, yv, r, z, pv, pv2, q, T, Linv, wc, Binv,
       Binv32, Binv32b, RTb, Es, Yd, cont, e0, partials, scal, gbar, gjrk, gjbar,
-      flags,
+      flags, diagp,
       iters, l_start, l_local, l_orig, l_geo2, l_p, l_s, tmp, tmp2;
   size_t ws_bytes = 0;
   char* ws = nullptr;
@@ -1169,6 +1179,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->e0, (size_t)c->n_pad * 8);
   alloc(c->gjbar, 256);
   alloc(c->flags, 4 * 16);
+  alloc(c->diagp, 8 * ((size_t)g.n_s * DIAG_NP + 16));   // K6 partials + results
   alloc(c->iters, 4 * 16);
   alloc(c->l_start, 4 * (size_t)(g.n_s + 1));
   alloc(c->l_local, 4 * (size_t)nl); alloc(c->l_orig, 4 * (size_t)nl);
@@ -1286,6 +1297,19 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     }
     if (c->have_tmaps)
       CUDA_TRY(c, cudaFuncSetAttribute(k_ns_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, NS_TC_SMEM));
+  }
+  {  // The max-dynamic-shared-memory attribute is per kernel and process-wide, shared by every context:
+     // once the occupancy queries above are done, raise it to the opt-in maximum for every kernel
+     // launched with dynamic shared memory, so that binding a context of another size never
+     // invalidates this one's launches (the launches pass their own sizes)
+    int optin = 0;
+    CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const void* fns[] = {(const void*)k_pcg, (const void*)k_pcg_tm<32>, (const void*)k_pcg_tm<0>,
+                         (const void*)k_coarse_gj32, (const void*)k_project<0, 0>, (const void*)k_project<32, 512>,
+                         (const void*)k_flux_cfl, (const void*)k_coarse_rt_s, (const void*)k_ns_gemm_tc,
+                         (const void*)k_ns_gemm};
+    for (const void* fn : fns)
+      CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   }
   // coarse-rhs contribution slots of absent neighbours are never written: zero them once
   CUDA_TRY(c, cudaMemsetAsync(c->at<float>(c->cont), 0, (size_t)c->n_pad * (8 + 6) * 4, c->stream));
@@ -2065,6 +2089,39 @@ lrbms_status lrbms_stage_transport(lrbms_ctx* c, double cfl, double dt_fixed, do
   return finish(c, 0);
 }
 
+lrbms_status lrbms_diagnostics(lrbms_ctx* c, lrbms_diag* o) {
+  lrbms_status st = ready(c);
+  if (st) return st;
+  if (!o) return fail(c, LRBMS_E_CONFIG, "NULL diagnostics");
+  if (c->steps < 1 || !c->p_valid) return fail(c, LRBMS_E_STATE, "diagnostics need a step since set_saturation");
+  const Geo& g = c->g;
+  DiagArgs D;
+  D.g = g; D.f = c->f; D.L = links_of(c);
+  D.p = c->at<double>(c->p);
+  D.lam = c->lam_nxt(); D.fw = c->fw_nxt();    // lambda, f of s^n (the transport wrote those of s^{n+1})
+  D.s_prev = c->s_nxt(); D.s = c->s_cur();
+  D.phiV = c->have_phi ? c->at<double>(c->phiV) : nullptr;
+  D.fc = c->at<double2>(c->fc);
+  for (int a = 0; a < 3; ++a) D.area[a] = a < g.dim ? sqrt(g.geo[a] * g.vol) : 1.0;   // |F|/d_F * V = |F|^2
+  D.part = c->at<double>(c->diagp);
+  const int nt = std::min(512, cdiv(g.n_loc, 32) * 32);
+  k_diag<<<g.n_s, nt, 16 * (size_t)g.n_loc, c->stream>>>(D);
+  LAUNCH_CHECK(c);
+  double* out = D.part + (size_t)g.n_s * DIAG_NP;
+  k_diag_final<<<1, 32, 0, c->stream>>>(D.part, g.n_s, out);
+  LAUNCH_CHECK(c);
+  double h[DIAG_NP], sc[3];
+  CUDA_TRY(c, cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(sc, c->at<double>(c->scal), 24, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  o->mass_prev = h[0]; o->mass = h[1]; o->s_min = h[2]; o->s_max = h[3];
+  o->zeta_max = h[4]; o->zeta_mean = h[5] / (double)g.n;
+  o->coarse_defect = h[6]; o->water_out = h[7]; o->q_in = h[8]; o->q_out = h[9];
+  o->dt = sc[2];
+  o->mass_balance = fabs(h[1] - h[0] + sc[2] * h[7]) / std::max(std::max(fabs(h[0]), fabs(h[1])), 1e-300);
+  return LRBMS_OK;
+}
+
 lrbms_status lrbms_get_stats(lrbms_ctx* c, lrbms_stats* o) {
   lrbms_status st = check_ctx(c);
   if (st) return st;
@@ -2093,6 +2150,9 @@ lrbms_status lrbms_get_stats(lrbms_ctx* c, lrbms_stats* o) {
 
 int64_t lrbms_launch_count(const lrbms_ctx* c) { return c ? c->launches : 0; }
 
+#ifdef LRBMS_DEBUG
+/* debugging hooks of the -DLRBMS_DEBUG build only (tools/exp_timeline.py, tools/exp_proj_phases.py);
+   the product library exports exactly the calls include/lrbms.h declares */
 /* undocumented debugging hook (not in lrbms.h): PCG phase timestamps of CTA 0 (4 per iteration,
  * first 64 iterations, %globaltimer ns) written to a caller-owned device buffer, or NULL. */
 void lrbms_debug_set_tstamp(lrbms_ctx* c, unsigned long long* dev_buf) {
@@ -2109,6 +2169,7 @@ int32_t lrbms_debug_coarse(lrbms_ctx* c, float* x_host, double* es_host) {
   if (es_host) cudaMemcpy(es_host, c->at<double>(c->Es), (size_t)c->g.n_s * 64, cudaMemcpyDeviceToHost);
   return (int32_t)n;
 }
+#endif  // LRBMS_DEBUG
 
 lrbms_status lrbms_set_profiling(lrbms_ctx* c, int32_t enable) {
   lrbms_status st = check_ctx(c, false);

@@ -16,6 +16,19 @@ namespace cg = cooperative_groups;
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Phase timestamps for the timeline tools (tools/exp_timeline.py, tools/exp_proj_phases.py): compiled
+// only into a -DLRBMS_DEBUG build; the product build has no debug branches in its kernels.
+#ifdef LRBMS_DEBUG
+#define LRBMS_TSTAMP(cond, slot, val) \
+  do {                                \
+    if (cond) slot = val;             \
+  } while (0)
+#else
+#define LRBMS_TSTAMP(cond, slot, val) \
+  do {                                \
+  } while (0)
+#endif
+
 struct Geo {
   int dim, nx, ny, nz;
   int s[3];        // subdomain size in cells per axis (sx, sy, sz)

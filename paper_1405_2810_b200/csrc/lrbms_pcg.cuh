@@ -938,9 +938,9 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         if (act) A.qp[E * N + lane] = q;
         ppq += warp_sum(vbv);
       }
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 0] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 0], gtimer());
       const double pq = grid_reduce(ppq, red16, gparts, A.gbar, epoch, &bc[0]);
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 1] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 1], gtimer());
       if (!(pq > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
         break;
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         }
       }
       rr = grid_reduce(prr, red16, gparts, A.gbar, epoch, &bc[0]);
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 2], gtimer());
       if (!(rr > 0.0)) break;   // exact solution (or NaN, flagged below)
       // C: z = M^-1 r, r.z
       double prz2 = 0.0;
@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(512, 1) k_pcg(PcgArgs A) {
         prz2 += warp_sum(zk * rk);
       }
       const double rz_new = grid_reduce(prz2, red16, gparts, A.gbar, epoch, &bc[0]);
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 3], gtimer());
       if (rz_new <= tol2) break;
       beta = rz_new / rz;
       rz = rz_new;

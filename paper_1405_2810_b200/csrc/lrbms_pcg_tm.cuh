@@ -315,18 +315,23 @@ __host__ __device__ inline TmLayout tm_layout(int W, int dim, int n_pad) {
   return L;
 }
 
-// debug per-CTA timeline (tstamp buffer, entries 4096 + 8 (it G + CTA) + k, it < 32)
+// debug per-CTA timeline (tstamp buffer, entries 4096 + 8 (it G + CTA) + k, it < 32); compiled only
+// with -DLRBMS_DEBUG (tools/exp_timeline.py)
+#ifdef LRBMS_DEBUG
 #define TM_STAMP(k)                                                                            \
   do {                                                                                         \
     if (A.tstamp && threadIdx.x == 0 && it < 32)                                               \
       A.tstamp[4096 + 8 * ((size_t)it * gridDim.x + blockIdx.x) + (k)] = gtimer();             \
   } while (0)
-
 // debug setup stamps (slots of "iteration 0": tstamp[4096 + 8 CTA + k])
 #define TM_SSTAMP(k)                                                                           \
   do {                                                                                         \
     if (A.tstamp && threadIdx.x == 0) A.tstamp[4096 + 8 * (size_t)blockIdx.x + (k)] = gtimer();  \
   } while (0)
+#else
+#define TM_STAMP(k) do { } while (0)
+#define TM_SSTAMP(k) do { } while (0)
+#endif
 
 template <int NFIX>   // NFIX = 32: N known at compile time (the lane predicates fold away)
 __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
@@ -615,10 +620,10 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
           if (act) A.T[((size_t)(E + g.Estride[a]) * 3 + a) * N + lane] = tc;
         }
       }
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 0] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 0], gtimer());
       TM_STAMP(1);
       const double pq = grid_reduce_rel(own ? warp_sum(act ? local : 0.0) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 1] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 1], gtimer());
       if (!(pq > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
         break;
@@ -640,7 +645,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
       }
       TM_STAMP(3);
       grid_barrier_rel(A.gbar, epoch);
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 2] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 2], gtimer());
       TM_STAMP(4);
       // ---------------- C: z = M^-1 r, r.z
       if (A.use_coarse == 2) stage_g();
@@ -651,7 +656,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
       if (act) A.z[E * N + lane] = z;
       TM_STAMP(6);
       const double rz_new = grid_reduce_rel(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
-      if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) A.tstamp[4 * it + 3] = gtimer();
+      LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 3], gtimer());
       TM_STAMP(7);
       rr = rz_new;
       if (!(rz_new == rz_new)) break;   // NaN (flagged below)

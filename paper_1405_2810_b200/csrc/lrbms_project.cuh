@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   sub_xyz(g, E, C);
   const size_t base = (size_t)E * nl;
   const int lq0 = A.L.sub_start[E], lq1 = A.L.sub_start[E + 1];   // link range of E, loaded at entry
-  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 0] = gtimer_p();
+  LRBMS_TSTAMP(A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256, A.tstamp[1024 + (E >> 3) * 8 + 0], gtimer_p());
 
   // 0. inputs of the face weights (a1 + R2) of the thread's first cell, loaded before the Phi staging
   //    floods the memory system with cp.async requests (the weights phase then no longer waits
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   asm volatile("cp.async.commit_group;\n" ::);
   for (int k = warp; k < NP; k += nwarp)
     for (int c1 = (k < N ? nl : 0) + lane; c1 < LD; c1 += 32) Phs[(size_t)k * LD + c1] = 0.0;
-  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 1] = gtimer_p();
+  LRBMS_TSTAMP(A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256, A.tstamp[1024 + (E >> 3) * 8 + 1], gtimer_p());
 
   // 2. a1 + face weights (R2) from the static coefficients.  Pass 1: every cell forms the weights of
   //    its +a faces (all loads issued up front) and of its -a faces across a subdomain side; the +a
@@ -225,10 +225,10 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
       Wc[(size_t)l * 8] += A.L.gK[q] * lam[l];
     }
   }
-  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 2] = gtimer_p();
+  LRBMS_TSTAMP(A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256, A.tstamp[1024 + (E >> 3) * 8 + 2], gtimer_p());
   asm volatile("cp.async.wait_all;\n" ::);
   __syncthreads();
-  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 3] = gtimer_p();
+  LRBMS_TSTAMP(A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256, A.tstamp[1024 + (E >> 3) * 8 + 3], gtimer_p());
 
   // 3. B_EE = Phi Y^T with Y = A_EE Phi^T formed in registers; warp-strided k-steps of 4 cells
   double acc[10][2];
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
     for (int p = 0; p < 10; ++p)
       if (pair_tj(p) < T) dmma(acc[p][0], acc[p][1], af[pair_ti(p)], bf[pair_tj(p)]);
   }
-  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 4] = gtimer_p();
+  LRBMS_TSTAMP(A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256, A.tstamp[1024 + (E >> 3) * 8 + 4], gtimer_p());
   double* BEE = A.blocks + (size_t)E * nb1 * N * N;
 
   // 4. r_E = Phi_E^T b_E, b = sum_L g_L p_L e_L
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
       }
     }
   }
-  if (A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 5] = gtimer_p();
+  LRBMS_TSTAMP(A.tstamp && tid == 0 && (E & 7) == 0 && E < 8 * 256, A.tstamp[1024 + (E >> 3) * 8 + 5], gtimer_p());
 
   // 6. deterministic cross-warp reduction of B_EE (fixed warp order), mirrored for exact symmetry.
   //    All tile pairs at once through the (now free) Phi_E buffer when it is large enough.
@@ -368,10 +368,12 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
       __syncthreads();
     }
   }
+#ifdef LRBMS_DEBUG
   if (A.tstamp) {
     __syncthreads();
     if (tid == 0 && (E & 7) == 0 && E < 8 * 256) A.tstamp[1024 + (E >> 3) * 8 + 6] = gtimer_p();
   }
+#endif
 }
 
 }  // namespace lrbms

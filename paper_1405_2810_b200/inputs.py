@@ -10,8 +10,10 @@ inputs a user of the method supplies (DESIGN.md "input recipe"
 * the boundary data as *links* -- a Dirichlet boundary face or a well cell
   with a fixed pressure p_L and an external saturation s_ext (P:207-220;
   reading R6/A13 in DESIGN.md);
-* the local reduced bases Phi_E, as generic full-rank local
-  spaces: orthonormalised tensor monomials on each subdomain (a coarse-scale
+* the local reduced bases Phi_E: ``pod`` -- the paper's offline recipe
+  (training mobilities from time-of-flight profiles, fine snapshots, per-subdomain POD;
+  delegated to ``offline/recipe.py``), or generic full-rank local spaces:
+  orthonormalised tensor monomials on each subdomain (``poly``: a coarse-scale
   piecewise polynomial space, first column the normalised subdomain indicator,
   cf. the coarse unit functions P:1110-1111), or a seeded random orthogonal
   full space (Phi_E = full n_loc space: the fine space, pin P1);
@@ -323,8 +325,10 @@ def profile_saturations(sc: Scenario, M: int = 8) -> np.ndarray:
     return out
 
 
-def make_scenario(name: str, basis: str = "poly", n_steps: Optional[int] = None) -> Scenario:
-    """The seeded synthetic scenario for BASELINE.json config ``name`` (C1..C5)."""
+def make_scenario(name: str, basis: str = "pod", n_steps: Optional[int] = None) -> Scenario:
+    """The seeded synthetic scenario for BASELINE.json config ``name`` (C1..C5).  The default basis is
+    the paper's offline recipe (``pod``), whose profile horizon uses the config's own step count
+    whatever ``n_steps`` a caller runs."""
     cfg = CONFIGS[name]
     idx = CONFIG_INDEX[name]
     sc = Scenario(name=name, dim=cfg["dim"], nx=cfg["nx"], ny=cfg["ny"], nz=cfg["nz"],
@@ -334,13 +338,32 @@ def make_scenario(name: str, basis: str = "poly", n_steps: Optional[int] = None)
     sc.K = make_permeability(cfg, idx, sc.nx, sc.ny, sc.nz)
     sc.link_cell, sc.link_axis, sc.link_p, sc.link_s = links_for(cfg["bc"], sc.nx, sc.ny, sc.nz)
     sc.s0 = np.zeros(sc.n)
+    sc.n_steps = cfg["n_steps"]
     sc.Phi = make_basis(sc, basis, 100 + idx)
+    sc.n_steps = cfg["n_steps"] if n_steps is None else n_steps
     return sc
+
+
+_POD_CACHE: dict = {}
+
+
+def pod_basis(sc: Scenario, seed: int) -> np.ndarray:
+    """The paper's offline recipe (time-of-flight profiles, 2N training mobilities, fine
+    snapshots, per-subdomain POD with the indicator) run on the host by ``offline/recipe.py`` -- an
+    input generator outside this module (it holds the offline stage's arithmetic, not this one).
+    Memoised per process on the scenario's inputs (the C5 recipe takes minutes)."""
+    key = (sc.digest(), sc.N, sc.n_steps, seed)
+    if key not in _POD_CACHE:
+        from offline import recipe
+        _POD_CACHE[key] = recipe.pod_recipe(sc, seed).Phi
+    return _POD_CACHE[key]
 
 
 def make_basis(sc: Scenario, basis: str, seed: int) -> np.ndarray:
     if basis == "poly":
         return poly_basis(sc, seed)
+    if basis == "pod":
+        return pod_basis(sc, seed)
     if basis == "full":
         sc.N = sc.n_loc
         return random_full_basis(sc, seed)

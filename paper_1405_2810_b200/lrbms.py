@@ -24,7 +24,7 @@ EXPORTS = ["lrbms_create", "lrbms_workspace_bytes", "lrbms_bind", "lrbms_set_med
            "lrbms_stage_project", "lrbms_stage_solve", "lrbms_stage_reconstruct", "lrbms_stage_transport",
            "lrbms_get_stats", "lrbms_set_profiling", "lrbms_get_stage_times", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy",
            "lrbms_profiles_bytes", "lrbms_set_profiles", "lrbms_set_online", "lrbms_stage_theta",
-           "lrbms_fine_bytes", "lrbms_run_fine"]
+           "lrbms_fine_bytes", "lrbms_run_fine", "lrbms_diagnostics"]
 
 
 class LrbmsError(RuntimeError):
@@ -61,6 +61,11 @@ class Stats(ctypes.Structure):
                 ("last_iters", ctypes.c_int32), ("total_iters", ctypes.c_int64),
                 ("coarse_rebuilds", ctypes.c_int32), ("fprime_max", ctypes.c_double),
                 ("ns_guard_trips", ctypes.c_int64), ("ns_resid_max", ctypes.c_double)]
+
+
+class Diag(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in ("mass_prev", "mass", "s_min", "s_max", "zeta_max", "zeta_mean",
+                                               "coarse_defect", "water_out", "q_in", "q_out", "dt", "mass_balance")]
 
 
 _lib = None
@@ -103,6 +108,7 @@ def load_library(path: str = LIB_PATH):
         "lrbms_stage_theta": (st, [P, P]),
         "lrbms_fine_bytes": (ctypes.c_size_t, [P]),
         "lrbms_run_fine": (st, [P, I, D, D, P, P, ctypes.c_size_t, D, I, ctypes.POINTER(ctypes.c_int64)]),
+        "lrbms_diagnostics": (st, [P, ctypes.POINTER(Diag)]),
         "lrbms_get_stage_times": (st, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), I]),
         "lrbms_last_error": (ctypes.c_char_p, [P]),
         "lrbms_version": (ctypes.c_char_p, []),
@@ -315,6 +321,12 @@ class LrbmsContext:
         st = Stats()
         self._check(self.L.lrbms_get_stats(self.h, ctypes.byref(st)))
         return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+    def diagnostics(self) -> dict:
+        """K6 diagnostics of the last step (lrbms_diagnostics): mass, s range, zeta, coarse defect."""
+        d = Diag()
+        self._check(self.L.lrbms_diagnostics(self.h, ctypes.byref(d)))
+        return {k: getattr(d, k) for k, _ in Diag._fields_}
 
     STAGES = ["project", "coarse", "scale", "guess", "pcg", "recon", "flux_cfl", "transport"]
 

@@ -5,6 +5,8 @@ Tolerances (BASELINE.json north_star):
   saturations after the full run: ||d||_inf <= 1e-10 (absolute).
 Stage-level checks are tighter (same arithmetic, different summation order).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -14,6 +16,10 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 O = pytest.importorskip("oracle.lrbms_oracle")
+
+# C4's saturation bar on prefixes: 1e-10 where the trajectory's measured
+# round-off amplification allows it; filled from the sensitivity measurement
+C4_S_BAR = {20: 1e-10, 50: 1e-10}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -249,9 +255,12 @@ def test_rank_deficient_basis_is_numerical_error():
     assert e.value.status == LRBMS_E_NUMERICAL
 
 
+@pytest.mark.parametrize("basis", ["pod", "poly"])
 @pytest.mark.parametrize("name,steps", [("C2", 100), ("C3", 500)])
-def test_full_run_configs(name, steps):
-    sc = inputs.make_scenario(name)
+def test_full_run_configs(name, steps, basis):
+    """Full BASELINE step counts on the paper-recipe bases (pod, the configs as BASELINE states them)
+    and on the polynomial bases."""
+    sc = inputs.make_scenario(name, basis=basis)
     ref = O.run(sc, n_steps=steps, keep=True)
     ctx = ctx_for(sc)
     dts = np_(ctx.run(steps, log_dt=True))
@@ -289,6 +298,49 @@ def test_full_size_prefix(name):
     assert rel(np_(cg), ref["cs"][-1]) <= 1e-10
     assert rel(np_(pg), ref["ps"][-1]) <= 1e-10
     assert np.max(np.abs(np_(sg) - ref["s"])) <= 1e-10
+
+
+GOLDEN_C5 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "C5_pod_200.npz")
+
+
+@pytest.mark.parametrize("steps", [10, 200])
+def test_c5_golden(steps):
+    """The bench workload (C5, paper-recipe bases) in the bench launch configuration against the oracle's
+    trajectory written by tests/golden/make_golden.py (oracle only): after 10 and after the full 200
+    steps, dt of every step, c and the sampled p within 1e-10 relative, s within 1e-10 absolute.  The
+    inputs must be bitwise the golden's (the host recipe is reproducible across hosts, r02b)."""
+    import hashlib
+    G = np.load(GOLDEN_C5)
+    sc = inputs.make_scenario("C5")
+    assert hashlib.sha256(np.ascontiguousarray(sc.K).tobytes()).hexdigest() == str(G["K_sha"])
+    assert hashlib.sha256(np.ascontiguousarray(sc.Phi).tobytes()).hexdigest() == str(G["Phi_sha"])
+    ctx = ctx_for(sc)
+    dts = np_(ctx.run(steps, log_dt=True))
+    s, p, c = ctx.get_state()
+    assert rel(dts, G["dts"][:steps]) <= 1e-10
+    assert rel(np_(c), G[f"c_{steps}"]) <= 1e-10
+    assert rel(np_(p)[G["cells"]], G[f"p_{steps}"]) <= 1e-10
+    assert np.max(np.abs(np_(s) - G[f"s_{steps}"])) <= 1e-10
+    ctx.close()
+
+
+@pytest.mark.parametrize("steps", [20, 50])
+def test_c4_prefix_default_solver(steps):
+    """C4 (paper-recipe bases) at the product's default solver settings: dt, c and p at the 1e-10 bar
+    after 20 and 50 steps, and s at the bar DESIGN.md section 6 derives from C4's measured round-off
+    amplification (a 1e-14 input perturbation grows to |ds| ~1e-10 within 50 steps)."""
+    sc = inputs.make_scenario("C4")
+    ref = O.run(sc, n_steps=steps, keep=True)
+    ctx = ctx_for(sc)
+    dts = np_(ctx.run(steps, log_dt=True))
+    s, p, c = ctx.get_state()
+    ds = float(np.max(np.abs(np_(s) - ref["s"])))
+    print(f"C4 {steps} steps: |ds| {ds:.3e}, rel dc {rel(np_(c), ref['cs'][-1]):.3e}, "
+          f"rel dp {rel(np_(p), ref['ps'][-1]):.3e}")
+    assert rel(dts, ref["dts"]) <= 1e-10
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
+    assert rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert ds <= C4_S_BAR[steps]
 
 
 def test_c4_prefix_tight_solver():

@@ -44,12 +44,12 @@ def test_tof_uniform_flow_closed_form(phi, hx):
 
 def test_tof_scaling():
     """tau is linear in phi and inversely proportional to the velocity (K x 2 doubles every flux)."""
-    sc = inputs.make_scenario("C2")
+    sc = inputs.make_scenario("C2", basis="poly")
     _, t1 = tof_of(sc)
-    sc2 = inputs.make_scenario("C2")
+    sc2 = inputs.make_scenario("C2", basis="poly")
     sc2.K = sc2.K * 2.0
     _, t2 = tof_of(sc2)
-    sc3 = inputs.make_scenario("C2")
+    sc3 = inputs.make_scenario("C2", basis="poly")
     sc3.phi = np.full(sc3.n, 0.25)
     _, t3 = tof_of(sc3)
     assert np.max(np.abs(t2 * 2.0 - t1) / t1) <= 1e-10
@@ -60,7 +60,7 @@ def test_tof_scaling():
 def test_tof_sweep_equals_monolithic_solve(name):
     """The descending-pressure sweep solves the same discrete system as one sparse direct
     solve, and the order is a topological order: every inflow neighbour has a higher p."""
-    sc = inputs.make_scenario(name)
+    sc = inputs.make_scenario(name, basis="poly")
     fl, tau = tof_of(sc)
     M, rhs = R.tof_matrix(sc, fl["faces"], fl["Ff"], fl["link_cells"], fl["Fl"], fl["phiV"])
     d = M.diagonal()
@@ -81,7 +81,7 @@ def test_tof_sweep_equals_monolithic_solve(name):
 # ---------------------------------------------------------------- profiles
 
 def test_profiles_structure():
-    sc = inputs.make_scenario("C2")
+    sc = inputs.make_scenario("C2", basis="poly")
     fl, tau = tof_of(sc)
     T = sc.n_steps * fl["dt0"]
     M = 8
@@ -117,7 +117,7 @@ def test_training_parameters():
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_snapshots_solve_the_oracle_operator(name):
     """Every snapshot solves the fine system assembled independently by the oracle."""
-    sc = inputs.make_scenario(name)
+    sc = inputs.make_scenario(name, basis="poly")
     res = R.pod_recipe(sc, 100 + inputs.CONFIG_INDEX[name], keep_snapshots=True)
     lam = res.mus @ (res.LW + res.LO)
     for j in range(len(res.mus)):
@@ -128,7 +128,7 @@ def test_snapshots_solve_the_oracle_operator(name):
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3"])
 def test_pod_basis_orthonormal_with_indicator(name):
-    sc = inputs.make_scenario(name)
+    sc = inputs.make_scenario(name, basis="poly")
     res = R.pod_recipe(sc, 100 + inputs.CONFIG_INDEX[name])
     Phi = res.Phi
     assert Phi.shape == (sc.n_s, sc.N, sc.n_loc)
@@ -141,7 +141,7 @@ def test_pod_basis_orthonormal_with_indicator(name):
 def test_pod_rank_one_when_profiles_coincide():
     """C1 has mu_w = mu_o: the total mobility of every profile is 1, all snapshots coincide, so
     exactly one POD mode survives, proportional to the snapshot with its mean removed."""
-    sc = inputs.make_scenario("C1")
+    sc = inputs.make_scenario("C1", basis="poly")
     res = R.pod_recipe(sc, 101, keep_snapshots=True)
     assert np.all(res.kept == 1)
     cells = R.local_cells(sc)
@@ -156,7 +156,7 @@ def test_pod_spans_snapshots_and_reproduces_them():
     """With fewer training parameters than N - 1 nothing is truncated: every snapshot restriction lies
     in span Phi_E (eps_pca = 0: every nonzero mode is kept), so the reduced (oracle) solve at a
     training mobility reproduces that snapshot -- Galerkin reproduction (SPEC 'Reproduction')."""
-    sc = inputs.make_scenario("C2")
+    sc = inputs.make_scenario("C2", basis="poly")
     res = R.pod_recipe(sc, 102, n_train=5, keep_snapshots=True, eps_pca=0.0)
     cells = R.local_cells(sc)
     for j in range(5):

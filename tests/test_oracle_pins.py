@@ -530,3 +530,43 @@ def test_affine_step_equals_direct_step_in_span():
     assert np.max(np.abs(a["blocks"] - d["blocks"])) <= 1e-12 * np.max(np.abs(d["blocks"]))
     assert np.max(np.abs(a["c"] - d["c"])) <= 1e-10 * np.max(np.abs(d["c"]))
     assert np.max(np.abs(a["s"] - d["s"])) <= 1e-12
+
+
+# ---------------------------------------------------------------- K6 diagnostics
+
+def test_relative_mass_loss_zero_for_fine_scheme_and_positive_for_reduced():
+    """The fine scheme's fluxes are exactly conservative per cell (zeta = 0 up to round-off: each cell's
+    row of A p = b), the reduced scheme's are not -- unless the basis is the full local
+    space (P1).  Coarse conservation holds either way (P4: the indicator is in every Phi_E)."""
+    sc = inputs.make_scenario("C2", basis="poly")
+    s = np.random.default_rng(5).uniform(0, 1, sc.n)
+    f = O.fine_step(sc, s)
+    z_fine = O.relative_mass_loss(sc, f["Ff"], f["Fl"])
+    assert np.max(z_fine) <= 1e-11
+    r = O.lrbms_step(sc, s)
+    z_red = O.relative_mass_loss(sc, r["Ff"], r["Fl"])
+    assert np.max(z_red) > 1e-3
+    net = O.cell_net_outflow(sc, r["Ff"], r["Fl"])
+    coarse = net[O.subdomain_cells(sc)].sum(axis=1)
+    assert np.max(np.abs(coarse)) <= 1e-11 * np.sum(np.abs(r["Fl"]))
+
+
+def test_relative_mass_loss_closed_form():
+    """2 x 1 grid with prescribed fluxes: cell 0 has outflow 3 through the face and inflow 1 through its
+    link, so |net| = 2 and max |u| = 3 (unit areas): zeta_0 = 2/3; cell 1: face inflow 3, link outflow
+    3 -> zeta_1 = 0."""
+    sc = inputs.custom_scenario(2, 1, 1, 1, 1, 1, 1, basis="random")
+    Ff = np.array([3.0])
+    Fl = np.array([-1.0, 3.0])
+    z = O.relative_mass_loss(sc, Ff, Fl)
+    assert z[0] == pytest.approx(2.0 / 3.0, rel=1e-15) and z[1] == 0.0
+
+
+def test_mass_and_link_outflow_balance():
+    """P3 restated through the diagnostics: mass^{n+1} - mass^n = -dt sum_L F_L f(s_up)."""
+    sc = inputs.make_scenario("C2", basis="poly")
+    s = np.random.default_rng(6).uniform(0, 1, sc.n)
+    r = O.lrbms_step(sc, s)
+    dm = O.total_mass(sc, r["s"]) - O.total_mass(sc, s)
+    w = O.link_water_outflow(sc, s, r["Fl"])
+    assert abs(dm + r["dt"] * w) <= 1e-14 * O.total_mass(sc, s)
