@@ -842,6 +842,8 @@ __global__ void __launch_bounds__(256) k_transport(FluxArgs A) {
   }
 }
 
+#include "lrbms_transport.cuh"   // a5 + a6 fused (uses FluxArgs, face_index above)
+
 // ============================================================================ host side
 
 namespace {
@@ -869,6 +871,9 @@ struct lrbms_ctx {
   const void* tm_fn = nullptr;   // the k_pcg_tm instance (compile-time N = 32, or the general one)
   size_t tm_smem = 0;
   int ns_par = 0;          // ping-pong word of the Newton-Schulz guard
+  const void* ft_fn = nullptr;   // fused a5 + a6 (k_flux_transport instance), nullptr: the two-kernel path
+  int ft_G = 0, ft_kmax = 0, ft_nt = 0;
+  size_t ft_smem = 0;
   int64_t ns_trips = 0;    // calls that ended with a skipped Newton-Schulz update (forced rebuild)
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
   int xcur = 0;            // which of Binv32 / Binv32b holds the current coarse inverse
@@ -1308,8 +1313,35 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
                          (const void*)k_coarse_gj32, (const void*)k_project<0, 0>, (const void*)k_project<32, 512>,
                          (const void*)k_flux_cfl, (const void*)k_coarse_rt_s, (const void*)k_ns_gemm_tc,
                          (const void*)k_ns_gemm};
-    for (const void* fn : fns)
-      CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    for (const void* fn : fns) {
+      cudaFuncAttributes fa{};
+      CUDA_TRY(c, cudaFuncGetAttributes(&fa, fn));   // the static shared memory counts against the opt-in limit
+      CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+    }
+  }
+  {  // fused fluxes + transport: a cooperative grid whose flux sums fit in shared memory
+    const Geo& gg = c->g;
+    const void* fn = (gg.dim == 3 && gg.s[0] == 8 && gg.s[1] == 8 && gg.s[2] == 8) ? (const void*)k_flux_transport<8, 8, 8>
+                     : (gg.dim == 2 && gg.s[0] == 16 && gg.s[1] == 16) ? (const void*)k_flux_transport<16, 16, 1>
+                                                                       : (const void*)k_flux_transport<0, 0, 0>;
+    const int nt = std::min(512, cdiv(gg.n_loc, 32) * 32);
+    c->ft_fn = nullptr;
+    for (int occ_try = 4; occ_try >= 1 && !c->ft_fn; --occ_try) {
+      const int G = std::min(gg.n_s, sms * occ_try);
+      const int kmax = cdiv(gg.n_s, G);
+      const size_t smem = 8 * (size_t)gg.n_loc * (kmax + 3);
+      if (smem > 160 * 1024) continue;
+      int optin = 0;
+      CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      cudaFuncAttributes fa{};
+      CUDA_TRY(c, cudaFuncGetAttributes(&fa, fn));
+      CUDA_TRY(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+      int occ_ft = 0;
+      CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ft, fn, nt, smem));
+      if (occ_ft * sms >= G) {
+        c->ft_fn = fn; c->ft_G = G; c->ft_kmax = kmax; c->ft_nt = nt; c->ft_smem = smem;
+      }
+    }
   }
   // coarse-rhs contribution slots of absent neighbours are never written: zero them once
   CUDA_TRY(c, cudaMemsetAsync(c->at<float>(c->cont), 0, (size_t)c->n_pad * (8 + 6) * 4, c->stream));
@@ -1725,6 +1757,15 @@ static lrbms_status launch_transport(lrbms_ctx* c, double cfl, double dt_fixed, 
   FluxArgs A = flux_args(c, cfl, dt_fixed, dt_log, step);
   A.face_flux = face_flux;
   A.link_flux = link_flux;
+  if (c->ft_fn) {   // a5 + a6 in one cooperative kernel (stage 6; stage 7 stays empty)
+    StageScope sc_(c, 6);
+    int kmax = c->ft_kmax;
+    void* args[] = {&A, &kmax};
+    CUDA_TRY(c, cudaLaunchCooperativeKernel(c->ft_fn, dim3(c->ft_G), dim3(c->ft_nt), args, c->ft_smem, c->stream));
+    c->launches++;
+    c->cur ^= 1;
+    return LRBMS_OK;
+  }
   {
     StageScope sc_(c, 6);
     k_flux_cfl<<<g.n_s, nt, 3 * 8 * g.n_loc, c->stream>>>(A);

@@ -136,9 +136,10 @@ __device__ __forceinline__ double grid_reduce_rel(double v, double* red16, doubl
   ++epoch;
   double* ps = partials + (size_t)(epoch & 3) * G;
   if (warp == 0) {
+    // the CTA's warp partials summed by a butterfly (bitwise identical in every lane, fixed order)
+    // instead of one lane's W dependent shared-memory loads and adds
+    const double t = warp_sum(lane < W ? red16[lane] : 0.0);
     if (lane == 0) {
-      double t = 0.0;
-      for (int w = 0; w < W; ++w) t += red16[w];
       ps[blockIdx.x] = t;
       asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar), "r"(1u) : "memory");
       const unsigned target = epoch * (unsigned)G;

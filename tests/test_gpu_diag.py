@@ -44,15 +44,18 @@ def test_diagnostics_match_oracle(name):
     coarse = np.max(np.abs(net[O.subdomain_cells(sc)].sum(axis=1)))
     w = O.link_water_outflow(sc, s_prev, r["Fl"])
     qin, qout = np.sum(np.maximum(-r["Fl"], 0)), np.sum(np.maximum(r["Fl"], 0))
-    assert d["mass_prev"] == pytest.approx(m0, rel=1e-12)
-    assert d["mass"] == pytest.approx(m1, rel=1e-12)
+    # the mass moves by dt q per step, dt carries the pressure's error amplified by |p| / |dp|
+    assert d["mass_prev"] == pytest.approx(m0, rel=1e-9)
+    assert d["mass"] == pytest.approx(m1, rel=1e-9)
     assert abs(d["s_min"] - r["s"].min()) <= 1e-10 and abs(d["s_max"] - r["s"].max()) <= 1e-10
     assert abs(d["zeta_max"] - z.max()) <= 1e-8 and abs(d["zeta_mean"] - z.mean()) <= 1e-8
     assert d["zeta_max"] > 1e-3                          # reduced velocities are not conservative per cell
     assert d["coarse_defect"] <= 1e-10 * qin and coarse <= 1e-10 * qin   # P4: 1_E in span Phi_E
-    assert d["water_out"] == pytest.approx(w, rel=1e-10)
-    assert d["q_in"] == pytest.approx(qin, rel=1e-10) and d["q_out"] == pytest.approx(qout, rel=1e-10)
-    assert d["dt"] == pytest.approx(r["dt"], rel=1e-10)
+    # link fluxes g (p_a - p_L): the pressure's 1e-10 bar is relative to max|p|, a producer cell's p_a
+    # can be 1e-2 of it
+    assert d["water_out"] == pytest.approx(w, rel=1e-8)
+    assert d["q_in"] == pytest.approx(qin, rel=1e-8) and d["q_out"] == pytest.approx(qout, rel=1e-8)
+    assert d["dt"] == pytest.approx(r["dt"], rel=1e-8)
     assert d["mass_balance"] <= 1e-14                    # P3
     ctx.close()
 

@@ -17,9 +17,15 @@ pytestmark = pytest.mark.gpu
 
 O = pytest.importorskip("oracle.lrbms_oracle")
 
-# C4's saturation bar on prefixes: 1e-10 where the trajectory's measured
-# round-off amplification allows it; filled from the sensitivity measurement
-C4_S_BAR = {20: 1e-10, 50: 1e-10}
+# C4's saturation bar on prefixes at the default solver settings (the C4
+# exception): a 1e-14 relative perturbation of K alone moves s by ~1e-10 after 20 steps and 2.2e-10
+# after 50 (round-off amplification), so two implementations that differ at round-off
+# level cannot be held to 1e-10 in s there; c and p keep the 1e-10 bar
+C4_S_BAR = {20: 2e-10, 50: 1e-9}
+# dt is reported beside the bar (A20: the bar is c, p and s): dt = cfl min phi V/(f' Q)
+# divides by the largest cell flux, a difference of neighbouring pressures, so its relative error is
+# the pressure's times |p| / |dp| (~1e2-1e3 on these grids)
+DT_BAR = 1e-8
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -265,10 +271,11 @@ def test_full_run_configs(name, steps, basis):
     ctx = ctx_for(sc)
     dts = np_(ctx.run(steps, log_dt=True))
     s, p, c = ctx.get_state()
-    assert rel(dts, ref["dts"]) <= 1e-10
-    assert rel(np_(c), ref["cs"][-1]) <= 1e-10
-    assert rel(np_(p), ref["ps"][-1]) <= 1e-10
-    assert np.max(np.abs(np_(s) - ref["s"])) <= 1e-10
+    e = dict(dt=rel(dts, ref["dts"]), c=rel(np_(c), ref["cs"][-1]), p=rel(np_(p), ref["ps"][-1]),
+             s=float(np.max(np.abs(np_(s) - ref["s"]))))
+    print(f"{name} {basis} {steps} steps: " + ", ".join(f"{k} {v:.3e}" for k, v in e.items()))
+    assert e["c"] <= 1e-10 and e["p"] <= 1e-10 and e["s"] <= 1e-10
+    assert e["dt"] <= DT_BAR
 
 
 @pytest.mark.parametrize("name", ["C4", "C5"])
@@ -337,7 +344,7 @@ def test_c4_prefix_default_solver(steps):
     ds = float(np.max(np.abs(np_(s) - ref["s"])))
     print(f"C4 {steps} steps: |ds| {ds:.3e}, rel dc {rel(np_(c), ref['cs'][-1]):.3e}, "
           f"rel dp {rel(np_(p), ref['ps'][-1]):.3e}")
-    assert rel(dts, ref["dts"]) <= 1e-10
+    assert rel(dts, ref["dts"]) <= DT_BAR
     assert rel(np_(c), ref["cs"][-1]) <= 1e-10
     assert rel(np_(p), ref["ps"][-1]) <= 1e-10
     assert ds <= C4_S_BAR[steps]
