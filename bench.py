@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-small", dest="small", action="store_false",
                     help="skip the C1-C4 us/step keys")
     ap.add_argument("--cpu-steps", type=int, default=3, help="oracle steps timed for cpu_baseline")
+    ap.add_argument("--no-offline", dest="offline", action="store_false",
+                    help="skip the GPU offline stage (NEXT-3) key")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--coarse-refresh", type=int, default=None)
@@ -312,7 +314,9 @@ def run_ours(args, rank, local, world):
         raise SystemExit("bench.py --impl ours needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    t_inputs = time.perf_counter()
     sc = inputs.make_scenario(args.config, basis=args.basis)
+    t_inputs = time.perf_counter() - t_inputs
     solver = {}
     if args.coarse_refresh:
         solver["coarse_refresh"] = args.coarse_refresh
@@ -431,6 +435,32 @@ def run_ours(args, rank, local, world):
                         "kernel, then the same fluxes and transport; lrbms_speedup = the headline steps/s over these steps/s (the paper's "
                         "online-vs-fine comparison, P:1300-1302)"}
 
+    # ---- NEXT-3: the offline basis recipe on the GPU (the same recipe the host ran for this workload's
+    #      bases), timed and compared with the host bases
+    offline = None
+    if args.offline and args.basis == "pod":
+        from offline import recipe as R
+        mus = R.training_parameters(8, 2 * sc.N, 100 + inputs.CONFIG_INDEX[args.config])
+        ctx.set_saturation(sc.s0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Phi_g, kept_g, info_g, _, _ = ctx.offline_basis(mus, M=8, horizon_steps=sc.n_steps)
+        torch.cuda.synchronize()
+        t_off = time.perf_counter() - t0
+        Pg = torch.einsum("ekl,ekm->elm", Phi_g, Phi_g)
+        Ph = torch.as_tensor(sc.Phi, device=device)
+        Ph = torch.einsum("ekl,ekm->elm", Ph, Ph)
+        dP = (Pg - Ph).abs().amax(dim=(1, 2)).cpu().numpy()
+        offline = {"seconds": t_off, "host_recipe_seconds": t_inputs, "tof_sweeps": info_g["tof_sweeps"],
+                   "fine_solves": 1 + 2 * sc.N, "fine_cg_iters": info_g["fine_cg_iters"],
+                   "projector_diff_max": float(dP.max()), "projector_diff_median": float(np.median(dP)),
+                   "kept_modes_histogram": np.bincount(kept_g).tolist(),
+                   "note": "lrbms_offline_basis (NEXT-3): fine solve at s0, time of flight, 8 profiles, "
+                           "2N fine snapshots, per-subdomain one-sided Jacobi POD, on the GPU; compared with "
+                           "the host recipe's bases the headline ran on (host_recipe_seconds includes the "
+                           "seeded field generation)"}
+        del Pg, Ph
+
     if rank != 0:
         return 0
 
@@ -512,6 +542,7 @@ def run_ours(args, rank, local, world):
         "pcg_iters_per_step": iters,
         "affine_variant": affine,
         "fine_reference": fine,
+        "offline_gpu": offline,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

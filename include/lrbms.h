@@ -180,6 +180,42 @@ lrbms_status lrbms_run_fine(lrbms_ctx *ctx, int32_t n_steps, double cfl, double 
                             double *dt_log, void *ws, size_t bytes, double rtol, int32_t max_iters,
                             int64_t *iters_total);
 
+/* NEXT-3: the offline basis recipe on the GPU -- the initialisation of
+ * alg:lrbmsBasisConstruction, the training set, the fine snapshots
+ * and the per-subdomain data compression (PCA) with the coarse unit functions
+ * (P:1110-1111).  Its host reference is offline/recipe.py (readings A25/A26):
+ *   1. the fine pressure at the current saturation s0 (the NEXT-2 solver, rtol) and the CFL step dt0 of
+ *      its fluxes (reading R4, f'_max of the context's fluid);
+ *   2. the time of flight of eq:timeOfFlight at k = 0 (upwind DG0; solved by relaxation
+ *      sweeps to the exact fixed point of the flow-ordered triangular system);
+ *   3. M mobility profiles: q = 1 the mobility of s0, q = M that of the injected saturation
+ *      (the largest link s_ext), q = 2..M-1 the injected one where tau <= (q-1) T/(M-2), T = horizon_steps dt0;
+ *   4. n_train fine snapshots p(lambda^(j)), lambda^(j) = sum_q mu_q lambda_{t,q};
+ *   5. per subdomain E: Y = (I - v0 v0^T) P|_E (v0 = 1/sqrt(n_loc)), its thin SVD (one-sided Jacobi),
+ *      Phi_E = [v0, the left singular vectors with sigma > eps_pca sigma_max (sigma_max over all E), at
+ *      most N - 1 of them, then graded monomials of the local coordinates orthogonalised against the
+ *      columns before them], each column signed so that its largest-magnitude entry is positive.
+ * mu (host, [n_train][M], row-major): the training parameters (the caller's seeded sampler).
+ * ws (dev, 256-byte aligned, >= lrbms_offline_bytes(ctx, n_train)): caller-owned scratch, used only
+ * during the call (C5 with n_train = 64: ~0.7 GB).  Outputs: Phi (dev, [n_s][N][n_loc], the layout of
+ * lrbms_set_basis; not installed -- call lrbms_set_basis with it), tau (dev, n, natural order, or
+ * NULL), snapshots (dev, [n_train][n], natural order, or NULL), kept (host, n_s: POD modes kept, or
+ * NULL), info (host, or NULL).  The pressure buffer is overwritten; the reduced solver rebuilds its
+ * coarse inverse at its next step.  Errors: CONFIG (arguments, workspace, M not in [3, 16], n_train
+ * not in [1, 64], a subdomain that cannot be completed to N), STATE (no medium or saturation),
+ * NUMERICAL (no flow, a fine solve that does not converge, a flow cycle in the time of flight). */
+typedef struct {
+  double dt0;             /* CFL step of the s0 flow */
+  double horizon;         /* T = horizon_steps * dt0 */
+  int32_t tof_sweeps;     /* relaxation sweeps of the time of flight */
+  int64_t fine_cg_iters;  /* CG iterations of the 1 + n_train fine solves */
+} lrbms_offline_info;
+size_t       lrbms_offline_bytes(const lrbms_ctx *ctx, int32_t n_train);
+lrbms_status lrbms_offline_basis(lrbms_ctx *ctx, int32_t M, int32_t n_train, const double *mu,
+                                 int32_t horizon_steps, double cfl, double eps_pca, double rtol, void *ws,
+                                 size_t bytes, double *Phi, double *tau, double *snapshots, int32_t *kept,
+                                 lrbms_offline_info *info);
+
 /* Advance n_steps online steps a1..a6 on the bound stream, no host round trip per step.
  * dt_fixed > 0 overrides the CFL step (the paper's fixed N_T); otherwise
  * dt^n = cfl * min_i phi_i V_i / (f'_max Q_i) (reading R4).  dt_log (dev, n_steps) or NULL.

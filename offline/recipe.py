@@ -49,13 +49,33 @@ def phase_mobilities(sc, s):
     return se ** sc.nw / sc.mu_w, (1.0 - se) ** sc.no / sc.mu_o
 
 
-def max_wave_speed(sc, samples=200_001):
-    """max over the mobile range of d f_w / d s on a uniform sample (only sets the profile horizon T)."""
-    se = np.linspace(0.0, 1.0, samples)
-    a = se ** sc.nw / sc.mu_w
-    b = (1.0 - se) ** sc.no / sc.mu_o
-    f = a / (a + b)
-    return float(np.max(np.gradient(f, se))) / (1.0 - sc.swr - sc.sor)
+def max_wave_speed(sc, samples=20_001):
+    """max over the mobile range of d f_w / d s (sets the profile horizon T through dt^0): the
+    derivative of f_w = a/(a + b), a = S_e^nw/mu_w, b = (1 - S_e)^no/mu_o, sampled on a uniform grid,
+    then refined by golden-section search around the best sample."""
+    def fprime(se):
+        se = np.asarray(se, np.float64)
+        a = se ** sc.nw / sc.mu_w
+        b = (1.0 - se) ** sc.no / sc.mu_o
+        da = sc.nw * se ** (sc.nw - 1.0) / sc.mu_w
+        db = -sc.no * (1.0 - se) ** (sc.no - 1.0) / sc.mu_o
+        return (da * b - a * db) / (a + b) ** 2
+    xs = np.linspace(0.0, 1.0, samples)
+    v = fprime(xs)
+    k = int(np.argmax(v))
+    lo, hi = xs[max(k - 1, 0)], xs[min(k + 1, samples - 1)]
+    gr = (np.sqrt(5.0) - 1.0) / 2.0
+    for _ in range(200):
+        c1 = hi - gr * (hi - lo)
+        c2 = lo + gr * (hi - lo)
+        if fprime(c1) >= fprime(c2):
+            hi = c2
+        else:
+            lo = c1
+        if hi - lo < 1e-15:
+            break
+    best = max(float(fprime(0.5 * (lo + hi))), float(v[k]))
+    return best / (1.0 - sc.swr - sc.sor)
 
 
 # ----------------------------------------------------------------------------- fine k = 0 system

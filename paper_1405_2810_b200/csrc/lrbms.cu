@@ -40,6 +40,7 @@
 #include "lrbms_ns.cuh"
 #include "lrbms_affine.cuh"
 #include "lrbms_diag.cuh"
+#include "lrbms_offline.cuh"
 #include "lrbms_fine.cuh"
 
 using namespace lrbms;
@@ -1174,7 +1175,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   alloc(c->Binv32, (size_t)c->n_pad * c->n_pad * 4);
   alloc(c->partials, 8 * (size_t)48 * 4096);
   alloc(c->scal, 8 * 16);
-  alloc(c->gbar, 256);
+  alloc(c->gbar, 8 * 128);   // the PCG's grid-barrier counters (8, 128 bytes apart)
   alloc(c->gjrk, 2 * 32 * (size_t)c->n_pad * 4);
   alloc(c->Binv32b, (size_t)c->n_pad * c->n_pad * 4);
   alloc(c->RTb, (size_t)c->n_pad * c->n_pad * 4);
@@ -1277,8 +1278,8 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
       }
     }
   }
-  CUDA_TRY(c, cudaFuncSetAttribute(k_project<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
-  CUDA_TRY(c, cudaFuncSetAttribute(k_project<32, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_project<0, 0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_project<32, 8, 8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
   CUDA_TRY(c, cudaFuncSetAttribute(k_coarse_rt_s, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   {  // TMA descriptors (128 x 32 fp32 boxes, 128-byte swizzle) for the tensor-core Newton-Schulz GEMM
@@ -1310,7 +1311,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     int optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const void* fns[] = {(const void*)k_pcg, (const void*)k_pcg_tm<32>, (const void*)k_pcg_tm<0>,
-                         (const void*)k_coarse_gj32, (const void*)k_project<0, 0>, (const void*)k_project<32, 512>,
+                         (const void*)k_coarse_gj32, (const void*)k_project<0, 0, 0, 0>, (const void*)k_project<32, 8, 8, 8>,
                          (const void*)k_flux_cfl, (const void*)k_coarse_rt_s, (const void*)k_ns_gemm_tc,
                          (const void*)k_ns_gemm};
     for (const void* fn : fns) {
@@ -1492,10 +1493,10 @@ static lrbms_status launch_project_to(lrbms_ctx* c, const double* lam, double* b
   A.fc = c->at<double2>(c->fc); A.lam = lam;
   A.blocks = blocks; A.rhs = rhs;
   A.tstamp = c->debug_tstamp;
-  if (c->g.N == 32 && c->g.n_loc == 512)
-    k_project<32, 512><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
+  if (c->g.N == 32 && c->g.dim == 3 && c->g.s[0] == 8 && c->g.s[1] == 8 && c->g.s[2] == 8)
+    k_project<32, 8, 8, 8><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
   else
-    k_project<0, 0><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
+    k_project<0, 0, 0, 0><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
   return LRBMS_OK;
 }
@@ -2006,21 +2007,19 @@ size_t lrbms_fine_bytes(const lrbms_ctx* c) {
   return total;
 }
 
-lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt_fixed, double* dt_log, void* ws,
-                            size_t bytes, double rtol, int32_t max_iters, int64_t* iters_total) {
-  lrbms_status st = check_ctx(c);
-  if (st) return st;
-  if (!c->have_medium || !c->have_sat) return fail(c, LRBMS_E_STATE, "set_medium and set_saturation must precede the fine run");
-  if (n_steps < 0) return fail(c, LRBMS_E_CONFIG, "n_steps < 0");
-  if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
-  if (!(rtol > 0) || max_iters <= 0) return fail(c, LRBMS_E_CONFIG, "fine solve needs rtol > 0 and max_iters > 0");
+}  // extern "C" (reopened below)
+
+// The fine solver's arguments on a caller-owned fine workspace (NEXT-2; also the snapshot solves of
+// the offline stage, NEXT-3): grid G and block nt of the cooperative CG.
+static lrbms_status fine_prepare(lrbms_ctx* c, void* ws, size_t bytes, double rtol, int32_t max_iters, FineArgs& F,
+                                 int& G, int& nt) {
   size_t offs[16], total;
   fine_layout(c, offs, &total);
   if (!ws || bytes < total || (reinterpret_cast<uintptr_t>(ws) & 255))
     return fail(c, LRBMS_E_CONFIG, "fine workspace missing, smaller than lrbms_fine_bytes or not 256-byte aligned");
+  if (!(rtol > 0) || max_iters <= 0) return fail(c, LRBMS_E_CONFIG, "fine solve needs rtol > 0 and max_iters > 0");
   const Geo& g = c->g;
   char* b = static_cast<char*>(ws);
-  FineArgs F;
   F.g = g; F.L = links_of(c);
   F.fc = c->at<double2>(c->fc);
   F.x = c->at<double>(c->p);
@@ -2043,7 +2042,7 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
 #define FINE_COARSE 1
 #endif
   // two-level preconditioner: E = Z^T A Z goes through the context's coarse level (stencil buffer,
-  // a full inverse on the first step of the call, then one Newton-Schulz update per step); the
+  // a full inverse on the first solve of the call, then one Newton-Schulz update per solve); the
   // reduced solver's coarse inverse is rebuilt at its next step
   F.coarse = FINE_COARSE && g.n_s > 1 && c->opts.use_coarse == 2;
   if (F.coarse) c->have_x = false;
@@ -2051,29 +2050,54 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
   F.wc = reinterpret_cast<double*>(b + offs[15]);
   F.n_pad = c->n_pad;
   F.dt_bits = (unsigned long long*)c->at<double>(c->scal);
+  F.build_nbr = 1;
   int per_sm = 0;
   CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fine_pcg, 256, 0));
-  const int G = std::min(4096, std::max(1, per_sm) * c->sms);
-  const int nt = std::min(512, cdiv(g.n_loc, 32) * 32);
+  G = std::min(4096, std::max(1, per_sm) * c->sms);
+  nt = std::min(512, cdiv(g.n_loc, 32) * 32);
   if (16 * (size_t)g.n_loc > 48 * 1024) return fail(c, LRBMS_E_CONFIG, "fine run: subdomain too large (n_loc > 3072)");
+  return LRBMS_OK;
+}
+
+// one fine pressure solve A(lam) x = b(lam) (def:pressureDG P:337-345), x = the context's p (warm start)
+static lrbms_status fine_solve(lrbms_ctx* c, FineArgs& F, const double* lam, int G, int nt) {
+  const Geo& g = c->g;
+  lrbms_status st;
+  F.lam = lam;
+  k_fine_setup<<<g.n_s, nt, 16 * (size_t)g.n_loc, c->stream>>>(F);
+  LAUNCH_CHECK(c);
+  F.build_nbr = 0;
+  if (F.coarse) {   // E = Z^T A Z, then its inverse kept current by the coarse level
+    k_fine_coarse_stencil<<<g.n_s, 256, 0, c->stream>>>(F, c->at<double>(c->Es));
+    LAUNCH_CHECK(c);
+    if ((st = launch_coarse(c))) return st;
+    F.Xc = coarse_x(c, c->xcur);
+  }
+  CUDA_TRY(c, cudaMemsetAsync(F.bar, 0, 4, c->stream));
+  void* args[] = {&F};
+  CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_fine_pcg, dim3(G), dim3(256), args, 0, c->stream));
+  c->launches++;
+  c->p_valid = true;
+  return LRBMS_OK;
+}
+
+extern "C" {
+
+lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt_fixed, double* dt_log, void* ws,
+                            size_t bytes, double rtol, int32_t max_iters, int64_t* iters_total) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!c->have_medium || !c->have_sat) return fail(c, LRBMS_E_STATE, "set_medium and set_saturation must precede the fine run");
+  if (n_steps < 0) return fail(c, LRBMS_E_CONFIG, "n_steps < 0");
+  if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
+  FineArgs F;
+  int G = 0, nt = 0;
+  if ((st = fine_prepare(c, ws, bytes, rtol, max_iters, F, G, nt))) return st;
+  const Geo& g = c->g;
   if (!c->p_valid) CUDA_TRY(c, cudaMemsetAsync(F.x, 0, 8 * (size_t)g.n, c->stream));
   CUDA_TRY(c, cudaMemsetAsync(F.iters, 0, 8, c->stream));
   for (int k = 0; k < n_steps; ++k) {
-    F.lam = c->lam_cur();
-    F.build_nbr = k == 0;
-    k_fine_setup<<<g.n_s, nt, 16 * (size_t)g.n_loc, c->stream>>>(F);
-    LAUNCH_CHECK(c);
-    if (F.coarse) {   // E = Z^T A Z, then its inverse kept current by the coarse level
-      k_fine_coarse_stencil<<<g.n_s, 256, 0, c->stream>>>(F, c->at<double>(c->Es));
-      LAUNCH_CHECK(c);
-      if ((st = launch_coarse(c))) return st;
-      F.Xc = coarse_x(c, c->xcur);
-    }
-    CUDA_TRY(c, cudaMemsetAsync(F.bar, 0, 4, c->stream));
-    void* args[] = {&F};
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_fine_pcg, dim3(G), dim3(256), args, 0, c->stream));
-    c->launches++;
-    c->p_valid = true;
+    if ((st = fine_solve(c, F, c->lam_cur(), G, nt))) return st;
     if ((st = launch_transport(c, cfl, dt_fixed, dt_log, k, nullptr, nullptr))) return st;
     c->steps++;
   }
@@ -2083,6 +2107,192 @@ lrbms_status lrbms_run_fine(lrbms_ctx* c, int32_t n_steps, double cfl, double dt
   st = finish(c, n_steps);
   if (iters_total) *iters_total = it[1];
   return st;
+}
+
+// ---------------------------------------------------------------- NEXT-3: the offline stage on the GPU
+static void offline_layout(const lrbms_ctx* c, int J, size_t* offs, size_t* total) {
+  const size_t n = c->g.n, ns = c->g.n_s;
+  size_t fo[16], ft = 0;
+  fine_layout(c, fo, &ft);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  offs[0] = take(ft);                    // the fine solver's workspace
+  offs[1] = take(8 * n);                 // outflow sums
+  offs[2] = take(8 * 6 * n);             // inflow magnitudes per side
+  offs[3] = take(8 * n);                 // tau
+  offs[4] = take(8 * n);                 // lambda^(j)
+  offs[5] = take(8 * (size_t)J * n);     // snapshots / Y columns
+  offs[6] = take(8 * ns * J);            // singular values
+  offs[7] = take(4 * ns * J);            // their order
+  offs[8] = take(4 * ns);                // kept modes
+  offs[9] = take(4 * 64 + 8 * 4);        // sweep flags, tmax, sref, dt0
+  *total = off;
+}
+
+}  // extern "C" (reopened below)
+
+static void graded_exponents(int dim, int count, int (*e)[3]) {
+  int k = 0;
+  for (int deg = 0; k < count && deg <= 64; ++deg) {
+    for (int ez = 0; ez <= (dim == 3 ? deg : 0) && k < count; ++ez)
+      for (int ey = 0; ey <= deg - ez && k < count; ++ey) {
+        e[k][0] = deg - ey - ez; e[k][1] = ey; e[k][2] = ez;
+        ++k;
+      }
+  }
+}
+
+extern "C" {
+
+size_t lrbms_offline_bytes(const lrbms_ctx* c, int32_t n_train) {
+  if (!c || n_train < 1 || n_train > OFF_MAXJ) return 0;
+  size_t offs[10], total = 0;
+  offline_layout(c, n_train, offs, &total);
+  return total;
+}
+
+lrbms_status lrbms_offline_basis(lrbms_ctx* c, int32_t M, int32_t n_train, const double* mu, int32_t horizon_steps,
+                                 double cfl, double eps_pca, double rtol, void* ws, size_t bytes, double* Phi,
+                                 double* tau_out, double* snapshots, int32_t* kept_out, lrbms_offline_info* info) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!c->have_medium || !c->have_sat) return fail(c, LRBMS_E_STATE, "set_medium and set_saturation must precede the offline stage");
+  if (M < 3 || M > OFF_MAXM) return fail(c, LRBMS_E_CONFIG, "number of profiles M = %d not in [3, %d]", M, OFF_MAXM);
+  if (n_train < 1 || n_train > OFF_MAXJ) return fail(c, LRBMS_E_CONFIG, "n_train = %d not in [1, %d]", n_train, OFF_MAXJ);
+  if (!mu || !Phi) return fail(c, LRBMS_E_CONFIG, "mu and Phi are required");
+  if (horizon_steps < 1 || !(cfl > 0) || !(eps_pca >= 0) || !(rtol > 0))
+    return fail(c, LRBMS_E_CONFIG, "need horizon_steps >= 1, cfl > 0, eps_pca >= 0, rtol > 0");
+  const Geo& g = c->g;
+  if ((size_t)(g.N + 1) * g.n_loc * 8 > 200 * 1024) return fail(c, LRBMS_E_CONFIG, "offline stage: (N + 1) n_loc too large");
+  size_t offs[10], total = 0;
+  offline_layout(c, n_train, offs, &total);
+  if (!ws || bytes < total || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(c, LRBMS_E_CONFIG, "offline workspace missing, smaller than lrbms_offline_bytes or not 256-byte aligned");
+  char* b = static_cast<char*>(ws);
+  const size_t n = g.n;
+  size_t fo[16], ft = 0;
+  fine_layout(c, fo, &ft);
+  FineArgs F;
+  int G = 0, nt = 0;
+  if ((st = fine_prepare(c, b + offs[0], ft, rtol, 100000, F, G, nt))) return st;
+  CUDA_TRY(c, cudaMemsetAsync(F.iters, 0, 8, c->stream));
+  if (!c->p_valid) CUDA_TRY(c, cudaMemsetAsync(F.x, 0, 8 * n, c->stream));
+  int* flags = reinterpret_cast<int*>(b + offs[9]);
+  double* dscr = reinterpret_cast<double*>(b + offs[9] + 256);   // tmax, sref, dt0
+  // 1. the fine pressure at s0 and the CFL step of its fluxes (k_flux_cfl's dt minimum)
+  c->have_x = false;
+  if ((st = fine_solve(c, F, c->lam_cur(), G, nt))) return st;
+  {
+    FluxArgs A = flux_args(c, cfl, 0.0, nullptr, 0);
+    const unsigned long long inf = 0x7ff0000000000000ull;
+    CUDA_TRY(c, cudaMemcpyAsync(A.dt_bits, &inf, 8, cudaMemcpyHostToDevice, c->stream));
+    const int ntf = std::min(512, cdiv(g.n_loc, 32) * 32);
+    k_flux_cfl<<<g.n_s, ntf, 3 * 8 * g.n_loc, c->stream>>>(A);
+    LAUNCH_CHECK(c);
+  }
+  double dt0 = 0.0;
+  {
+    unsigned long long bits = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&bits, c->at<double>(c->scal), 8, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    memcpy(&dt0, &bits, 8);
+  }
+  if (!(dt0 > 0.0) || !std::isfinite(dt0)) return fail(c, LRBMS_E_NUMERICAL, "offline stage: no flow at s0");
+  const double T = horizon_steps * dt0;
+  // 2. time of flight
+  OffArgs O;
+  O.g = g; O.L = links_of(c); O.fc = c->at<double2>(c->fc);
+  O.p = c->at<double>(c->p); O.lam0 = c->lam_cur();
+  O.phiV = c->have_phi ? c->at<double>(c->phiV) : nullptr;
+  O.outs = reinterpret_cast<double*>(b + offs[1]);
+  O.inm = reinterpret_cast<double*>(b + offs[2]);
+  O.tau = reinterpret_cast<double*>(b + offs[3]);
+  k_off_flux<<<g.n_s, std::min(512, cdiv(g.n_loc, 32) * 32), 0, c->stream>>>(O);
+  LAUNCH_CHECK(c);
+  int sweeps = 0;
+  const int SB = 64;
+  const int gsw = std::min(cdiv(g.n, 256), c->sms * 8);
+  for (;;) {
+    CUDA_TRY(c, cudaMemsetAsync(flags, 0, 4 * SB, c->stream));
+    for (int k = 0; k < SB; ++k) {
+      O.changed = flags + k;
+      k_off_tof_sweep<<<gsw, 256, 0, c->stream>>>(O);
+      LAUNCH_CHECK(c);
+    }
+    int hf[SB];
+    CUDA_TRY(c, cudaMemcpyAsync(hf, flags, 4 * SB, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    sweeps += SB;
+    if (!hf[SB - 1]) {
+      for (int k = 0; k < SB; ++k)
+        if (!hf[k]) { sweeps += k + 1 - SB; break; }
+      break;
+    }
+    if (sweeps > 4 * (int)n + SB) return fail(c, LRBMS_E_NUMERICAL, "offline stage: time of flight did not converge (flow cycle?)");
+  }
+  k_off_tof_max<<<1, 1024, 0, c->stream>>>(O, dscr);
+  LAUNCH_CHECK(c);
+  k_off_tof_fill<<<gsw, 256, 0, c->stream>>>(O, dscr);
+  LAUNCH_CHECK(c);
+  if (tau_out) {
+    k_to_natural<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, O.tau, tau_out);
+    LAUNCH_CHECK(c);
+  }
+  // 3 + 4. training mobilities and fine snapshots
+  TrainArgs TA;
+  TA.n = n; TA.M = M; TA.tau = O.tau; TA.s0 = c->s_cur(); TA.f = c->f;
+  double s_inj = -INFINITY;
+  for (int q = 0; q < c->n_links; ++q) s_inj = std::max(s_inj, c->h_s[q]);
+  TA.s_inj = s_inj;
+  for (int q = 0; q < OFF_MAXM; ++q) TA.thr[q] = (q >= 1 && q <= M - 2) ? q * T / (M - 2) : 0.0;
+  TA.lam = reinterpret_cast<double*>(b + offs[4]);
+  double* P = reinterpret_cast<double*>(b + offs[5]);
+  for (int j = 0; j < n_train; ++j) {
+    for (int q = 0; q < OFF_MAXM; ++q) TA.mu[q] = q < M ? mu[(size_t)j * M + q] : 0.0;
+    k_off_train_lambda<<<gsw, 256, 0, c->stream>>>(TA);
+    LAUNCH_CHECK(c);
+    c->have_x = false;   // the training mobilities differ too much for a Newton-Schulz update
+    if ((st = fine_solve(c, F, TA.lam, G, nt))) return st;
+    CUDA_TRY(c, cudaMemcpyAsync(P + (size_t)j * n, c->at<double>(c->p), 8 * n, cudaMemcpyDeviceToDevice, c->stream));
+    if (snapshots) {
+      k_to_natural<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, c->at<double>(c->p), snapshots + (size_t)j * n);
+      LAUNCH_CHECK(c);
+    }
+  }
+  // 5. per-subdomain POD and the bases
+  PodArgs PA;
+  PA.g = g; PA.J = n_train; PA.N = g.N; PA.P = P;
+  PA.sigma = reinterpret_cast<double*>(b + offs[6]);
+  PA.order = reinterpret_cast<int*>(b + offs[7]);
+  PA.kept = reinterpret_cast<int*>(b + offs[8]);
+  PA.Phi = Phi; PA.eps_pca = eps_pca; PA.sref = dscr + 1;
+  PA.nmono = std::min(OFF_NMONO, g.N + 8);
+  graded_exponents(g.dim, PA.nmono, PA.mexp);
+  k_off_pod_svd<<<g.n_s, 512, 0, c->stream>>>(PA);
+  LAUNCH_CHECK(c);
+  k_off_sigma_max<<<1, 1024, 0, c->stream>>>(PA.sigma, (size_t)g.n_s * n_train, dscr + 1);
+  LAUNCH_CHECK(c);
+  const size_t asm_smem = 8 * (size_t)(g.N + 1) * g.n_loc;
+  CUDA_TRY(c, cudaFuncSetAttribute(k_off_pod_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_smem));
+  k_off_pod_assemble<<<g.n_s, 512, asm_smem, c->stream>>>(PA);
+  LAUNCH_CHECK(c);
+  std::vector<int> kept(g.n_s);
+  int it[2] = {0, 0};
+  CUDA_TRY(c, cudaMemcpyAsync(kept.data(), PA.kept, 4 * (size_t)g.n_s, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(it, F.iters, 8, cudaMemcpyDeviceToHost, c->stream));
+  st = finish(c, 0);   // device flags of the fine solves (non-convergence, NaN)
+  c->have_x = false;   // the reduced solver rebuilds its coarse inverse at its next step
+  if (st) return st;
+  for (int E = 0; E < g.n_s; ++E)
+    if (kept[E] < 0) return fail(c, LRBMS_E_CONFIG, "offline stage: subdomain %d cannot be completed to N = %d", E, g.N);
+  if (kept_out) memcpy(kept_out, kept.data(), 4 * (size_t)g.n_s);
+  if (info) {
+    info->dt0 = dt0;
+    info->horizon = T;
+    info->tof_sweeps = sweeps;
+    info->fine_cg_iters = it[1];
+  }
+  return LRBMS_OK;
 }
 
 lrbms_status lrbms_stage_project(lrbms_ctx* c, double* blocks, double* r) {

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(128, CHOL_MINB) k_block_chol(Geo g, double* __
   __shared__ double dg[4][32];
   __shared__ __align__(16) double xs[4][32 * 8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (H.gbar_reset && blockIdx.x == 0 && threadIdx.x == 0) *H.gbar_reset = 0u;
+  if (H.gbar_reset && blockIdx.x == 0 && threadIdx.x < 8) H.gbar_reset[32 * threadIdx.x] = 0u;   // k_pcg_tm's counters
   const int E = blockIdx.x * (blockDim.x >> 5) + w;
   if (E >= g.n_s) return;
   const int N = NFIX ? NFIX : g.N;

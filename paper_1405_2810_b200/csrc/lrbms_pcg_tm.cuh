@@ -156,6 +156,55 @@ __device__ __forceinline__ double grid_reduce_rel(double v, double* red16, doubl
   return *bc;
 }
 
+// The on-chip PCG's grid synchronisations arrive on PCG_NBAR counters (128 bytes apart: different L2
+// lines) instead of one, CTA b on counter b % PCG_NBAR, so that the 147 arrivals do not serialise on
+// one address; lanes 0..PCG_NBAR-1 of warp 0 each acquire one counter.  Same epochs, same
+// deterministic partial sums as grid_reduce_rel.
+#ifndef PCG_NBAR
+#define PCG_NBAR 8
+#endif
+constexpr int PCG_BAR_STRIDE = 32;   // unsigned words between counters
+__device__ __forceinline__ void bar_arrive_wait_n(unsigned* bar, unsigned epoch) {
+  const int lane = threadIdx.x & 31, G = gridDim.x;
+  if (lane == 0)
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar + PCG_BAR_STRIDE * (blockIdx.x % PCG_NBAR)),
+                 "r"(1u)
+                 : "memory");
+  if (lane < PCG_NBAR) {
+    const unsigned cnt = (unsigned)((G - lane + PCG_NBAR - 1) / PCG_NBAR);   // CTAs b < G with b % NBAR == lane
+    const unsigned target = epoch * cnt;
+    const unsigned* ctr = bar + PCG_BAR_STRIDE * lane;
+    while (ld_acquire_gpu(ctr) < target) {
+    }
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ double grid_reduce_n(double v, double* red16, double* partials, unsigned* bar,
+                                               unsigned& epoch, double* bc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5, G = gridDim.x;
+  if (lane == 0) red16[warp] = v;
+  __syncthreads();
+  ++epoch;
+  double* ps = partials + (size_t)(epoch & 3) * G;
+  if (warp == 0) {
+    const double t = warp_sum(lane < W ? red16[lane] : 0.0);
+    if (lane == 0) ps[blockIdx.x] = t;
+    bar_arrive_wait_n(bar, epoch);
+    double sum = 0.0;
+    for (int b = lane; b < G; b += 32) sum += __ldcg(ps + b);
+    sum = warp_sum(sum);
+    if (lane == 0) *bc = sum;
+  }
+  __syncthreads();
+  return *bc;
+}
+__device__ __forceinline__ void grid_barrier_n(unsigned* bar, unsigned& epoch) {
+  __syncthreads();
+  ++epoch;
+  if ((threadIdx.x >> 5) == 0) bar_arrive_wait_n(bar, epoch);
+  __syncthreads();
+}
+
 // Grid barrier without a reduction (release arrival on the same counter / epoch as grid_reduce_rel).
 __device__ __forceinline__ void grid_barrier_rel(unsigned* bar, unsigned& epoch) {
   __syncthreads();
@@ -243,6 +292,53 @@ __device__ __noinline__ void hist_weights(const PcgArgs& A, double* sh, double (
   // the 44 fixed-order sums of the Gram / rhs partials (formed by k_hist_sum before the launch)
   for (int q = threadIdx.x; q < 44; q += blockDim.x) sh[q] = A.gsum[q];
   __syncthreads();
+  double G[8][8], rhs8[8];
+  int q = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = i; j < 8; ++j) {
+      const double v = (j < nh) ? sh[q] : 0.0;
+      G[i][j] = v; G[j][i] = v;
+      ++q;
+    }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rhs8[i] = i < nh ? sh[36 + i] : 0.0;
+  bool keep[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    keep[k] = k < nh && G[k][k] > 1e-12 * fabs(G[0][0]) && G[k][k] > 0.0;
+    if (keep[k]) {
+      const double piv = G[k][k];
+#pragma unroll
+      for (int i = k + 1; i < 8; ++i) {
+        const double f = G[i][k] / piv;
+#pragma unroll
+        for (int j = k; j < 8; ++j) G[i][j] -= f * G[k][j];
+        rhs8[i] -= f * rhs8[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 7; k >= 0; --k) {
+    if (k < nh && keep[k]) {
+      double v = rhs8[k];
+#pragma unroll
+      for (int j = k + 1; j < 8; ++j) v -= G[k][j] * alpha_h[j];
+      alpha_h[k] = v / G[k][k];
+    }
+  }
+}
+
+// the same, for one warp (k_pcg_tm: the CTA's warp 0)
+__device__ __noinline__ void hist_weights_warp(const PcgArgs& A, double* sh, double (&alpha_h)[8]) {
+  const int nh = A.nh;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) alpha_h[j] = 0.0;
+  if (nh <= 0) return;
+  // the 44 fixed-order sums of the Gram / rhs partials (formed by k_hist_sum before the launch)
+  for (int q = threadIdx.x & 31; q < 44; q += 32) sh[q] = A.gsum[q];
+  __syncwarp();
   double G[8][8], rhs8[8];
   int q = 0;
 #pragma unroll
@@ -512,7 +608,17 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
   // ---- initial guess: Galerkin combination of the history, y0 = W alpha, r0 = rb - V alpha
   double alpha_h[8];
   TM_SSTAMP(2);
-  hist_weights(A, sh46, alpha_h);
+  {   // one warp solves the 8 x 8 history system (every thread of the CTA doing it was 7-18 us of
+      // fp64 divisions competing for the pipe), the weights go to the others through shared memory
+    __shared__ double ah_s[8];
+    if (warp == 0) {
+      hist_weights_warp(A, sh46, alpha_h);
+      if (lane < 8) ah_s[lane] = alpha_h[lane];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) alpha_h[j] = ah_s[j];
+  }
   TM_SSTAMP(3);
   const size_t R = (size_t)g.n_s * N;
   double y = 0.0, r = 0.0;
@@ -531,7 +637,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     if (lane == 0) A.wc[E] = w;
   }
   TM_SSTAMP(4);
-  const double bb = grid_reduce_rel(pbb, red16, gparts, A.gbar, epoch, &bc[0]);
+  const double bb = grid_reduce_n(pbb, red16, gparts, A.gbar, epoch, &bc[0]);
   TM_SSTAMP(5);
   const double tol2 = A.rtol * A.rtol * bb;
   double rr = 1.0;
@@ -545,7 +651,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
         if (lane == 0) A.e0[E] = (double)e;
         y += zh * (double)e;
       }
-      grid_barrier_rel(A.gbar, epoch);
+      grid_barrier_n(A.gbar, epoch);
       if (own) {
         double rk = r - zh * __ldcg(A.e0 + E);
 #pragma unroll
@@ -554,7 +660,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
         r = act ? rk : 0.0;
       }
       scatter(r);
-      grid_barrier_rel(A.gbar, epoch);
+      grid_barrier_n(A.gbar, epoch);
       stage_g();
     } else if (A.use_coarse == 1) {
       stage_wc();
@@ -562,7 +668,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
     double z = r;
     if (A.use_coarse) { const float ec = coarse_dot(); z = act ? r + zh * (double)ec : 0.0; }
     if (act) A.z[E * N + lane] = z;
-    double rz = grid_reduce_rel(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+    double rz = grid_reduce_n(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
     TM_SSTAMP(6);
     double beta = 0.0, p = 0.0;
     for (it = (rz <= tol2) ? A.max_iters + 2 : 1; it <= A.max_iters; ++it) {
@@ -623,7 +729,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
       }
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 0], gtimer());
       TM_STAMP(1);
-      const double pq = grid_reduce_rel(own ? warp_sum(act ? local : 0.0) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      const double pq = grid_reduce_n(own ? warp_sum(act ? local : 0.0) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 1], gtimer());
       if (!(pq > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
@@ -645,7 +751,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
         if (lane == 0) A.wc[E] = w;
       }
       TM_STAMP(3);
-      grid_barrier_rel(A.gbar, epoch);
+      grid_barrier_n(A.gbar, epoch);
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 2], gtimer());
       TM_STAMP(4);
       // ---------------- C: z = M^-1 r, r.z
@@ -656,7 +762,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
       if (A.use_coarse) { const float ec = coarse_gemv(); z = act ? r + zh * (double)ec : 0.0; }
       if (act) A.z[E * N + lane] = z;
       TM_STAMP(6);
-      const double rz_new = grid_reduce_rel(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      const double rz_new = grid_reduce_n(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 3], gtimer());
       TM_STAMP(7);
       rr = rz_new;

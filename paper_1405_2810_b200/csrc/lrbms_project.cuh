@@ -59,10 +59,46 @@ __device__ __forceinline__ int pair_tj(int p) {
   return p < 4 ? p : p < 7 ? p - 3 : p < 9 ? p - 5 : 3;
 }
 
-template <int NFIX, int NLFIX>   // compile-time N and n_loc (C5: 32, 512), 0 = runtime
+// Local index helpers of a subdomain shape known at compile time (SX, SY, SZ > 0: the divisions and
+// modulos fold to shifts and masks for 8 x 8 x 8) or at run time (0: read from g)
+template <int SX, int SY, int SZ>
+struct LShape {
+  int sx, sy, sz, st1, st2;
+  __device__ __forceinline__ explicit LShape(const Geo& g)
+      : sx(SX ? SX : g.s[0]), sy(SY ? SY : g.s[1]), sz(SZ ? SZ : g.s[2]), st1(SX ? SX : g.s[0]),
+        st2((SX ? SX : g.s[0]) * (SY ? SY : g.s[1])) {}
+  __device__ __forceinline__ void xyz(int l, int c[3]) const {
+    c[0] = l % sx;
+    c[1] = (l / sx) % sy;
+    c[2] = l / st2;
+  }
+  __device__ __forceinline__ int s(int a) const { return a == 0 ? sx : (a == 1 ? sy : sz); }
+  __device__ __forceinline__ int stride(int a) const { return a == 0 ? 1 : (a == 1 ? st1 : st2); }
+  __device__ __forceinline__ int nface(int a) const { return a == 0 ? sy * sz : (a == 1 ? sx * sz : sx * sy); }
+  // internal index of the neighbour along axis a, direction dir (-1 outside the domain)
+  __device__ __forceinline__ int nb(const Geo& g, int E, const int C[3], int l, const int c[3], int a, int dir) const {
+    const int nc = c[a] + dir, sa = s(a), st = stride(a), nl = st2 * sz;
+    if (nc >= 0 && nc < sa) return E * nl + l + dir * st;
+    if (nc < 0) return C[a] == 0 ? -1 : (E - g.Estride[a]) * nl + l + (sa - 1) * st;
+    return C[a] == g.S[a] - 1 ? -1 : (E + g.Estride[a]) * nl + l - (sa - 1) * st;
+  }
+  __device__ __forceinline__ int face_pos(const int c[3], int a) const {
+    return a == 0 ? c[1] + sy * c[2] : (a == 1 ? c[0] + sx * c[2] : c[0] + sx * c[1]);
+  }
+  __device__ __forceinline__ int face_cell(int f, int a, int ca) const {
+    if (a == 0) { const int y = f % sy, z = f / sy; return ca + sx * (y + sy * z); }
+    if (a == 1) { const int x = f % sx, z = f / sx; return x + sx * (ca + sy * z); }
+    const int x = f % sx, y = f / sx;
+    return x + sx * (y + sy * ca);
+  }
+};
+
+template <int NFIX, int SX, int SY, int SZ>   // compile-time N and subdomain shape (C5: 32; 8, 8, 8), 0 = runtime
 __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   extern __shared__ __align__(16) double sm[];
   const Geo& g = A.g;
+  constexpr int NLFIX = SX * SY * SZ;
+  const LShape<SX, SY, SZ> S(g);
   const int N = NFIX ? NFIX : g.N, nl = NLFIX ? NLFIX : g.n_loc, E = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   const int nb1 = 1 + g.dim, LD = A.LD, NP = A.NP, T = NP / 8, nfp = A.nfp, LDN = A.LDN;
@@ -90,18 +126,18 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
       lp[a] = lm[a] = 0.0;
       wpos[a] = -1;
       if (a >= g.dim) continue;
-      const int st = g.lstride[a];
-      if (c[a] + 1 < g.s[a]) {
+      const int st = S.stride(a);
+      if (c[a] + 1 < S.s(a)) {
         fp[a] = A.fc[(base + l) * 3 + a];
         lp[a] = A.lam[base + l + st];
       } else if (C[a] + 1 < g.S[a]) {
-        const int nb = neighbour(g, E, C, l, c, a, +1);
+        const int nb = S.nb(g, E, C, l, c, a, +1);
         fp[a] = A.fc[(base + l) * 3 + a];
         lp[a] = A.lam[nb];
-        wpos[a] = face_pos(g, c, a);
+        wpos[a] = S.face_pos(c, a);
       }
       if (c[a] == 0 && C[a] > 0) {
-        const int nb = neighbour(g, E, C, l, c, a, -1);
+        const int nb = S.nb(g, E, C, l, c, a, -1);
         fm[a] = A.fc[(size_t)nb * 3 + a];
         lm[a] = A.lam[nb];
       }
@@ -112,7 +148,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   int w_wpos[3];
   if (tid < nl) {
     int c0[3];
-    local_xyz(g, tid, c0);
+    S.xyz(tid, c0);
     load_winputs(tid, c0, w_ll, w_fp, w_fm, w_lp, w_lm, w_wpos);
   }
 
@@ -133,24 +169,24 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
       for (int c1 = lane; c1 < nl; c1 += 32) cp_async8(Phs + (size_t)k * LD + c1, PhiE + (size_t)k * nl + c1);
   }
   for (int a = 0; a < 3; ++a) {
-    const int nf = a < g.dim ? g.nface[a] : 0;
+    const int nf = a < g.dim ? S.nface(a) : 0;
     double* dst = PhN + (size_t)a * NP * LDN;
     if (has[a]) {
       const double* PhiN = A.Phi + (size_t)(E + g.Estride[a]) * N * nl;
       if (a > 0 && v16) {
         for (int k = warp; k < N; k += nwarp)
           for (int f2 = 2 * lane; f2 < nf; f2 += 64)
-            cp_async16(dst + (size_t)k * LDN + f2, PhiN + (size_t)k * nl + face_cell(g, f2, a, 0));
+            cp_async16(dst + (size_t)k * LDN + f2, PhiN + (size_t)k * nl + S.face_cell(f2, a, 0));
       } else {
         for (int k = warp; k < N; k += nwarp)
           for (int f = lane; f < nf; f += 32)
-            cp_async8(dst + (size_t)k * LDN + f, PhiN + (size_t)k * nl + face_cell(g, f, a, 0));
+            cp_async8(dst + (size_t)k * LDN + f, PhiN + (size_t)k * nl + S.face_cell(f, a, 0));
       }
     }
     for (int k = warp; k < NP; k += nwarp)
       for (int f = (has[a] && k < N ? nf : 0) + lane; f < LDN; f += 32) dst[(size_t)k * LDN + f] = 0.0;
     for (int f = tid; f < nfp; f += nt) {
-      fcell[a * nfp + f] = (f < nf) ? face_cell(g, f, a, g.s[a] - 1) : 0;
+      fcell[a * nfp + f] = (f < nf) ? S.face_cell(f, a, S.s(a) - 1) : 0;
       wi[a * nfp + f] = 0.0;
     }
   }
@@ -165,7 +201,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   __syncthreads();   // wi / fcell initialised by the staging loop
   for (int l = tid; l < nl; l += nt) {
     int c[3];
-    local_xyz(g, l, c);
+    S.xyz(l, c);
     double ll;
     double2 fp[3], fm[3];
     double lp[3], lm[3];
@@ -190,9 +226,9 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
         if (wpos[a] >= 0) {
           wi[a * nfp + wpos[a]] = wp;
           dc += wp;
-        } else if (c[a] + 1 < g.s[a]) {
+        } else if (c[a] + 1 < S.s(a)) {
           wl[a] = wp;
-          Wc[(size_t)(l + g.lstride[a]) * 8 + 1 + 2 * a] = wp;   // -a weight of the upper cell
+          Wc[(size_t)(l + S.stride(a)) * 8 + 1 + 2 * a] = wp;   // -a weight of the upper cell
         }
         dc += face_w(fm[a], lm[a], ll);
       }
@@ -207,7 +243,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
   __syncthreads();
   for (int l = tid; l < nl; l += nt) {
     int c[3];
-    local_xyz(g, l, c);
+    S.xyz(l, c);
     double* w = Wc + (size_t)l * 8;
     double d = w[7];
 #pragma unroll
@@ -235,7 +271,7 @@ __global__ void __launch_bounds__(512) k_project(ProjArgs A) {
 #pragma unroll
   for (int p = 0; p < 10; ++p) acc[p][0] = acc[p][1] = 0.0;
   const int fr = lane >> 2, fc = lane & 3;
-  const int st0 = g.lstride[0], st1 = g.lstride[1], st2 = g.lstride[2];
+  const int st0 = 1, st1 = S.st1, st2 = S.st2;
   for (int ks = warp; ks < A.nlp / 4; ks += nwarp) {
     const int l = 4 * ks + fc;
     double wv[8] = {0, 0, 0, 0, 0, 0, 0, 0};

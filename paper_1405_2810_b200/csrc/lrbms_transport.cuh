@@ -35,41 +35,51 @@ __global__ void __launch_bounds__(512) k_flux_transport(FluxArgs A, int kmax) {
   double* netl = oneg + nl;
   double mn = INFINITY;
 
-  // ---- phase 1: fluxes, flux sums, Q, the CTA's dt bound
+  // ---- phase 1: fluxes, flux sums, Q, the CTA's dt bound.  32-bit cell indices (n < 2^31, checked at
+  //      bind); the neighbour across a subdomain side is i +- xo[a]
+  const int lst[3] = {1, st1, st2};
+  const int sa[3] = {s0, s1, s2};
+  int xo[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) xo[a] = g.Estride[a] * nl - (sa[a] - 1) * lst[a];
   int k = 0;
   for (int E = blockIdx.x; E < g.n_s; E += G, ++k) {
     int C[3];
     sub_xyz(g, E, C);
-    const size_t base = (size_t)E * nl;
+    bool lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = C[a] > 0;
+      hi[a] = C[a] + 1 < g.S[a];
+    }
+    const int base = E * nl;
     const int q0 = A.L.sub_start[E], q1 = A.L.sub_start[E + 1];
     const bool links = q1 > q0;
     for (int l = tid; l < nl; l += nt) {
       const int c0 = l % s0, c1 = (l / s0) % s1, c2 = l / st2;
       const int cc[3] = {c0, c1, c2};
-      const int lst[3] = {1, st1, st2};
-      const int sa[3] = {s0, s1, s2};
-      const size_t gl = base + l;
+      const int gl = base + l;
       const double pl = A.p[gl], ll = A.lam[gl], fl = A.fw[gl];
-      const double2* fco = A.fc + gl * 3;
+      const double2* fco = A.fc + 3 * gl;
       double pos = 0.0, neg = 0.0, acc = 0.0;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         if (a >= dim) break;
         // -a face (this cell is T2; F = w (p_lower - p) leaves the lower cell), then the +a face (this
         // cell is T1): the order of k_flux_cfl, so the sums are bitwise those of the two-kernel path
-        size_t nb = SIZE_MAX;
+        int nb = -1;
         if (cc[a] > 0) nb = gl - lst[a];
-        else if (C[a] > 0) nb = gl - (size_t)g.Estride[a] * nl + (size_t)(sa[a] - 1) * lst[a];
-        if (nb != SIZE_MAX) {
-          const double F = face_w(A.fc[nb * 3 + a], A.lam[nb], ll) * (A.p[nb] - pl);
+        else if (lo[a]) nb = gl - xo[a];
+        if (nb >= 0) {
+          const double F = face_w(A.fc[3 * nb + a], A.lam[nb], ll) * (A.p[nb] - pl);
           pos += fmax(-F, 0.0);
           neg += fmax(F, 0.0);
           acc += -(F * (F >= 0.0 ? A.fw[nb] : fl));
         }
-        nb = SIZE_MAX;
+        nb = -1;
         if (cc[a] + 1 < sa[a]) nb = gl + lst[a];
-        else if (C[a] + 1 < g.S[a]) nb = gl + (size_t)g.Estride[a] * nl - (size_t)(sa[a] - 1) * lst[a];
-        if (nb != SIZE_MAX) {
+        else if (hi[a]) nb = gl + xo[a];
+        if (nb >= 0) {
           const double F = face_w(fco[a], ll, A.lam[nb]) * (pl - A.p[nb]);
           pos += fmax(F, 0.0);
           neg += fmax(-F, 0.0);
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(512) k_flux_transport(FluxArgs A, int kmax) {
         const double Q = fmax(pos, neg);
         if (Q > 0.0) mn = fmin(mn, A.cfl * (A.phiV ? A.phiV[gl] : g.vol) / (A.fpmax * Q));
         if (!(Q == Q)) atomicOr(A.flags, FLAG_NAN);
-        netk[(size_t)k * nl + l] = acc;
+        netk[k * nl + l] = acc;
       }
     }
     if (links) {   // the subdomain's links in its link order (one thread: deterministic), then Q
@@ -108,7 +118,7 @@ __global__ void __launch_bounds__(512) k_flux_transport(FluxArgs A, int kmax) {
         const double Q = fmax(opos[l], oneg[l]);
         if (Q > 0.0) mn = fmin(mn, A.cfl * (A.phiV ? A.phiV[base + l] : g.vol) / (A.fpmax * Q));
         if (!(Q == Q)) atomicOr(A.flags, FLAG_NAN);
-        netk[(size_t)k * nl + l] = netl[l];
+        netk[k * nl + l] = netl[l];
       }
       __syncthreads();   // opos/oneg/netl are reused by the next subdomain with links
     }
@@ -127,13 +137,13 @@ __global__ void __launch_bounds__(512) k_flux_transport(FluxArgs A, int kmax) {
   // ---- phase 2: the upwind update of the same cells, and lambda, f_w of s^{n+1}
   double dt = A.dt_fixed;
   if (!(dt > 0.0)) dt = __longlong_as_double((long long)__ldcg(A.dt_bits));
+  const double dtv = dt / g.vol;   // (dt / pv) with pv = V when phi = 1, hoisted: the same rounding
   k = 0;
   for (int E = blockIdx.x; E < g.n_s; E += G, ++k) {
-    const size_t base = (size_t)E * nl;
+    const int base = E * nl;
     for (int l = tid; l < nl; l += nt) {
-      const size_t gl = base + l;
-      const double pv = A.phiV ? A.phiV[gl] : g.vol;
-      const double sn = A.s[gl] - dt / pv * netk[(size_t)k * nl + l];
+      const int gl = base + l;
+      const double sn = A.s[gl] - (A.phiV ? dt / A.phiV[gl] : dtv) * netk[k * nl + l];
       A.s_out[gl] = sn;
       double lw, lo;
       mobilities(A.f, sn, lw, lo);

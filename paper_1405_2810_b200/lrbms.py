@@ -24,7 +24,8 @@ EXPORTS = ["lrbms_create", "lrbms_workspace_bytes", "lrbms_bind", "lrbms_set_med
            "lrbms_stage_project", "lrbms_stage_solve", "lrbms_stage_reconstruct", "lrbms_stage_transport",
            "lrbms_get_stats", "lrbms_set_profiling", "lrbms_get_stage_times", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy",
            "lrbms_profiles_bytes", "lrbms_set_profiles", "lrbms_set_online", "lrbms_stage_theta",
-           "lrbms_fine_bytes", "lrbms_run_fine", "lrbms_diagnostics"]
+           "lrbms_fine_bytes", "lrbms_run_fine", "lrbms_diagnostics", "lrbms_offline_bytes",
+           "lrbms_offline_basis"]
 
 
 class LrbmsError(RuntimeError):
@@ -61,6 +62,11 @@ class Stats(ctypes.Structure):
                 ("last_iters", ctypes.c_int32), ("total_iters", ctypes.c_int64),
                 ("coarse_rebuilds", ctypes.c_int32), ("fprime_max", ctypes.c_double),
                 ("ns_guard_trips", ctypes.c_int64), ("ns_resid_max", ctypes.c_double)]
+
+
+class OfflineInfo(ctypes.Structure):
+    _fields_ = [("dt0", ctypes.c_double), ("horizon", ctypes.c_double), ("tof_sweeps", ctypes.c_int32),
+                ("fine_cg_iters", ctypes.c_int64)]
 
 
 class Diag(ctypes.Structure):
@@ -109,6 +115,9 @@ def load_library(path: str = LIB_PATH):
         "lrbms_fine_bytes": (ctypes.c_size_t, [P]),
         "lrbms_run_fine": (st, [P, I, D, D, P, P, ctypes.c_size_t, D, I, ctypes.POINTER(ctypes.c_int64)]),
         "lrbms_diagnostics": (st, [P, ctypes.POINTER(Diag)]),
+        "lrbms_offline_bytes": (ctypes.c_size_t, [P, I]),
+        "lrbms_offline_basis": (st, [P, I, I, P, I, D, D, D, P, ctypes.c_size_t, P, P, P, P,
+                                     ctypes.POINTER(OfflineInfo)]),
         "lrbms_get_stage_times": (st, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), I]),
         "lrbms_last_error": (ctypes.c_char_p, [P]),
         "lrbms_version": (ctypes.c_char_p, []),
@@ -321,6 +330,34 @@ class LrbmsContext:
         st = Stats()
         self._check(self.L.lrbms_get_stats(self.h, ctypes.byref(st)))
         return {k: getattr(st, k) for k, _ in Stats._fields_}
+
+    def offline_basis(self, mus, M=8, horizon_steps=None, cfl=None, eps_pca=1e-8, rtol=1e-13,
+                      want_tau=False, want_snapshots=False):
+        """NEXT-3: the offline basis recipe on the GPU (lrbms_offline_basis) from the current saturation;
+        mus: [n_train][M] training parameters (host).  Returns (Phi [n_s][N][n_loc] device tensor,
+        kept (numpy), info dict, tau or None, snapshots or None).  Marshalling only."""
+        torch = self.torch
+        sc = self.sc
+        mus = np.ascontiguousarray(mus, np.float64)
+        J = int(mus.shape[0])
+        nbytes = self.L.lrbms_offline_bytes(self.h, J)
+        if nbytes == 0:
+            raise LrbmsError(LRBMS_E_CONFIG, f"n_train = {J} not supported")
+        with torch.cuda.device(self.device):
+            ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        ptr = (ws.data_ptr() + 255) // 256 * 256
+        Phi = self.empty(sc.n_s, sc.N, sc.n_loc)
+        tau = self.empty(sc.n) if want_tau else None
+        snaps = self.empty(J, sc.n) if want_snapshots else None
+        kept = np.zeros(sc.n_s, np.int32)
+        info = OfflineInfo()
+        hs = sc.n_steps if horizon_steps is None else horizon_steps
+        self._check(self.L.lrbms_offline_basis(
+            self.h, int(M), J, mus.ctypes.data_as(ctypes.c_void_p), int(hs), float(sc.cfl if cfl is None else cfl),
+            float(eps_pca), float(rtol), ctypes.c_void_p(ptr), nbytes, _ptr(Phi), _ptr(tau), _ptr(snaps),
+            kept.ctypes.data_as(ctypes.c_void_p), ctypes.byref(info)))
+        del ws
+        return Phi, kept, {k: getattr(info, k) for k, _ in OfflineInfo._fields_}, tau, snaps
 
     def diagnostics(self) -> dict:
         """K6 diagnostics of the last step (lrbms_diagnostics): mass, s range, zeta, coarse defect."""
