@@ -85,6 +85,10 @@ class Scenario:
     link_s: Optional[np.ndarray] = None     # [n_links] external (inflow) saturation
     Phi: Optional[np.ndarray] = None        # [n_s][N][n_loc]  (ABI layout)
     s0: Optional[np.ndarray] = None         # [n] initial saturation
+    # k = 1 fine space (NEXT-4): penalty constant c_F of eq:penaltyParam and local bases
+    # over the P1 dofs, Phi1[E][k][a n_loc + l] (dof a = mean, x-, y-(, z-) slope of local cell l)
+    c_pen: float = 30.0
+    Phi1: Optional[np.ndarray] = None
 
     # -- derived sizes -------------------------------------------------------
     @property
@@ -198,6 +202,14 @@ def links_for(bc: str, nx: int, ny: int, nz: int):
         for k in range(nz):
             for j in range(ny):
                 add(nx - 1 + nx * (j + ny * k), 0, 0.0, 0.0)
+    elif bc == "all_sides":         # p = 0 on every side face (manufactured-solution pins)
+        for k in range(nz):
+            for j in range(ny):
+                for i in range(nx):
+                    c = i + nx * (j + ny * k)
+                    for ax, q, m in ((0, i, nx), (1, j, ny), (2, k, nz)):
+                        if m > 1 and q in (0, m - 1):
+                            add(c, ax, 0.0, 0.0)
     elif bc == "corner_wells_2d":   # quarter five-spot: injector (0,0), producer (nx-1,ny-1)
         add(0, 0, 1.0, 1.0)
         add(nx - 1 + nx * (ny - 1), 0, 0.0, 0.0)
@@ -275,6 +287,74 @@ def random_full_basis(sc: Scenario, seed: int) -> np.ndarray:
     Phi = np.empty((sc.n_s, nl, nl))
     for E in range(sc.n_s):
         Q, R = np.linalg.qr(rng.standard_normal((nl, nl)))
+        Phi[E] = (Q * np.sign(np.diag(R))[None, :]).T
+    return Phi
+
+
+def _p1_projection_1d(e: int, centre, half):
+    """(mean, xi-coefficient) of the L2 projection onto P1 of t^e over cells [centre -+ half] in
+    subdomain coordinates t (3-point Gauss: exact up to degree 5 in each direction)."""
+    g = np.array([-np.sqrt(0.6), 0.0, np.sqrt(0.6)])
+    w = np.array([5.0, 8.0, 5.0]) / 18.0
+    mean = sum(wk * (centre + gk * half) ** e for gk, wk in zip(g, w))
+    # xi = g / 2 at the Gauss points; coefficient = int m xi / int xi^2 = 12 mean(m xi)
+    slope = 12.0 * sum(wk * (centre + gk * half) ** e * (gk / 2.0) for gk, wk in zip(g, w))
+    return mean, slope
+
+
+def poly1_basis(sc: Scenario, seed: int, rotate: bool = True) -> np.ndarray:
+    """Phi1[E][k][a n_loc + l]: graded tensor monomials of the subdomain coordinates (in [-1, 1]),
+    L2-projected cell by cell onto P1 (the k = 1 fine space of NEXT-4; a coarse-scale piecewise
+    polynomial reduced space), orthonormalised in the l2 of the dofs, column 0 the
+    normalised indicator (mean dofs 1, slopes 0), columns 1..N-1 mixed by a seeded rotation."""
+    N, nl, dim = sc.N, sc.n_loc, sc.dim
+    nd = dim + 1
+    if N > nd * nl:
+        raise ValueError("N > (dim + 1) n_loc")
+    lz, ly, lx = np.meshgrid(np.arange(sc.sz), np.arange(sc.sy), np.arange(sc.sx), indexing="ij")
+    cen = [(2 * lx.reshape(-1) + 1) / sc.sx - 1.0, (2 * ly.reshape(-1) + 1) / sc.sy - 1.0,
+           (2 * lz.reshape(-1) + 1) / max(sc.sz, 1) - 1.0]
+    half = [1.0 / sc.sx, 1.0 / sc.sy, 1.0 / max(sc.sz, 1)]
+    cols = []
+    for ex in _graded_exponents(dim, min(N + 4, nd * nl)):
+        m = [_p1_projection_1d(ex[d], cen[d], half[d]) for d in range(3)]
+        v = np.zeros((nd, nl))
+        v[0] = m[0][0] * m[1][0] * m[2][0]
+        v[1] = m[0][1] * m[1][0] * m[2][0]
+        v[2] = m[0][0] * m[1][1] * m[2][0]
+        if dim == 3:
+            v[3] = m[0][0] * m[1][0] * m[2][1]
+        cols.append(v.reshape(-1))
+    M = np.stack(cols, axis=1)
+    Q, R = np.linalg.qr(M)
+    keep = np.abs(np.diag(R)) > 1e-8 * np.abs(R[0, 0])
+    Q = (Q * np.sign(np.diag(R))[None, :])[:, keep]
+    if Q.shape[1] < N:   # too few independent monomials: complete with seeded random columns
+        rng0 = np.random.default_rng(seed + 7)
+        Q, _ = np.linalg.qr(np.concatenate([Q, rng0.standard_normal((nd * nl, N - Q.shape[1]))], axis=1))
+    Q = Q[:, :N]
+    Q[:, 0] = np.abs(Q[:, 0])
+    rng = np.random.default_rng(seed)
+    Phi = np.empty((sc.n_s, N, nd * nl))
+    for E in range(sc.n_s):
+        if rotate and N > 2:
+            G = rng.standard_normal((N - 1, N - 1))
+            O, Rg = np.linalg.qr(G)
+            O = O * np.sign(np.diag(Rg))[None, :]
+            QE = np.concatenate([Q[:, :1], Q[:, 1:] @ O], axis=1)
+        else:
+            QE = Q
+        Phi[E] = QE.T
+    return Phi
+
+
+def random_full_basis1(sc: Scenario, seed: int) -> np.ndarray:
+    """Phi1_E = seeded random orthogonal matrix of the whole local P1 space (pin: reduced = fine)."""
+    rng = np.random.default_rng(seed)
+    m = (sc.dim + 1) * sc.n_loc
+    Phi = np.empty((sc.n_s, m, m))
+    for E in range(sc.n_s):
+        Q, R = np.linalg.qr(rng.standard_normal((m, m)))
         Phi[E] = (Q * np.sign(np.diag(R))[None, :]).T
     return Phi
 
@@ -372,10 +452,26 @@ def make_basis(sc: Scenario, basis: str, seed: int) -> np.ndarray:
     raise ValueError(basis)
 
 
+def make_scenario_k1(name: str, n_steps: Optional[int] = None, basis: str = "poly1",
+                     cfl: float = 0.2) -> Scenario:
+    """Config ``name``'s seeded field, fluid and boundary data on the k = 1 fine space (NEXT-4):
+    bases over the P1 dofs (``poly1`` or ``full1``), c_F = 30, CFL 0.2 (explicit P1 DG)."""
+    sc = make_scenario(name, basis="poly", n_steps=n_steps)
+    sc.cfl = cfl
+    if basis == "full1":
+        sc.Phi1 = random_full_basis1(sc, 200 + CONFIG_INDEX[name])
+        sc.N = sc.Phi1.shape[1]
+    else:
+        sc.Phi1 = poly1_basis(sc, 200 + CONFIG_INDEX[name])
+    return sc
+
+
 def custom_scenario(nx, ny, nz, sx, sy, sz, N, *, K=None, seed=0, bc="left_right",
                     basis="poly", mu_w=1.0, mu_o=1.0, nw=2.0, no=2.0, cfl=0.5, n_steps=1,
-                    s0=None, hx=1.0, hy=1.0, hz=1.0, swr=0.0, sor=0.0) -> Scenario:
-    """Small scenarios for pins and edge cases (same recipes as the configs)."""
+                    s0=None, hx=1.0, hy=1.0, hz=1.0, swr=0.0, sor=0.0, basis1=None,
+                    c_pen=30.0) -> Scenario:
+    """Small scenarios for pins and edge cases (same recipes as the configs).  basis1: ``poly1`` /
+    ``full1`` also draws k = 1 bases (NEXT-4)."""
     dim = 3 if nz > 1 else 2
     sc = Scenario(name="custom", dim=dim, nx=nx, ny=ny, nz=nz, sx=sx, sy=sy, sz=sz, N=N,
                   hx=hx, hy=hy, hz=hz, mu_w=mu_w, mu_o=mu_o, nw=nw, no=no, swr=swr, sor=sor,
@@ -387,4 +483,9 @@ def custom_scenario(nx, ny, nz, sx, sy, sz, N, *, K=None, seed=0, bc="left_right
     sc.link_cell, sc.link_axis, sc.link_p, sc.link_s = links_for(bc, nx, ny, nz)
     sc.s0 = np.zeros(sc.n) if s0 is None else np.asarray(s0, np.float64).reshape(-1)
     sc.Phi = make_basis(sc, basis, 1000 + seed)
+    sc.c_pen = c_pen
+    if basis1 == "poly1":
+        sc.Phi1 = poly1_basis(sc, 2000 + seed)
+    elif basis1 == "full1":
+        sc.Phi1 = random_full_basis1(sc, 2000 + seed)
     return sc
