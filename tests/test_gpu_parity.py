@@ -26,6 +26,13 @@ C4_S_BAR = {20: 2e-10, 50: 1e-9}
 # divides by the largest cell flux, a difference of neighbouring pressures, so its relative error is
 # the pressure's times |p| / |dp| (~1e2-1e3 on these grids)
 DT_BAR = 1e-8
+# s after the full run: 1e-10 (BASELINE.json) except where the trajectory itself amplifies round-off
+# beyond it.  C3 on the paper-recipe (pod) bases: a 1e-14 relative perturbation of K moves s by 1.3e-11
+# after 10 steps and 1.0e-10 after 500 (GPU path against itself, rtol 1e-14;
+# profiles/r02k_c3_sens.txt), so two implementations that differ at round-off level (dense Cholesky vs
+# deflated PCG) cannot be held to 1e-10 there.  Measured against the oracle: 8.9e-10 at the default
+# rtol 5e-13, 2.2e-10 at 1e-13, 8.6e-11 at 1e-14 (profiles/r02k_c3_rtol.txt); c and p keep the 1e-10 bar.
+FULL_RUN_S_BAR = {("C3", "pod"): 2e-9}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -274,8 +281,22 @@ def test_full_run_configs(name, steps, basis):
     e = dict(dt=rel(dts, ref["dts"]), c=rel(np_(c), ref["cs"][-1]), p=rel(np_(p), ref["ps"][-1]),
              s=float(np.max(np.abs(np_(s) - ref["s"]))))
     print(f"{name} {basis} {steps} steps: " + ", ".join(f"{k} {v:.3e}" for k, v in e.items()))
-    assert e["c"] <= 1e-10 and e["p"] <= 1e-10 and e["s"] <= 1e-10
+    assert e["c"] <= 1e-10 and e["p"] <= 1e-10 and e["s"] <= FULL_RUN_S_BAR.get((name, basis), 1e-10)
     assert e["dt"] <= DT_BAR
+
+
+def test_c3_pod_tight_solver():
+    """C3 on the paper-recipe bases amplifies round-off (FULL_RUN_S_BAR): with the reduced solve
+    iterated to rtol 1e-14 the full 500-step run lands at the level of that amplification."""
+    sc = inputs.make_scenario("C3", basis="pod")
+    ref = O.run(sc, n_steps=500, keep=True)
+    ctx = ctx_for(sc, rtol=1e-14)
+    ctx.run(500)
+    s, p, c = ctx.get_state()
+    ds = float(np.max(np.abs(np_(s) - ref["s"])))
+    print(f"C3 pod 500 steps, rtol 1e-14: |ds| {ds:.3e}, rel dc {rel(np_(c), ref['cs'][-1]):.3e}")
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10 and rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert ds <= 3e-10
 
 
 @pytest.mark.parametrize("name", ["C4", "C5"])
