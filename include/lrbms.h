@@ -55,7 +55,8 @@ typedef enum {
 } lrbms_status;
 
 /* Fine grid + coarse partition + local basis size.
- * dim = 2 requires nz = sz = 1.  sx | nx, sy | ny, sz | nz.  1 <= N <= min(32, sx*sy*sz).
+ * dim = 2 requires nz = sz = 1.  sx | nx, sy | ny, sz | nz.  1 <= N <= 32; the k = 0 basis
+ * (lrbms_set_basis) needs N <= sx*sy*sz, the k = 1 basis (lrbms_k1_set_basis) N <= (dim + 1) sx*sy*sz.
  * hx, hy, hz > 0 are the cell widths (|F|/d_F and the cell volume follow from them). */
 typedef struct {
   int32_t dim, nx, ny, nz;
@@ -215,6 +216,35 @@ lrbms_status lrbms_offline_basis(lrbms_ctx *ctx, int32_t M, int32_t n_train, con
                                  int32_t horizon_steps, double cfl, double eps_pca, double rtol, void *ws,
                                  size_t bytes, double *Phi, double *tau, double *snapshots, int32_t *kept,
                                  lrbms_offline_info *info);
+
+/* NEXT-4: the online step on the k = 1 SWIP-DG fine space -- the paper's (inferred) fine
+ * discretisation: pressure eq:swipBilP P:295-303 with the penalty eq:penaltyParam P:305-310 made
+ * lambda-free by the Remark P:312-320 (sigma_F = c_F / max(mu_w, mu_n) * 2 K_1 K_2 / (K_1 + K_2), h_F =
+ * diam(F)); velocity: the normal fluxes of eq:velocityDG P:366-377; saturation: eq:saturationDG
+ * P:389-399 with eq:upwind P:400-417 (explicit Euler, two-point Gauss per direction); the limiter of
+ * P:419-469 (shock detector, flagging, gradient scales, eq:limiterMain); the reduced pressure
+ * def:coarseScalePressure P:621-631 on the P1 dofs with the mobility of the cell means.  Readings A4, A5,
+ * A25-A30.
+ * Dofs of a cell: the coefficients of 1 and of (x_a - centre_a) / h_a, a = 1..dim; P1 fields are
+ * [dim + 1][n] (dof-major, natural cell order).  Phi1 (dev): [n_s][N][(dim + 1) n_loc], entry
+ * a n_loc + l = dof a of local cell l; full row rank per subdomain is the caller's duty (a
+ * rank-deficient Phi1_E makes the block Cholesky fail: NUMERICAL).
+ * ws (dev, 256-byte aligned, >= lrbms_k1_bytes(ctx)): caller-owned, in use until the context is
+ * destroyed or lrbms_k1_set_basis is called again; Phi1 is copied into it.  Every link must lie on a
+ * domain-boundary face of its axis (they are the Dirichlet faces, A29): CONFIG otherwise.  Needs
+ * set_medium; replaces the indicator coefficients of the k = 0 basis (call lrbms_set_basis again
+ * before k = 0 steps) and resets the reduced solver's history.
+ * lrbms_k1_set_saturation: s1 (dev, [dim + 1][n]).  lrbms_k1_run: as lrbms_run; limiter = 0 skips the
+ * limiter.  lrbms_k1_get_state: s1, p1 (dev, [dim + 1][n]), c (dev, n_s N), n_flagged (host: cells the
+ * limiter flagged in the last step); NULL = skip.  lrbms_k1_stage_project: the blocks and the
+ * right-hand side of the current saturation, in the layout of lrbms_stage_project. */
+size_t       lrbms_k1_bytes(const lrbms_ctx *ctx);
+lrbms_status lrbms_k1_set_basis(lrbms_ctx *ctx, const double *Phi1, double c_pen, void *ws, size_t bytes);
+lrbms_status lrbms_k1_set_saturation(lrbms_ctx *ctx, const double *s1);
+lrbms_status lrbms_k1_run(lrbms_ctx *ctx, int32_t n_steps, double cfl, double dt_fixed, int32_t limiter,
+                          double *dt_log);
+lrbms_status lrbms_k1_get_state(lrbms_ctx *ctx, double *s1, double *p1, double *c, int32_t *n_flagged);
+lrbms_status lrbms_k1_stage_project(lrbms_ctx *ctx, double *blocks, double *r);
 
 /* Advance n_steps online steps a1..a6 on the bound stream, no host round trip per step.
  * dt_fixed > 0 overrides the CFL step (the paper's fixed N_T); otherwise

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "liblrbms.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("lrbms.cu", "lrbms_kernels.cuh", "lrbms_pcg.cuh", "lrbms_project.cuh", "lrbms_ns.cuh", "lrbms_pcg_tm.cuh", "lrbms_affine.cuh", "lrbms_fine.cuh", "lrbms_diag.cuh", "lrbms_transport.cuh", "lrbms_offline.cuh")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("lrbms.cu", "lrbms_kernels.cuh", "lrbms_pcg.cuh", "lrbms_project.cuh", "lrbms_ns.cuh", "lrbms_pcg_tm.cuh", "lrbms_affine.cuh", "lrbms_fine.cuh", "lrbms_diag.cuh", "lrbms_transport.cuh", "lrbms_offline.cuh", "lrbms_k1.cuh")]
 HEADERS = [os.path.join(ROOT, "include", "lrbms.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -42,6 +42,7 @@
 #include "lrbms_diag.cuh"
 #include "lrbms_offline.cuh"
 #include "lrbms_fine.cuh"
+#include "lrbms_k1.cuh"
 
 using namespace lrbms;
 
@@ -861,7 +862,7 @@ struct lrbms_ctx {
   Geo g{};
   Flu f{};
   int n_links = 0;
-  std::vector<int> h_sub_start, h_local, h_orig;
+  std::vector<int> h_sub_start, h_local, h_orig, h_axis, h_side;   // h_side: -1 / +1 boundary side of the link's cell, 0: interior cell
   std::vector<double> h_geo2, h_p, h_s;
   double fpmax = 0.0;
   lrbms_solver_opts opts{5e-13, 5000, 200, 2, 8, 1};
@@ -908,6 +909,13 @@ struct lrbms_ctx {
   // stage profiling (CUDA events)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
+  // NEXT-4 (k = 1 fine space): caller-owned workspace, set by lrbms_k1_set_basis
+  char* k1ws = nullptr;
+  bool k1_ready = false, k1_sat = false;
+  int k1_cur = 0;
+  double k1_cpen = 0.0;
+  size_t k1_off[20] = {0};
+  size_t k1_smem = 0;
   // NEXT-1 (the paper's affine online variant): caller-owned profile workspace
   char* pws = nullptr;
   int prof_M = 0, prof_G = 0;
@@ -1062,7 +1070,7 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   g.n_loc = gr->sx * gr->sy * gr->sz;
   g.N = gr->N;
   g.n = (int)nll;
-  if (g.N < 1 || g.N > 32 || g.N > g.n_loc) return bad("need 1 <= N <= min(32, n_loc)");
+  if (g.N < 1 || g.N > 32 || g.N > (g.dim + 1) * g.n_loc) return bad("need 1 <= N <= min(32, (dim + 1) n_loc)");
   if (g.n_loc > 4096) return bad("n_loc > 4096 not supported");
   g.lstride[0] = 1; g.lstride[1] = g.s[0]; g.lstride[2] = g.s[0] * g.s[1];
   g.Estride[0] = 1; g.Estride[1] = g.S[0]; g.Estride[2] = g.S[0] * g.S[1];
@@ -1108,6 +1116,14 @@ lrbms_status lrbms_create(const lrbms_grid* gr, const lrbms_fluid* fl, const lrb
   for (auto& r : recs) {
     c->h_local.push_back(r.l);
     c->h_orig.push_back(r.orig);
+    c->h_axis.push_back(r.axis);
+    {
+      const int cell = lk->cell[r.orig];
+      const int ijk[3] = {cell % g.nx, (cell / g.nx) % g.ny, cell / (g.nx * g.ny)};
+      const int nxyz[3] = {g.nx, g.ny, g.nz};
+      c->h_side.push_back(nxyz[r.axis] > 1 && ijk[r.axis] == 0 ? -1
+                          : (nxyz[r.axis] > 1 && ijk[r.axis] == nxyz[r.axis] - 1 ? 1 : 0));
+    }
     c->h_geo2.push_back(g.geo2[r.axis]);
     c->h_p.push_back(lk->p[r.orig]);
     c->h_s.push_back(lk->s_ext[r.orig]);
@@ -1413,6 +1429,7 @@ lrbms_status lrbms_set_basis(lrbms_ctx* c, const double* Phi) {
   if (st) return st;
   if (!Phi) return fail(c, LRBMS_E_CONFIG, "Phi is NULL");
   const Geo& g = c->g;
+  if (g.N > g.n_loc) return fail(c, LRBMS_E_CONFIG, "k = 0 basis: need N <= n_loc");
   CUDA_TRY(c, cudaMemcpyAsync(c->at<double>(c->Phi), Phi, c->Phi.bytes, cudaMemcpyDeviceToDevice, c->stream));
   k_basis_indicator<<<g.n_s, 256, 0, c->stream>>>(g, c->at<double>(c->Phi), c->at<double>(c->zc));
   LAUNCH_CHECK(c);
@@ -2292,6 +2309,271 @@ lrbms_status lrbms_offline_basis(lrbms_ctx* c, int32_t M, int32_t n_train, const
     info->tof_sweeps = sweeps;
     info->fine_cg_iters = it[1];
   }
+  return LRBMS_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-4: the k = 1 fine space
+// workspace slots: 0 Phi1, 1 fk, 2 lam, 3 s1 (a), 4 s1 (b), 5 sbar, 6 p1, 7 Fhi, 8 Flo, 9 Flink,
+// 10 l_axis, 11 l_side, 12 l_c1, 13 l_kl, 14 lfirst, 15 nflag
+static void k1_layout(const lrbms_ctx* c, size_t* offs, size_t* total) {
+  const Geo& g = c->g;
+  const size_t n = g.n, nd = g.dim + 1, nl = (size_t)std::max(c->n_links, 1);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  offs[0] = take((size_t)g.n_s * g.N * nd * g.n_loc * 8);
+  offs[1] = take(n * 3 * 16);
+  offs[2] = take(n * 8);
+  offs[3] = take(nd * n * 8); offs[4] = take(nd * n * 8); offs[5] = take(nd * n * 8); offs[6] = take(nd * n * 8);
+  offs[7] = take(3 * n * 8); offs[8] = take(3 * n * 8);
+  offs[9] = take(nl * 8);
+  offs[10] = take(nl * 4); offs[11] = take(nl * 4);
+  offs[12] = take(nl * 8); offs[13] = take(nl * 8);
+  offs[14] = take(n * 4);
+  offs[15] = take(256);
+  *total = off;
+}
+
+static K1Args k1_args(lrbms_ctx* c) {
+  const Geo& g = c->g;
+  K1Args A;
+  memset(&A, 0, sizeof A);
+  A.g = g; A.f = c->f; A.L = links_of(c);
+  A.nd = g.dim + 1;
+  A.NP = (g.N + 7) / 8 * 8;
+  int ld = A.nd * K1_CH;
+  while (ld % 16 != 4) ++ld;
+  A.LDK = ld;
+  A.cpm = c->k1_cpen / std::max(c->f.mu_w, c->f.mu_o);
+  // cell widths from the stored geometry: geo[a] = |F_a| / h_a and vol = |F_a| h_a
+  double hh[3];
+  for (int a = 0; a < 3; ++a) hh[a] = std::sqrt(g.vol / g.geo[a]);
+  double d2 = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    A.h[a] = hh[a];
+    A.area[a] = g.vol / hh[a];
+    A.inv_h2[a] = 1.0 / (hh[a] * hh[a]);
+    double t2 = 0.0;
+    for (int t = 0; t < g.dim; ++t)
+      if (t != a) t2 += hh[t] * hh[t];
+    A.hF[a] = std::sqrt(t2);   // h_F = diam(F)
+    if (a < g.dim) d2 += hh[a] * hh[a];
+  }
+  A.det_scale = 1.0 / (0.08 * g.dim * std::sqrt(std::sqrt(d2)) * g.vol);
+  char* b = c->k1ws;
+  const size_t* o = c->k1_off;
+  A.Phi1 = reinterpret_cast<const double*>(b + o[0]);
+  A.fk = reinterpret_cast<const double2*>(b + o[1]);
+  A.lam = reinterpret_cast<const double*>(b + o[2]);
+  A.lam_out = reinterpret_cast<double*>(b + o[2]);
+  A.s1 = reinterpret_cast<const double*>(b + o[c->k1_cur ? 4 : 3]);
+  A.s1_out = reinterpret_cast<double*>(b + o[c->k1_cur ? 3 : 4]);
+  A.sbar = reinterpret_cast<double*>(b + o[5]);
+  A.p1 = reinterpret_cast<double*>(b + o[6]);
+  A.Fhi = reinterpret_cast<double*>(b + o[7]);
+  A.Flo = reinterpret_cast<double*>(b + o[8]);
+  A.Flink = reinterpret_cast<double*>(b + o[9]);
+  A.l_axis = reinterpret_cast<const int*>(b + o[10]);
+  A.l_side = reinterpret_cast<const int*>(b + o[11]);
+  A.l_c1 = reinterpret_cast<const double*>(b + o[12]);
+  A.l_kl = reinterpret_cast<const double*>(b + o[13]);
+  A.lfirst = reinterpret_cast<const int*>(b + o[14]);
+  A.nflag = reinterpret_cast<int*>(b + o[15]);
+  A.K = c->at<double>(c->K);
+  A.phiV = c->have_phi ? c->at<double>(c->phiV) : nullptr;
+  A.c = c->at<double>(c->c);
+  A.blocks = c->at<double>(c->blocks);
+  A.rhs = c->at<double>(c->rhs);
+  A.dt_bits = (unsigned long long*)c->at<double>(c->scal);
+  A.t_acc = c->at<double>(c->scal) + 1;
+  A.flags = c->at<int>(c->flags);
+  A.fpmax = c->fpmax;
+  return A;
+}
+
+static void reset_solver_history(lrbms_ctx* c) {
+  c->solves = 0;
+  c->hist_count = 0;
+  c->hist_head = KHIST - 1;
+  c->steps = 0;
+  c->total_iters = 0;
+  c->last_iters = 0;
+  c->last_rebuild_step = -1;
+  c->have_x = false;
+  c->have_blocks = false;
+}
+
+static lrbms_status k1_ready(lrbms_ctx* c, bool need_sat) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!c->k1_ready) return fail(c, LRBMS_E_STATE, "lrbms_k1_set_basis must precede the k = 1 calls");
+  if (need_sat && !c->k1_sat) return fail(c, LRBMS_E_STATE, "lrbms_k1_set_saturation must precede the k = 1 step");
+  return LRBMS_OK;
+}
+
+static lrbms_status k1_launch_project(lrbms_ctx* c) {
+  StageScope sc_(c, 0);
+  K1Args A = k1_args(c);
+  k1_project<<<c->g.n_s, 512, c->k1_smem, c->stream>>>(A);
+  LAUNCH_CHECK(c);
+  c->have_blocks = true;
+  return LRBMS_OK;
+}
+
+size_t lrbms_k1_bytes(const lrbms_ctx* c) {
+  if (!c) return 0;
+  size_t offs[20], total;
+  k1_layout(c, offs, &total);
+  return total;
+}
+
+lrbms_status lrbms_k1_set_basis(lrbms_ctx* c, const double* Phi1, double c_pen, void* ws, size_t bytes) {
+  lrbms_status st = check_ctx(c);
+  if (st) return st;
+  if (!c->have_medium) return fail(c, LRBMS_E_STATE, "set_medium must precede lrbms_k1_set_basis");
+  if (!Phi1) return fail(c, LRBMS_E_CONFIG, "Phi1 is NULL");
+  if (!(c_pen > 0)) return fail(c, LRBMS_E_CONFIG, "the penalty constant c_F must be > 0");
+  size_t total;
+  k1_layout(c, c->k1_off, &total);
+  if (!ws || bytes < total || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return fail(c, LRBMS_E_CONFIG, "k = 1 workspace missing, smaller than lrbms_k1_bytes or not 256-byte aligned");
+  for (int q = 0; q < c->n_links; ++q)
+    if (c->h_side[q] == 0)
+      return fail(c, LRBMS_E_CONFIG, "k = 1: link %d is not on a boundary face of its axis (Dirichlet faces only, A29)",
+                  c->h_orig[q]);
+  const Geo& g = c->g;
+  c->k1ws = static_cast<char*>(ws);
+  c->k1_cpen = c_pen;
+  c->k1_cur = 0;
+  K1Args A = k1_args(c);
+  c->k1_smem = 8 * (2 * (size_t)A.NP * A.LDK + 19 * (size_t)K1_CH) + 4 * 8 * (size_t)K1_CH;
+  CUDA_TRY(c, cudaFuncSetAttribute(k1_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->k1_smem));
+  const size_t* o = c->k1_off;
+  CUDA_TRY(c, cudaMemcpyAsync(c->k1ws + o[0], Phi1, (size_t)g.n_s * g.N * A.nd * g.n_loc * 8, cudaMemcpyDeviceToDevice,
+                              c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->k1ws + o[10], c->h_axis.data(), 4 * (size_t)c->n_links, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->k1ws + o[11], c->h_side.data(), 4 * (size_t)c->n_links, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->k1ws + o[14], 0xFF, 4 * (size_t)g.n, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->k1ws + o[15], 0, 256, c->stream));
+  k1_face_coef<<<cdiv(g.n, 256), 256, 0, c->stream>>>(A, c->at<double>(c->K), reinterpret_cast<double2*>(c->k1ws + o[1]));
+  LAUNCH_CHECK(c);
+  k1_link_coef<<<cdiv(g.n_s, 128), 128, 0, c->stream>>>(A, c->at<double>(c->K), reinterpret_cast<double*>(c->k1ws + o[12]),
+                                                         reinterpret_cast<double*>(c->k1ws + o[13]),
+                                                         reinterpret_cast<int*>(c->k1ws + o[14]));
+  LAUNCH_CHECK(c);
+  // the coarse space of the reduced solver: the subdomain indicators in the P1 bases (the k = 0
+  // basis, whose indicator coefficients these replace, must be set again before k = 0 steps)
+  k1_indicator<<<g.n_s, 256, 0, c->stream>>>(g, A.nd, A.Phi1, c->at<double>(c->zc));
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));   // the host link arrays may go out of scope
+  c->have_basis = false;
+  c->k1_ready = true;
+  c->k1_sat = false;
+  reset_solver_history(c);
+  invalidate_profiles(c);
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_k1_set_saturation(lrbms_ctx* c, const double* s1) {
+  lrbms_status st = k1_ready(c, false);
+  if (st) return st;
+  if (!s1) return fail(c, LRBMS_E_CONFIG, "s1 is NULL");
+  const Geo& g = c->g;
+  c->k1_cur = 0;
+  K1Args A = k1_args(c);
+  for (int a = 0; a < A.nd; ++a) {
+    k_to_internal<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, s1 + (size_t)a * g.n, const_cast<double*>(A.s1) + (size_t)a * g.n);
+    LAUNCH_CHECK(c);
+  }
+  k1_mobility<<<cdiv(g.n, 256), 256, 0, c->stream>>>(A);
+  LAUNCH_CHECK(c);
+  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->c), 0, c->c.bytes, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(A.p1, 0, (size_t)A.nd * g.n * 8, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<double>(c->scal), 0, 128, c->stream));
+  CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->iters), 0, 64, c->stream));
+  reset_solver_history(c);
+  c->k1_sat = true;
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_k1_run(lrbms_ctx* c, int32_t n_steps, double cfl, double dt_fixed, int32_t limiter, double* dt_log) {
+  lrbms_status st = k1_ready(c, true);
+  if (st) return st;
+  if (n_steps < 0) return fail(c, LRBMS_E_CONFIG, "n_steps < 0");
+  if (!(dt_fixed > 0) && !(cfl > 0)) return fail(c, LRBMS_E_CONFIG, "need cfl > 0 or dt_fixed > 0");
+  const Geo& g = c->g;
+  const int nt = std::min(256, cdiv(g.n_loc, 32) * 32);
+  // The k = 1 reduced operator couples the subdomains through the penalty, so the coarse components
+  // carry much of the solution and the deflated preconditioner (A-DEF2), which is only as symmetric as
+  // its fp32 coarse inverse is exact, stalls near 1e-9 (measured on C1, reproduced on the host with an
+  // fp32-rounded inverse).  The additive two-level preconditioner is symmetric for
+  // any symmetric coarse inverse: the k = 1 steps use it, with the inverse rebuilt every <= 20 steps.
+  struct Restore {
+    lrbms_ctx* c;
+    lrbms_solver_opts o;
+    ~Restore() { c->opts = o; }
+  } restore{c, c->opts};
+  if (c->opts.use_coarse == 2) {
+    c->opts.use_coarse = 1;
+    c->opts.coarse_refresh = std::min(c->opts.coarse_refresh, 20);
+  }
+  for (int k = 0; k < n_steps; ++k) {
+    if ((st = k1_launch_project(c))) return st;
+    if ((st = launch_solve(c))) return st;
+    K1Args A = k1_args(c);
+    A.cfl = cfl; A.dt_fixed = dt_fixed; A.dt_log = dt_log; A.step = k; A.limiter = limiter;
+    {
+      StageScope sc_(c, 5);
+      k1_recon<<<g.n_s, 256, 0, c->stream>>>(A);
+      LAUNCH_CHECK(c);
+    }
+    {
+      StageScope sc_(c, 6);
+      k1_flux<<<g.n_s, nt, 0, c->stream>>>(A);
+      LAUNCH_CHECK(c);
+    }
+    {
+      StageScope sc_(c, 7);
+      k1_transport<<<g.n_s, nt, 0, c->stream>>>(A);
+      LAUNCH_CHECK(c);
+      k1_limit<<<g.n_s, nt, 0, c->stream>>>(A);
+      LAUNCH_CHECK(c);
+    }
+    c->k1_cur ^= 1;
+    c->steps++;
+  }
+  return finish(c, n_steps);
+}
+
+lrbms_status lrbms_k1_get_state(lrbms_ctx* c, double* s1, double* p1, double* cc, int32_t* n_flagged) {
+  lrbms_status st = k1_ready(c, true);
+  if (st) return st;
+  const Geo& g = c->g;
+  K1Args A = k1_args(c);
+  for (int a = 0; a < A.nd; ++a) {
+    if (s1) {
+      k_to_natural<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, A.s1 + (size_t)a * g.n, s1 + (size_t)a * g.n);
+      LAUNCH_CHECK(c);
+    }
+    if (p1) {
+      k_to_natural<<<cdiv(g.n, 256), 256, 0, c->stream>>>(g, A.p1 + (size_t)a * g.n, p1 + (size_t)a * g.n);
+      LAUNCH_CHECK(c);
+    }
+  }
+  if (cc) CUDA_TRY(c, cudaMemcpyAsync(cc, c->at<double>(c->c), c->c.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  int nf = 0;
+  CUDA_TRY(c, cudaMemcpyAsync(&nf, A.nflag, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (n_flagged) *n_flagged = nf;
+  return LRBMS_OK;
+}
+
+lrbms_status lrbms_k1_stage_project(lrbms_ctx* c, double* blocks, double* r) {
+  lrbms_status st = k1_ready(c, true);
+  if (st) return st;
+  if ((st = k1_launch_project(c))) return st;
+  if (blocks) CUDA_TRY(c, cudaMemcpyAsync(blocks, c->at<double>(c->blocks), c->blocks.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  if (r) CUDA_TRY(c, cudaMemcpyAsync(r, c->at<double>(c->rhs), c->rhs.bytes, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return LRBMS_OK;
 }
 

@@ -25,7 +25,8 @@ EXPORTS = ["lrbms_create", "lrbms_workspace_bytes", "lrbms_bind", "lrbms_set_med
            "lrbms_get_stats", "lrbms_set_profiling", "lrbms_get_stage_times", "lrbms_launch_count", "lrbms_last_error", "lrbms_version", "lrbms_destroy",
            "lrbms_profiles_bytes", "lrbms_set_profiles", "lrbms_set_online", "lrbms_stage_theta",
            "lrbms_fine_bytes", "lrbms_run_fine", "lrbms_diagnostics", "lrbms_offline_bytes",
-           "lrbms_offline_basis"]
+           "lrbms_offline_basis", "lrbms_k1_bytes", "lrbms_k1_set_basis", "lrbms_k1_set_saturation",
+           "lrbms_k1_run", "lrbms_k1_get_state", "lrbms_k1_stage_project"]
 
 
 class LrbmsError(RuntimeError):
@@ -118,6 +119,12 @@ def load_library(path: str = LIB_PATH):
         "lrbms_offline_bytes": (ctypes.c_size_t, [P, I]),
         "lrbms_offline_basis": (st, [P, I, I, P, I, D, D, D, P, ctypes.c_size_t, P, P, P, P,
                                      ctypes.POINTER(OfflineInfo)]),
+        "lrbms_k1_bytes": (ctypes.c_size_t, [P]),
+        "lrbms_k1_set_basis": (st, [P, P, D, P, ctypes.c_size_t]),
+        "lrbms_k1_set_saturation": (st, [P, P]),
+        "lrbms_k1_run": (st, [P, I, D, D, I, P]),
+        "lrbms_k1_get_state": (st, [P, P, P, P, ctypes.POINTER(ctypes.c_int32)]),
+        "lrbms_k1_stage_project": (st, [P, P, P]),
         "lrbms_get_stage_times": (st, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), I]),
         "lrbms_last_error": (ctypes.c_char_p, [P]),
         "lrbms_version": (ctypes.c_char_p, []),
@@ -144,7 +151,7 @@ class LrbmsContext:
     partition sizes, fluid constants, links (cell, axis, p, s_ext), K, phi, Phi, s0.
     """
 
-    def __init__(self, sc, device="cuda", stream=None, solver: Optional[dict] = None):
+    def __init__(self, sc, device="cuda", stream=None, solver: Optional[dict] = None, k1_only: bool = False):
         import torch
 
         if not torch.cuda.is_available():
@@ -182,8 +189,9 @@ class LrbmsContext:
         if solver:
             self.set_solver(**solver)
         self.set_medium(sc.K, sc.phi)
-        self.set_basis(sc.Phi)
-        self.set_saturation(sc.s0)
+        if not k1_only:   # k1_only: a context for the k = 1 fine space alone (NEXT-4; N may exceed n_loc)
+            self.set_basis(sc.Phi)
+            self.set_saturation(sc.s0)
 
     # -- helpers -----------------------------------------------------------------------------
     def _check(self, status):
@@ -358,6 +366,46 @@ class LrbmsContext:
             kept.ctypes.data_as(ctypes.c_void_p), ctypes.byref(info)))
         del ws
         return Phi, kept, {k: getattr(info, k) for k, _ in OfflineInfo._fields_}, tau, snaps
+
+    # -- NEXT-4: the k = 1 fine space (marshalling only) ----------------------------------------
+    def k1_set_basis(self, Phi1, c_pen=None):
+        torch = self.torch
+        sc = self.sc
+        nbytes = self.L.lrbms_k1_bytes(self.h)
+        with torch.cuda.device(self.device):
+            self.k1_ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        ptr = (self.k1_ws.data_ptr() + 255) // 256 * 256
+        t = self.dev(Phi1)
+        assert t.numel() == sc.n_s * sc.N * (sc.dim + 1) * sc.n_loc, "Phi1 must be [n_s][N][(dim + 1) n_loc]"
+        self._check(self.L.lrbms_k1_set_basis(self.h, _ptr(t), float(sc.c_pen if c_pen is None else c_pen),
+                                              ctypes.c_void_p(ptr), nbytes))
+
+    def k1_set_saturation(self, s1):
+        t = self.dev(np.asarray(s1, np.float64).reshape(self.sc.dim + 1, self.sc.n))
+        self._check(self.L.lrbms_k1_set_saturation(self.h, _ptr(t)))
+        self.stream.synchronize()
+
+    def k1_run(self, n_steps, cfl=None, dt_fixed=0.0, limiter=True, log_dt=False):
+        cfl = self.sc.cfl if cfl is None else cfl
+        dt_log = self.empty(max(n_steps, 1)) if log_dt else None
+        self._check(self.L.lrbms_k1_run(self.h, int(n_steps), float(cfl), float(dt_fixed), 1 if limiter else 0,
+                                        _ptr(dt_log)))
+        return dt_log[:n_steps] if log_dt else None
+
+    def k1_get_state(self):
+        sc = self.sc
+        nd = sc.dim + 1
+        s1, p1, c = self.empty(nd, sc.n), self.empty(nd, sc.n), self.empty(sc.n_s, sc.N)
+        nf = ctypes.c_int32(0)
+        self._check(self.L.lrbms_k1_get_state(self.h, _ptr(s1), _ptr(p1), _ptr(c), ctypes.byref(nf)))
+        return s1, p1, c, int(nf.value)
+
+    def k1_stage_project(self):
+        sc = self.sc
+        blocks = self.empty(sc.n_s, 1 + sc.dim, sc.N, sc.N)
+        r = self.empty(sc.n_s, sc.N)
+        self._check(self.L.lrbms_k1_stage_project(self.h, _ptr(blocks), _ptr(r)))
+        return blocks, r
 
     def diagnostics(self) -> dict:
         """K6 diagnostics of the last step (lrbms_diagnostics): mass, s range, zeta, coarse defect."""
