@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--rtol", type=float, default=None)
     ap.add_argument("--fine-steps", type=int, default=5,
                     help="steps timed in the fine-scale reference scheme (NEXT-2, Phi_E = I; 0 = skip)")
+    ap.add_argument("--k1-steps", type=int, default=10,
+                    help="steps of the k = 1 fine-space variant (NEXT-4) timed as an extra key (0 = skip)")
     ap.add_argument("--affine-steps", type=int, default=50,
                     help="steps timed in the paper's affine online variant (NEXT-1; 0 = skip)")
     return ap.parse_args()
@@ -461,6 +463,52 @@ def run_ours(args, rank, local, world):
                            "seeded field generation)"}
         del Pg, Ph
 
+    # ---- NEXT-4: the online step on the k = 1 SWIP-DG fine space (P1 transport + limiter) on the same
+    #      grid, medium, fluid and wells (polynomial P1 bases; its own context)
+    k1 = None
+    if args.k1_steps > 0:
+        sc1 = inputs.make_scenario_k1(args.config)
+        ctx1 = LrbmsContext(sc1, device=device, k1_only=True)
+        ctx1.k1_set_basis(sc1.Phi1)
+        s1_0 = np.zeros((sc1.dim + 1, sc1.n))
+        s1_0[0] = sc1.s0
+        ctx1.k1_set_saturation(s1_0)
+        ctx1.k1_run(3)
+        barrier(world)
+        torch.cuda.synchronize()
+        st0 = ctx1.stats()
+        e8 = torch.cuda.Event(enable_timing=True)
+        e9 = torch.cuda.Event(enable_timing=True)
+        e8.record(stream)
+        ctx1.k1_run(args.k1_steps)
+        e9.record(stream)
+        torch.cuda.synchronize()
+        ms_1 = max_over_ranks(e8.elapsed_time(e9), world, device)
+        st1 = ctx1.stats()
+        ctx1.set_profiling(True)
+        ctx1.k1_run(args.k1_steps)
+        torch.cuda.synchronize()
+        st_1 = ctx1.stage_times()
+        ctx1.set_profiling(False)
+        nflag = ctx1.k1_get_state()[3]
+        nd = sc1.dim + 1
+        # algorithmic bytes of the k = 1 projection and reconstruction: one pass of Phi1 each
+        phi1_bytes = 8.0 * sc1.n_s * sc1.N * nd * sc1.n_loc
+        proj_bytes = phi1_bytes + 8.0 * sc1.n_s * (1 + sc1.dim) * sc1.N ** 2 + (48.0 + 8.0) * sc1.n
+        k1 = {"value": world * args.k1_steps / (ms_1 / 1e3), "unit": "steps/s", "ms_per_step": ms_1 / args.k1_steps,
+              "steps": args.k1_steps, "fine_dofs": nd * sc1.n, "reduced_dofs": sc1.n_s * sc1.N,
+              "pcg_iters_per_step": (st1["total_iters"] - st0["total_iters"]) / args.k1_steps,
+              "stage_us_per_step": {k: round(1e3 * v[0] / args.k1_steps, 1) for k, v in st_1.items()},
+              "limiter_flagged_cells_last_step": nflag,
+              "project_gbs": proj_bytes / (st_1["project"][0] / args.k1_steps / 1e3) / 1e9,
+              "recon_gbs": (phi1_bytes + 8.0 * nd * sc1.n) / (st_1["recon"][0] / args.k1_steps / 1e3) / 1e9,
+              "note": "lrbms_k1_run (NEXT-4): eq:swipBilP projection on the P1 dofs (k1_project, DMMA), the "
+                      "reduced solve with the additive two-level preconditioner, eq:velocityDG fluxes, "
+                      "eq:saturationDG transport and the limiter of P:419-469; stage 'transport' = transport + "
+                      "limiter; project_gbs / recon_gbs = one pass of Phi1 (+ outputs) over the stage time"}
+        ctx1.close()
+        del ctx1
+
     if rank != 0:
         return 0
 
@@ -543,6 +591,7 @@ def run_ours(args, rank, local, world):
         "affine_variant": affine,
         "fine_reference": fine,
         "offline_gpu": offline,
+        "k1_variant": k1,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
