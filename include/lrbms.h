@@ -184,7 +184,7 @@ lrbms_status lrbms_run_fine(lrbms_ctx *ctx, int32_t n_steps, double cfl, double 
 /* NEXT-3: the offline basis recipe on the GPU -- the initialisation of
  * alg:lrbmsBasisConstruction, the training set, the fine snapshots
  * and the per-subdomain data compression (PCA) with the coarse unit functions
- * (P:1110-1111).  Its host reference is offline/recipe.py (readings A25/A26):
+ * (P:1110-1111).  Its host reference is offline/recipe.py (readings A31/A32):
  *   1. the fine pressure at the current saturation s0 (the NEXT-2 solver, rtol) and the CFL step dt0 of
  *      its fluxes (reading R4, f'_max of the context's fluid);
  *   2. the time of flight of eq:timeOfFlight at k = 0 (upwind DG0; solved by relaxation
@@ -282,7 +282,7 @@ lrbms_status lrbms_get_stats(lrbms_ctx *ctx, lrbms_stats *out);
  * fixed-order sum, deterministic; synchronises the stream).  Needs a step since set_saturation
  * (STATE otherwise).  zeta is the paper's relative mass loss of the step's velocity,
  * zeta(T) = |int_dT u.n dS| / max_{x in dT} |u(x)|, with u.n on a face or link its
- * flux density F/|F| (A27); 0 for the fine scheme, > 0 for reduced bases.
+ * flux density F/|F| (A33); 0 for the fine scheme, > 0 for reduced bases.
  * coarse_defect = max_E |sum_{i in E} int_dT_i u.n| (0 when 1_E is in span Phi_E).
  * mass_balance = |mass - mass_prev + dt water_out| / max(mass, mass_prev) (pin P3: round-off). */
 typedef struct {

@@ -13,13 +13,13 @@ of P:663-670 / P:1026-1028, the fine snapshots of P:679-680 and the
   1. fine pressure and velocity at s = S0 (P:644-646, def:pressureDG P:337-345 at k = 0, R2);
   2. time of flight (eq:timeOfFlight P:505-512 at k = 0: upwind DG0, solved cell by cell in
      descending-pressure order -- the flow-ordered back-substitution of P:517-521);
-  3. M mobility profiles lambda_{alpha,q} (P:650-662) with the horizon T = n_steps * dt^0 (A25);
+  3. M mobility profiles lambda_{alpha,q} (P:650-662) with the horizon T = n_steps * dt^0 (A31);
   4. 2N training parameters mu in the simplex (normalised exponentials clamped at 1e-4, S:528);
   5. fine snapshots p(lambda^(j)), lambda_alpha^(j) = sum_q mu_q lambda_{alpha,q} (P:679-680);
   6. per subdomain: the snapshot restrictions with the normalised indicator v0 projected out, their
      thin SVD (POD without mean subtraction), Phi_E = [v0, leading left singular vectors]
      (P:706-719); modes below the noise floor are not kept, and a rank-deficient Phi_E
-     is completed by graded monomials orthogonalised against it (reading A26).
+     is completed by graded monomials orthogonalised against it (reading A32).
 
 fp64 NumPy/SciPy.  Fine solves: sparse LU (SuperLU) up to 300k cells; above, a two-level PCG
 (Jacobi + subdomain-indicator coarse space) to a relative residual of 1e-14, snapshots in parallel
@@ -349,7 +349,7 @@ def pod_bases(sc, P, N, eps_pca=1e-8):
     singular vectors in decreasing singular value, each signed so that its largest-magnitude entry
     is positive.  A mode is kept if sigma > eps_pca * sigma_ref, sigma_ref the largest Y_E singular
     value over all subdomains (the snapshots' noise floor is global).  If fewer than N - 1 modes
-    remain, Phi_E is completed by graded monomials orthogonalised against it (A26).
+    remain, Phi_E is completed by graded monomials orthogonalised against it (A32).
     Returns (Phi [n_s][N][n_loc], kept [n_s]: POD modes kept per subdomain)."""
     nl = sc.n_loc
     v0 = np.full(nl, 1.0 / np.sqrt(nl))

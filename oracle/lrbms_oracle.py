@@ -575,7 +575,7 @@ def cell_net_outflow(sc, Ff, Fl):
 def relative_mass_loss(sc, Ff, Fl):
     """zeta(T) = |int_{dT} u.n dS| / max_{x in dT} |u(x)|.  At k = 0 the velocity on a
     face is represented by its normal flux density F_F/|F|, so the max runs over the cell's faces and
-    links (reading A27)."""
+    links (reading A33)."""
     a, b, ax = interior_faces(sc)
     area = face_areas(sc)
     umax = np.zeros(sc.n)

@@ -1224,7 +1224,10 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     int prio_lo = 0, prio_hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     // low priority: the initial-guess kernels on the main stream are the longer path of the overlap
-    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
+#ifndef SIDE_PRIO_HI
+#define SIDE_PRIO_HI 0
+#endif
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, SIDE_PRIO_HI ? prio_hi : prio_lo));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->cpy, cudaStreamNonBlocking, prio_hi));
@@ -1673,7 +1676,10 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
     const bool rebuild = !c->have_x || c->last_rebuild_step < 0 ||
                          c->steps - c->last_rebuild_step >= c->opts.coarse_refresh;
     cudaStream_t main = c->stream;
-    if (!rebuild && mode == 2 && c->side) {
+#ifndef NO_SIDE
+#define NO_SIDE 0
+#endif
+    if (!NO_SIDE && !rebuild && mode == 2 && c->side) {
       CUDA_TRY(c, cudaEventRecord(c->fork_ev, main));
       CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->fork_ev, 0));
       c->stream = c->side;

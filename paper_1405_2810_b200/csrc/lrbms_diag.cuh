@@ -3,7 +3,7 @@
 // On the state after a step (p^n of the step, lambda(s^n), f(s^n), s^n and s^{n+1} still in the
 // double buffers): the water volume before and after (eq:saturationDG conserves it up to the link
 // fluxes: pin P3), the saturation range, the relative mass loss of the reduced velocity
-//   zeta(T) = |int_dT u.n dS| / max_{x in dT} |u(x)|            (reading A27)
+//   zeta(T) = |int_dT u.n dS| / max_{x in dT} |u(x)|            (reading A33)
 // (its maximum and mean over the cells), the coarse conservation defect max_E |sum_{i in E} div_i|
 // (0 when 1_E is in span Phi_E: P4), the water leaving through links, and the total link
 // in- and outflow.  One CTA per subdomain writes fixed-order partials; k_diag_final sums them in

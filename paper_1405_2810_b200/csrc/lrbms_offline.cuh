@@ -15,7 +15,7 @@
 //   5. per subdomain: Y = (I - v0 v0^T) P|_E, its thin SVD by one-sided (Hestenes) Jacobi rotations on
 //      the snapshot columns (accurate singular vectors down to eps ||Y||, which the Gram-matrix route
 //      would lose), Phi_E = [v0, left singular vectors above the noise floor, graded monomials
-//      orthogonalised against them up to N] (reading A26).
+//      orthogonalised against them up to N] (reading A32).
 #pragma once
 #include "lrbms_kernels.cuh"
 
