@@ -1262,14 +1262,18 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   }
   {  // on-chip PCG: one warp per subdomain, at most 14 warps (448 threads) per CTA, one CTA per SM
     c->tm_W = 0;
-    const int W = cdiv(c->g.n_s, sms);
-    if (W <= 14 && c->g.N <= 32) {
+    // small configurations (n_s <= 16): ONE CTA with a warp per subdomain, so that the three grid
+    // synchronisations of an iteration are CTA barriers (no L2 round trips): C1, C2
+    const bool single = c->g.n_s <= 16;
+    const int W = single ? c->g.n_s : cdiv(c->g.n_s, sms);
+    if (W <= (single ? 16 : 14) && c->g.N <= 32) {
       const int G = cdiv(c->g.n_s, W);
       const TmLayout Ls = tm_layout(W, c->g.dim, c->n_pad);
       if (Ls.total <= 227 * 1024 - 1024) {
         // at least 116 KB so that no two CTAs share an SM (each allocates all 512 TMEM columns)
         const size_t smem = std::max<size_t>(Ls.total, 116 * 1024);
-        c->tm_fn = c->g.N == 32 ? (const void*)k_pcg_tm<32> : (const void*)k_pcg_tm<0>;
+        c->tm_fn = single ? (const void*)k_pcg_tm<0, 512>
+                          : (c->g.N == 32 ? (const void*)k_pcg_tm<32> : (const void*)k_pcg_tm<0>);
         CUDA_TRY(c, cudaFuncSetAttribute(c->tm_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int occ_tm = 0;
         CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tm, c->tm_fn, 32 * W, smem));
@@ -1330,7 +1334,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     int optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const void* fns[] = {(const void*)k_pcg, (const void*)k_pcg_tm<32>, (const void*)k_pcg_tm<0>,
-                         (const void*)k_coarse_gj32, (const void*)k_project<0, 0, 0, 0>, (const void*)k_project<32, 8, 8, 8>,
+                         (const void*)k_pcg_tm<0, 512>, (const void*)k_coarse_gj32, (const void*)k_project<0, 0, 0, 0>, (const void*)k_project<32, 8, 8, 8>,
                          (const void*)k_flux_cfl, (const void*)k_coarse_rt_s, (const void*)k_ns_gemm_tc,
                          (const void*)k_ns_gemm};
     for (const void* fn : fns) {

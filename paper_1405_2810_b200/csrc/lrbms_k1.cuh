@@ -223,16 +223,20 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
           if (a < nd) y[a] += vol * A.inv_h2[a - 1] * v[a];
         // Dirichlet faces of the cell (links, A29): the one-sided face terms
         for (int q = tl[lc]; q >= 0 && q < lq1 && A.L.local[q] == l; ++q) {
-          const int ax = A.l_axis[q];
+          const int axq = A.l_axis[q];
           const double sg = (double)A.l_side[q], c1 = A.l_c1[q], kl = A.l_kl[q] * A.lam[base + l];
-          const double j0 = v[0] + 0.5 * sg * v[1 + ax];
-          const double DN = kl * sg * v[1 + ax];
-          const double G = c1 * j0 - DN;
-          y[0] += G;
-          y[1 + ax] += 0.5 * sg * G - kl * sg * j0;
 #pragma unroll
-          for (int t = 0; t < 3; ++t)
-            if (t != ax && 1 + t < nd) y[1 + t] += c1 * (1.0 / 12.0) * v[1 + t];
+          for (int ax = 0; ax < 3; ++ax) {   // compile-time dof indices
+            if (ax != axq) continue;
+            const double j0 = v[0] + 0.5 * sg * v[1 + ax];
+            const double DN = kl * sg * v[1 + ax];
+            const double G = c1 * j0 - DN;
+            y[0] += G;
+            y[1 + ax] += 0.5 * sg * G - kl * sg * j0;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+              if (t != ax && 1 + t < nd) y[1 + t] += c1 * (1.0 / 12.0) * v[1 + t];
+          }
         }
       }
 #pragma unroll
@@ -314,7 +318,9 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
             if (q < nd) { v[q] = pm[(size_t)q * nl]; w[q] = pn[(size_t)q * nl]; }
           // rows of the own cell (T1) for a function supported on the upper cell (T2) only
           const double zero[4] = {0.0, 0.0, 0.0, 0.0};
-          k1_face_rows(nd, a, true, tc1[lc], tko[lc], tkn[lc], zero, w, y);
+          if (a == 0) k1_face_rows(nd, 0, true, tc1[lc], tko[lc], tkn[lc], zero, w, y);   // compile-time dof indices
+          else if (a == 1) k1_face_rows(nd, 1, true, tc1[lc], tko[lc], tkn[lc], zero, w, y);
+          else k1_face_rows(nd, 2, true, tc1[lc], tko[lc], tkn[lc], zero, w, y);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -480,8 +486,11 @@ __global__ void __launch_bounds__(256) k1_transport(K1Args A) {
           R[1 + a] += wv * ua * fv / A.h[a];
         }
     }
-    // interior faces
-    for (int a = 0; a < dim; ++a) {
+    // interior faces (axis and side unrolled: the dof arrays stay in registers)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a >= dim) continue;
+#pragma unroll
       for (int up = 0; up < 2; ++up) {
         const int nb = neighbour(g, E, C, l, c, a, up ? +1 : -1);
         if (nb < 0) continue;
@@ -520,24 +529,28 @@ __global__ void __launch_bounds__(256) k1_transport(K1Args A) {
     }
     // Dirichlet faces: n outward; chi = s_D on inflow (F < 0), the cell's trace on outflow
     for (int q = A.lfirst[gi]; q >= 0 && q < q1 && A.L.local[q] == l; ++q) {
-      const int a = A.l_axis[q];
+      const int aq = A.l_axis[q];
       const double sg = (double)A.l_side[q], F = A.Flink[q];
-      for (int k = 0; k < ntp; ++k) {
-        double x[3] = {0.0, 0.0, 0.0};
-        int bit = ntp >> 1;
 #pragma unroll
-        for (int t = 0; t < 3; ++t)
-          if (t != a && t < dim) {
-            x[t] = (k & bit) ? K1_GP : -K1_GP;
-            bit >>= 1;
-          }
-        const double su = F >= 0.0 ? k1_trace(nd, s, a, sg, x) : A.L.s_ext[q];
-        const double gq = F * wf * frac_flow(A.f, su);
-        R[0] -= gq;
-        R[1 + a] -= 0.5 * sg * gq;
+      for (int a = 0; a < 3; ++a) {
+        if (a != aq) continue;
+        for (int k = 0; k < ntp; ++k) {
+          double x[3] = {0.0, 0.0, 0.0};
+          int bit = ntp >> 1;
 #pragma unroll
-        for (int t = 0; t < 3; ++t)
-          if (t != a && t < dim) R[1 + t] -= gq * x[t];
+          for (int t = 0; t < 3; ++t)
+            if (t != a && t < dim) {
+              x[t] = (k & bit) ? K1_GP : -K1_GP;
+              bit >>= 1;
+            }
+          const double su = F >= 0.0 ? k1_trace(nd, s, a, sg, x) : A.L.s_ext[q];
+          const double gq = F * wf * frac_flow(A.f, su);
+          R[0] -= gq;
+          R[1 + a] -= 0.5 * sg * gq;
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+            if (t != a && t < dim) R[1 + t] -= gq * x[t];
+        }
       }
     }
     const double pv = A.phiV ? A.phiV[gi] : g.vol;
@@ -589,9 +602,14 @@ __global__ void __launch_bounds__(256) k1_limit(K1Args A) {
       double S = 0.0;
       double nbm[6], nbx[6];
       bool has[6];
-      for (int a = 0; a < dim; ++a)
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
         for (int up = 0; up < 2; ++up) {
           const int d = 2 * a + up;
+          has[d] = false;
+          nbm[d] = nbx[d] = 0.0;
+          if (a >= dim) continue;
           const int nb = neighbour(g, E, C, l, c, a, up ? +1 : -1);
           has[d] = nb >= 0;
           nbm[d] = nbx[d] = 0.0;
@@ -610,7 +628,8 @@ __global__ void __launch_bounds__(256) k1_limit(K1Args A) {
         if (A.Flink[q] < 0.0) {
           const int a = A.l_axis[q];
           const double sg = (double)A.l_side[q];
-          S += A.area[a] * fabs(s[0] + 0.5 * sg * s[1 + a] - A.L.s_ext[q]) * A.det_scale;
+          const double sl = a == 0 ? s[1] : (a == 1 ? s[2] : s[3]);
+          S += A.area[a] * fabs(s[0] + 0.5 * sg * sl - A.L.s_ext[q]) * A.det_scale;
         }
       double spread = 0.0;
 #pragma unroll
@@ -620,7 +639,9 @@ __global__ void __launch_bounds__(256) k1_limit(K1Args A) {
       const bool flagged = S > 1.0 || s[0] - spread < 0.0 || s[0] + spread > 1.0;
       if (flagged) {
         ++nfl;
-        for (int a = 0; a < dim; ++a)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
           for (int up = 0; up < 2; ++up) {
             const int d = 2 * a + up;
             if (!has[d]) continue;

@@ -186,6 +186,14 @@ __device__ __forceinline__ double grid_reduce_n(double v, double* red16, double*
   __syncthreads();
   ++epoch;
   double* ps = partials + (size_t)(epoch & 3) * G;
+  if (G == 1) {   // a single CTA (small configurations): the CTA barrier is the grid barrier
+    if (warp == 0) {
+      const double t = warp_sum(lane < W ? red16[lane] : 0.0);
+      if (lane == 0) *bc = t;
+    }
+    __syncthreads();
+    return *bc;
+  }
   if (warp == 0) {
     const double t = warp_sum(lane < W ? red16[lane] : 0.0);
     if (lane == 0) ps[blockIdx.x] = t;
@@ -201,6 +209,7 @@ __device__ __forceinline__ double grid_reduce_n(double v, double* red16, double*
 __device__ __forceinline__ void grid_barrier_n(unsigned* bar, unsigned& epoch) {
   __syncthreads();
   ++epoch;
+  if (gridDim.x == 1) return;   // a single CTA: global writes of the CTA are visible after the CTA barrier
   if ((threadIdx.x >> 5) == 0) bar_arrive_wait_n(bar, epoch);
   __syncthreads();
 }
@@ -430,8 +439,10 @@ __host__ __device__ inline TmLayout tm_layout(int W, int dim, int n_pad) {
 #define TM_SSTAMP(k) do { } while (0)
 #endif
 
-template <int NFIX>   // NFIX = 32: N known at compile time (the lane predicates fold away)
-__global__ void __launch_bounds__(448, 1) k_pcg_tm(PcgArgs A) {
+// NFIX = 32: N known at compile time (the lane predicates fold away); MAXT: the block-size bound (448:
+// 14 warps, 146 registers per thread; 512: 16 warps for the single-CTA launch of small configurations)
+template <int NFIX, int MAXT = 448>
+__global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ uint32_t tbase_s;
   __shared__ double red16[16];
