@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -1265,7 +1266,13 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     // small configurations (n_s <= 16): ONE CTA with a warp per subdomain, so that the three grid
     // synchronisations of an iteration are CTA barriers (no L2 round trips): C1, C2
     const bool single = c->g.n_s <= 16;
-    const int W = single ? c->g.n_s : cdiv(c->g.n_s, sms);
+    // otherwise at least 8 warps (two per scheduler) per CTA: fewer CTAs make the grid synchronisations
+    // cheaper (C3, 132 subdomains: 1110 us per solve with 132 one-warp CTAs, 837-878 us with 19-17 CTAs
+    // of 7-8 warps; C4: 495 us at 7 x 147, 473 us at 8 x 128; r02p sweep)
+    int W = single ? c->g.n_s : std::min(14, std::max(cdiv(c->g.n_s, sms), 8));
+#ifdef LRBMS_DEBUG
+    if (const char* e = getenv("LRBMS_TM_W")) W = std::max(W, std::min(14, atoi(e)));   // experiments only
+#endif
     if (W <= (single ? 16 : 14) && c->g.N <= 32) {
       const int G = cdiv(c->g.n_s, W);
       const TmLayout Ls = tm_layout(W, c->g.dim, c->n_pad);
@@ -2423,7 +2430,7 @@ static lrbms_status k1_ready(lrbms_ctx* c, bool need_sat) {
 static lrbms_status k1_launch_project(lrbms_ctx* c) {
   StageScope sc_(c, 0);
   K1Args A = k1_args(c);
-  k1_project<<<c->g.n_s, 512, c->k1_smem, c->stream>>>(A);
+  k1_project<<<c->g.n_s, 256, c->k1_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
   c->have_blocks = true;
   return LRBMS_OK;

@@ -10,7 +10,7 @@
 // the reduced solve (a3: block Cholesky scaling, coarse level, deflated on-chip PCG) is reused unchanged.
 //
 // Kernels of one step:
-//   k1_project   one CTA (16 warps) per subdomain: Y = A_EE Phi1_E^T formed chunk by chunk (32 cells x
+//   k1_project   one CTA (8 warps, three per SM) per subdomain: Y = A_EE Phi1_E^T formed chunk by chunk (32 cells x
 //                nd dofs) in shared memory from the face coefficients (a table per chunk), B_EE =
 //                Phi1_E Y on the fp64 tensor cores (mma.sync m8n8k4 -> DMMA, a warp per 8 x 8 output
 //                tile over the whole contraction: no cross-warp reduction, deterministic), then the
@@ -142,7 +142,7 @@ __device__ __forceinline__ void k1_face_rows(int nd, int ax, bool up, double c1,
     if (t != ax && 1 + t < nd) y[1 + t] += c2 * (v[1 + t] - w[1 + t]);
 }
 
-__global__ void __launch_bounds__(512) k1_project(K1Args A) {
+__global__ void __launch_bounds__(256, 3) k1_project(K1Args A) {
   extern __shared__ __align__(16) double sm[];
   const Geo& g = A.g;
   const int N = g.N, nl = g.n_loc, nd = A.nd, E = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
@@ -166,10 +166,17 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
   const int fr = lane >> 2, fc = lane & 3;
   double* BEE = A.blocks + (size_t)E * (1 + g.dim) * N * N;
 
-  // ---- B_EE: chunks of K1_CH cells
-  const bool pair_live = warp < 10 && pair_tj(warp) < T;
-  const int pti = pair_ti(warp < 10 ? warp : 0), ptj = pair_tj(warp < 10 ? warp : 0);
-  double acc0 = 0.0, acc1 = 0.0;
+  // ---- B_EE: chunks of K1_CH cells; warp w owns the upper tile pairs w and w + 8 (10 pairs, 8 warps)
+  bool pair_live[2];
+  int pti[2], ptj[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int pr = warp + 8 * q;
+    pair_live[q] = pr < 10 && pair_tj(pr) < T;
+    pti[q] = pair_ti(pr < 10 ? pr : 0);
+    ptj[q] = pair_tj(pr < 10 ? pr : 0);
+  }
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   for (int l0 = 0; l0 < nl; l0 += K1_CH) {
     __syncthreads();
     for (int u = tid; u < K1_CH * 6; u += nt) {
@@ -197,23 +204,42 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
       tl[lc] = l < nl ? A.lfirst[base + l] : -1;
     }
     __syncthreads();
+    // pass A: the chunk's own dofs (coalesced) -> Ps
+    for (int u = tid; u < NP * K1_CH; u += nt) {
+      const int m = u / K1_CH, lc = u - m * K1_CH, l = l0 + lc;
+      const bool live = m < N && l < nl;
+      const double* pm = PE + (size_t)m * rowlen + l;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (a < nd) Ps[(size_t)m * LDK + a * K1_CH + lc] = live ? pm[(size_t)a * nl] : 0.0;
+    }
+    __syncthreads();
+    // pass B: the rows of A_EE Phi1^T; neighbours inside the chunk come from Ps, the others from L1/L2
     for (int u = tid; u < NP * K1_CH; u += nt) {
       const int m = u / K1_CH, lc = u - m * K1_CH, l = l0 + lc;
       double v[4] = {0.0, 0.0, 0.0, 0.0}, y[4] = {0.0, 0.0, 0.0, 0.0};
       if (m < N && l < nl) {
         const double* pm = PE + (size_t)m * rowlen;
+        const double* ps = Ps + (size_t)m * LDK;
 #pragma unroll
         for (int a = 0; a < 4; ++a)
-          if (a < nd) v[a] = pm[(size_t)a * nl + l];
+          if (a < nd) v[a] = ps[a * K1_CH + lc];
 #pragma unroll
         for (int d = 0; d < 6; ++d) {
           const int nbv = tnb[lc * 6 + d];
           if (nbv == -2) continue;
           double w[4] = {0.0, 0.0, 0.0, 0.0};
           if (nbv >= 0) {
+            const int nc = nbv - l0;
+            if (nc >= 0 && nc < K1_CH) {
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
-              if (a < nd) w[a] = pm[(size_t)a * nl + nbv];
+              for (int a = 0; a < 4; ++a)
+                if (a < nd) w[a] = ps[a * K1_CH + nc];
+            } else {
+#pragma unroll
+              for (int a = 0; a < 4; ++a)
+                if (a < nd) w[a] = pm[(size_t)a * nl + nbv];
+            }
           }
           k1_face_rows(nd, d >> 1, d & 1, tc1[lc * 6 + d], tko[lc * 6 + d], tkn[lc * 6 + d], v, w, y);
         }
@@ -241,29 +267,30 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
       }
 #pragma unroll
       for (int a = 0; a < 4; ++a)
-        if (a < nd) {
-          Ps[(size_t)m * LDK + a * K1_CH + lc] = v[a];
-          Ys[(size_t)m * LDK + a * K1_CH + lc] = y[a];
-        }
+        if (a < nd) Ys[(size_t)m * LDK + a * K1_CH + lc] = y[a];
     }
     __syncthreads();
-    if (pair_live) {
-      const double* pa = Ps + (size_t)(8 * pti + fr) * LDK + fc;
-      const double* pb = Ys + (size_t)(8 * ptj + fr) * LDK + fc;
-      for (int ks = 0; ks < KD; ks += 4) dmma(acc0, acc1, pa[ks], pb[ks]);
-    }
-  }
-  if (pair_live) {   // upper tile pairs, mirrored: B_EE exactly symmetric
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int cl = 2 * fc + hh, i = 8 * pti + fr, j = 8 * ptj + cl;
-      const double val = hh ? acc1 : acc0;
-      if (i < N && j < N && (pti < ptj || fr <= cl)) {
-        BEE[i * N + j] = val;
-        BEE[j * N + i] = val;
+    for (int q = 0; q < 2; ++q)
+      if (pair_live[q]) {
+        const double* pa = Ps + (size_t)(8 * pti[q] + fr) * LDK + fc;
+        const double* pb = Ys + (size_t)(8 * ptj[q] + fr) * LDK + fc;
+        for (int ks = 0; ks < KD; ks += 4) dmma(acc[q][0], acc[q][1], pa[ks], pb[ks]);
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (pair_live[q]) {   // upper tile pairs, mirrored: B_EE exactly symmetric
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int cl = 2 * fc + hh, i = 8 * pti[q] + fr, j = 8 * ptj[q] + cl;
+        const double val = acc[q][hh];
+        if (i < N && j < N && (pti[q] < ptj[q] || fr <= cl)) {
+          BEE[i * N + j] = val;
+          BEE[j * N + i] = val;
+        }
       }
     }
-  }
 
   // ---- r_E = Phi1_E b_E: b(w) = sum_{F in Gamma_D} int_F (sigma_F / h_F w - lambda K grad w . n) p_D
   if (tid < N) {
@@ -278,8 +305,15 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
   }
 
   // ---- couplings B_{E,E+e_a}[i][j] = Phi1_E[i] . A_{E,E+a} Phi1_{E+a}[j]: chunks of K1_CH faces
-  const bool tile_live = warp < T * T;
-  const int ti = tile_live ? warp / T : 0, tj = tile_live ? warp - (warp / T) * T : 0;
+  bool tile_live[2];
+  int ti[2], tj[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int tt = warp + 8 * q;
+    tile_live[q] = tt < T * T;
+    ti[q] = tile_live[q] ? tt / T : 0;
+    tj[q] = tile_live[q] ? tt - (tt / T) * T : 0;
+  }
   for (int a = 0; a < g.dim; ++a) {
     double* BEN = BEE + (size_t)(1 + a) * N * N;
     if (C[a] + 1 >= g.S[a]) {
@@ -289,7 +323,7 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
     const int nf = g.nface[a];
     const size_t baseN = (size_t)(E + g.Estride[a]) * nl;
     const double* PN = A.Phi1 + (size_t)(E + g.Estride[a]) * N * rowlen;
-    double c0 = 0.0, c1a = 0.0;
+    double cc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     for (int f0 = 0; f0 < nf; f0 += K1_CH) {
       __syncthreads();
       for (int lc = tid; lc < K1_CH; lc += nt) {
@@ -330,17 +364,21 @@ __global__ void __launch_bounds__(512) k1_project(K1Args A) {
           }
       }
       __syncthreads();
-      if (tile_live) {
-        const double* pa = Ps + (size_t)(8 * ti + fr) * LDK + fc;
-        const double* pb = Ys + (size_t)(8 * tj + fr) * LDK + fc;
-        for (int ks = 0; ks < KD; ks += 4) dmma(c0, c1a, pa[ks], pb[ks]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (tile_live[q]) {
+          const double* pa = Ps + (size_t)(8 * ti[q] + fr) * LDK + fc;
+          const double* pb = Ys + (size_t)(8 * tj[q] + fr) * LDK + fc;
+          for (int ks = 0; ks < KD; ks += 4) dmma(cc[q][0], cc[q][1], pa[ks], pb[ks]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (tile_live[q]) {
+        const int i = 8 * ti[q] + fr, j = 8 * tj[q] + 2 * fc;
+        if (i < N && j < N) BEN[i * N + j] = cc[q][0];
+        if (i < N && j + 1 < N) BEN[i * N + j + 1] = cc[q][1];
       }
-    }
-    if (tile_live) {
-      const int i = 8 * ti + fr, j = 8 * tj + 2 * fc;
-      if (i < N && j < N) BEN[i * N + j] = c0;
-      if (i < N && j + 1 < N) BEN[i * N + j + 1] = c1a;
-    }
   }
 }
 
