@@ -871,6 +871,7 @@ struct lrbms_ctx {
   int pcg_W = 1, pcg_G = 1, gj_G = 1;
   int sms = 148;   // SM count of the device (wave size of the one-CTA-per-SM kernels)
   int tm_W = 0, tm_G = 0;   // on-chip PCG (k_pcg_tm) launch; tm_W = 0: not usable
+  bool tm_cluster = false;  // the k_pcg_tm grid is one thread-block cluster (<= 16 CTAs: cluster barriers)
   const void* tm_fn = nullptr;   // the k_pcg_tm instance (compile-time N = 32, or the general one)
   size_t tm_smem = 0;
   int ns_par = 0;          // ping-pong word of the Newton-Schulz guard
@@ -1270,6 +1271,10 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     // cheaper (C3, 132 subdomains: 1110 us per solve with 132 one-warp CTAs, 837-878 us with 19-17 CTAs
     // of 7-8 warps; C4: 495 us at 7 x 147, 473 us at 8 x 128; r02p sweep)
     int W = single ? c->g.n_s : std::min(14, std::max(cdiv(c->g.n_s, sms), 8));
+    // mid-size configurations (C3): the grid as ONE cluster of <= 16 CTAs with hardware cluster barriers
+    // (tried below; falls back to the cooperative launch when such a cluster cannot be scheduled)
+    const bool want_cluster = !single && c->g.n_s <= 16 * 14;
+    if (want_cluster) W = std::max(8, cdiv(c->g.n_s, 16));
 #ifdef LRBMS_DEBUG
     if (const char* e = getenv("LRBMS_TM_W")) W = std::max(W, std::min(14, atoi(e)));   // experiments only
 #endif
@@ -1286,6 +1291,23 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
         CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tm, c->tm_fn, 32 * W, smem));
         if (occ_tm == 1 && G <= sms) {
           c->tm_W = W; c->tm_G = G; c->tm_smem = smem;
+          c->tm_cluster = false;
+#ifndef PCG_CLUSTER
+#define PCG_CLUSTER 1
+#endif
+          if (PCG_CLUSTER && want_cluster && G <= 16) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(G); cfg.blockDim = dim3(32 * W); cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = G; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at; cfg.numAttrs = 1;
+            int ncl = 0;
+            if (cudaFuncSetAttribute(c->tm_fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                cudaOccupancyMaxActiveClusters(&ncl, c->tm_fn, &cfg) == cudaSuccess && ncl >= 1)
+              c->tm_cluster = true;
+            (void)cudaGetLastError();
+          }
         }
       }
     }
@@ -1742,7 +1764,18 @@ static lrbms_status launch_solve(lrbms_ctx* c) {
   StageScope sc_(c, 4);
   void* args[] = {&A};   // A.gbar was zeroed by k_block_chol
   if (forked) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->join_ev, 0));
-  if (c->opts.onchip && c->tm_W > 0) {
+  A.cluster = 0;
+  if (c->opts.onchip && c->tm_W > 0 && c->tm_cluster) {
+    A.cluster = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->tm_G); cfg.blockDim = dim3(32 * c->tm_W); cfg.dynamicSmemBytes = c->tm_smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->tm_G; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaLaunchKernelExC(&cfg, c->tm_fn, args));
+  } else if (c->opts.onchip && c->tm_W > 0) {
     CUDA_TRY(c, cudaLaunchCooperativeKernel(c->tm_fn, dim3(c->tm_G), dim3(32 * c->tm_W), args, c->tm_smem,
                                             c->stream));
   } else {

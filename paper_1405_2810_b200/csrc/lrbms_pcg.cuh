@@ -67,6 +67,7 @@ struct PcgArgs {
   float* cont;            // [n_pad][8] contributions Y_{E,F}.r_E to the coarse rhs of F, by side
   double* e0;             // [n_pad] coarse correction of the starting vector
   float* cont_tm;         // k_pcg_tm coarse-rhs contributions, side-major [6][n_pad]
+  int cluster;            // k_pcg_tm: 1 = the grid is ONE thread-block cluster (hardware cluster barriers, DSMEM partials)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -214,6 +214,45 @@ __device__ __forceinline__ void grid_barrier_n(unsigned* bar, unsigned& epoch) {
   __syncthreads();
 }
 
+// Mid-size configurations (17 <= n_s <= 224: C3): the whole grid is ONE thread-block cluster of <= 16
+// CTAs, so the grid synchronisations are hardware cluster barriers (barrier.cluster arrive.release /
+// wait.acquire, which also order the CTAs' global-memory exchange at cluster scope) and the per-CTA
+// partials of a reduction are written straight into every CTA's shared memory over DSMEM: no L2 round
+// trip for the arrival, the spin or the partials.  Same fixed-order sums (a butterfly over the CTA
+// ranks, bitwise identical in every CTA).
+__device__ __forceinline__ double cluster_reduce(double v, double* red16, double (*cpart)[16], unsigned& epoch,
+                                                 double* bc) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+  const int G = (int)cl.num_blocks(), me = (int)cl.block_rank();
+  if (lane == 0) red16[warp] = v;
+  __syncthreads();
+  ++epoch;
+  if (warp == 0) {
+    const double t = warp_sum(lane < W ? red16[lane] : 0.0);
+    if (lane < G) *cl.map_shared_rank(&cpart[epoch & 1][me], lane) = t;
+  }
+  cl.sync();
+  if (warp == 0) {
+    const double sum = warp_sum(lane < G ? cpart[epoch & 1][lane] : 0.0);
+    if (lane == 0) *bc = sum;
+  }
+  __syncthreads();
+  return *bc;
+}
+__device__ __forceinline__ double sync_reduce(int cluster, double v, double* red16, double (*cpart)[16],
+                                              double* partials, unsigned* bar, unsigned& epoch, double* bc) {
+  return cluster ? cluster_reduce(v, red16, cpart, epoch, bc) : grid_reduce_n(v, red16, partials, bar, epoch, bc);
+}
+__device__ __forceinline__ void sync_barrier(int cluster, unsigned* bar, unsigned& epoch) {
+  if (cluster) {
+    ++epoch;
+    cg::this_cluster().sync();
+  } else {
+    grid_barrier_n(bar, epoch);
+  }
+}
+
 // Grid barrier without a reduction (release arrival on the same counter / epoch as grid_reduce_rel).
 __device__ __forceinline__ void grid_barrier_rel(unsigned* bar, unsigned& epoch) {
   __syncthreads();
@@ -448,7 +487,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
   __shared__ double red16[16];
   __shared__ double bc[4];
   __shared__ double sh46[46];
+  __shared__ double cpart[2][16];   // cluster mode: the CTAs' partials of a reduction (written over DSMEM)
   const Geo& g = A.g;
+  const int CL = A.cluster;
   const int N = NFIX ? NFIX : g.N, dim = g.dim;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int E = blockIdx.x * W + warp;
@@ -648,7 +689,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
     if (lane == 0) A.wc[E] = w;
   }
   TM_SSTAMP(4);
-  const double bb = grid_reduce_n(pbb, red16, gparts, A.gbar, epoch, &bc[0]);
+  const double bb = sync_reduce(CL, pbb, red16, cpart, gparts, A.gbar, epoch, &bc[0]);
   TM_SSTAMP(5);
   const double tol2 = A.rtol * A.rtol * bb;
   double rr = 1.0;
@@ -662,7 +703,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
         if (lane == 0) A.e0[E] = (double)e;
         y += zh * (double)e;
       }
-      grid_barrier_n(A.gbar, epoch);
+      sync_barrier(CL, A.gbar, epoch);
       if (own) {
         double rk = r - zh * __ldcg(A.e0 + E);
 #pragma unroll
@@ -671,7 +712,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
         r = act ? rk : 0.0;
       }
       scatter(r);
-      grid_barrier_n(A.gbar, epoch);
+      sync_barrier(CL, A.gbar, epoch);
       stage_g();
     } else if (A.use_coarse == 1) {
       stage_wc();
@@ -679,7 +720,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
     double z = r;
     if (A.use_coarse) { const float ec = coarse_dot(); z = act ? r + zh * (double)ec : 0.0; }
     if (act) A.z[E * N + lane] = z;
-    double rz = grid_reduce_n(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+    double rz = sync_reduce(CL, own ? warp_sum(z * r) : 0.0, red16, cpart, gparts, A.gbar, epoch, &bc[0]);
     TM_SSTAMP(6);
     double beta = 0.0, p = 0.0;
     for (it = (rz <= tol2) ? A.max_iters + 2 : 1; it <= A.max_iters; ++it) {
@@ -740,7 +781,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
       }
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 0], gtimer());
       TM_STAMP(1);
-      const double pq = grid_reduce_n(own ? warp_sum(act ? local : 0.0) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      const double pq = sync_reduce(CL, own ? warp_sum(act ? local : 0.0) : 0.0, red16, cpart, gparts, A.gbar, epoch, &bc[0]);
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 1], gtimer());
       if (!(pq > 0.0)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(A.flags, FLAG_BREAKDOWN);
@@ -762,7 +803,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
         if (lane == 0) A.wc[E] = w;
       }
       TM_STAMP(3);
-      grid_barrier_n(A.gbar, epoch);
+      sync_barrier(CL, A.gbar, epoch);
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 2], gtimer());
       TM_STAMP(4);
       // ---------------- C: z = M^-1 r, r.z
@@ -773,7 +814,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pcg_tm(PcgArgs A) {
       if (A.use_coarse) { const float ec = coarse_gemv(); z = act ? r + zh * (double)ec : 0.0; }
       if (act) A.z[E * N + lane] = z;
       TM_STAMP(6);
-      const double rz_new = grid_reduce_n(own ? warp_sum(z * r) : 0.0, red16, gparts, A.gbar, epoch, &bc[0]);
+      const double rz_new = sync_reduce(CL, own ? warp_sum(z * r) : 0.0, red16, cpart, gparts, A.gbar, epoch, &bc[0]);
       LRBMS_TSTAMP(A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && it < 64, A.tstamp[4 * it + 3], gtimer());
       TM_STAMP(7);
       rr = rz_new;
