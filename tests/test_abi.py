@@ -73,7 +73,7 @@ def _sass_of(prefix):
 def test_onchip_pcg_uses_tensor_memory():
     """k_pcg_tm keeps the scaled couplings in tensor memory: tcgen05.st at staging (STTM), tcgen05.ld
     every iteration (LDTM), cp.async staging (LDGSTS) and release reductions for its grid barriers."""
-    sass = _sass_of("_ZN5lrbms8k_pcg_tmILi32EEE")
+    sass = _sass_of("_ZN5lrbms8k_pcg_tmILi32ELi448EEE")
     for op in ("LDTM", "STTM", "LDGSTS", "REDG.E.ADD.STRONG.GPU"):
         assert op in sass, op
 
@@ -114,3 +114,24 @@ def test_create_validates_without_gpu(lib):
         assert st == 2, bad
         assert lib.lrbms_last_error(h)
         lib.lrbms_destroy(h)
+
+
+def test_k1_host_checks_without_gpu(lib):
+    """NEXT-4 host logic: N may exceed n_loc up to (dim + 1) n_loc (k = 1 bases), the k = 1 workspace size
+    follows the layout, and the k = 1 calls before lrbms_bind are STATE errors, not crashes."""
+    st, h = _create(lib, sx=2, sy=2, N=12)          # n_loc = 4, (dim + 1) n_loc = 12
+    assert st == 0 and h
+    nb = lib.lrbms_k1_bytes(h)
+    assert nb >= 8 * (64 * 12 * 3 * 4)                # at least Phi1: n_s N (dim + 1) n_loc doubles
+    assert lib.lrbms_k1_run(h, 1, 0.2, 0.0, 1, None) == 6
+    assert lib.lrbms_k1_set_saturation(h, None) == 6
+    lib.lrbms_destroy(h)
+    st, h = _create(lib, sx=2, sy=2, N=13)
+    assert st == 2
+    lib.lrbms_destroy(h)
+
+
+def test_onchip_pcg_cluster_mode_in_sass():
+    """The mid-size launch of k_pcg_tm synchronises with hardware cluster barriers (UCGABAR / barrier.cluster)."""
+    sass = _sass_of("_ZN5lrbms8k_pcg_tmILi0ELi448EEE")
+    assert "UCGABAR" in sass or "CGABAR" in sass or "ACQBULK" in sass
