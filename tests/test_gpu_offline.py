@@ -36,17 +36,23 @@ def test_offline_gpu_matches_host_recipe(name):
     Phi, tau, snaps = (t.cpu().numpy() for t in (Phi, tau, snaps))
     print(f"{name}: dt0 {info['dt0']:.6e} (host {host.dt0:.6e}), {info['tof_sweeps']} sweeps, "
           f"{info['fine_cg_iters']} CG iterations, kept {np.bincount(kept)}")
-    assert info["dt0"] == pytest.approx(host.dt0, rel=1e-8)   # dt: the pressure error times |p|/|dp| (DT_BAR)
-    # tau divides by the cell's outflow, a sum of pressure differences that is small near stagnation
-    # points: the fine pressures' ~1e-12 difference (iterative vs direct solve) is amplified there
-    # (C3: channels of 1e3..1e4 mD in a 1e-3 background leave nearly stagnant cells whose outflow is a
-    # pressure difference of ~1e-8: measured 8e-6 there, r02o)
-    assert np.max(np.abs(tau - host.tau) / host.tau) <= (1e-4 if name == "C3" else 1e-7)
-    # the median: tau accumulates along the flow paths, so a relative pressure difference of ~1e-13
-    # per cell adds up over the path length (measured 2.9e-11 on C4's 512-cell paths, r02j)
-    assert np.median(np.abs(tau - host.tau) / host.tau) <= 2e-10
+    # Bars.  dt: the pressure error times |p|/|dp| (DT_BAR).  tau divides by the cell's outflow, a sum of
+    # pressure differences that is small near stagnation points, and accumulates along the flow paths:
+    # the fine pressures' ~1e-12 difference (iterative vs direct solve) is amplified there (max), and adds
+    # up over the path length (median; measured 2.9e-11 on C4's 512-cell paths, r02j).  C3 (channels of
+    # 1e3..1e4 mD in a 1e-3 background, quarter five-spot) is the ill-conditioned case: the pressures
+    # agree to 1.3e-11, but most of its background cells are nearly stagnant (pressure differences of
+    # ~1e-8 to their neighbours), so the relative tau difference is ~1e-8 in the median and 8e-6 at the
+    # worst cell (r02o / r02q).
+    c3 = name == "C3"
+    e_tau = np.abs(tau - host.tau) / host.tau
+    e_snap = float(np.max(np.abs(snaps - host.P)))
+    print(f"  tau: max {e_tau.max():.3e}, median {np.median(e_tau):.3e}; snapshots: max abs {e_snap:.3e}")
+    assert info["dt0"] == pytest.approx(host.dt0, rel=1e-8)
+    assert e_tau.max() <= (1e-4 if c3 else 1e-7)
+    assert np.median(e_tau) <= (1e-7 if c3 else 2e-10)
     # snapshots: against the host's and as solutions of the oracle's independently assembled operator
-    assert np.max(np.abs(snaps - host.P)) <= 1e-10
+    assert e_snap <= 1e-10
     lam = host.mus @ (host.LW + host.LO)
     for j in range(0, len(host.mus), max(1, len(host.mus) // 4)):
         A, b = O.fine_operator(sc, lam[j])
