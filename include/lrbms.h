@@ -233,7 +233,8 @@ lrbms_status lrbms_offline_basis(lrbms_ctx *ctx, int32_t M, int32_t n_train, con
  * destroyed or lrbms_k1_set_basis is called again; Phi1 is copied into it.  Every link must lie on a
  * domain-boundary face of its axis (they are the Dirichlet faces, A29): CONFIG otherwise.  Needs
  * set_medium; replaces the indicator coefficients of the k = 0 basis (call lrbms_set_basis again
- * before k = 0 steps) and resets the reduced solver's history.
+ * before k = 0 steps) and resets the reduced solver's history.  Conversely lrbms_set_medium and
+ * lrbms_set_basis invalidate the k = 1 setup (STATE until lrbms_k1_set_basis is called again).
  * lrbms_k1_set_saturation: s1 (dev, [dim + 1][n]).  lrbms_k1_run: as lrbms_run; limiter = 0 skips the
  * limiter.  lrbms_k1_get_state: s1, p1 (dev, [dim + 1][n]), c (dev, n_s N), n_flagged (host: cells the
  * limiter flagged in the last step); NULL = skip.  lrbms_k1_stage_project: the blocks and the

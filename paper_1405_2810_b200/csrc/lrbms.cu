@@ -1457,6 +1457,7 @@ lrbms_status lrbms_set_medium(lrbms_ctx* c, const double* K, const double* phi) 
   c->have_medium = true;
   c->have_blocks = false;
   invalidate_profiles(c);   // b_q, d_q were projected with the old K
+  c->k1_ready = false;      // the k = 1 face coefficients were formed from the old K
   return LRBMS_OK;
 }
 
@@ -1474,6 +1475,7 @@ lrbms_status lrbms_set_basis(lrbms_ctx* c, const double* Phi) {
   c->last_rebuild_step = -1;
   c->have_x = false;
   invalidate_profiles(c);   // b_q, d_q were projected onto the old Phi
+  c->k1_ready = false;      // the indicator coefficients now belong to the k = 0 basis
   return LRBMS_OK;
 }
 

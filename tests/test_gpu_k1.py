@@ -183,3 +183,12 @@ def test_k0_steps_after_k1_need_the_k0_basis_again():
     ctx.run(5)
     s, _, _ = ctx.get_state()
     assert float(np.max(np.abs(np_(s) - ref["s"]))) <= 1e-10
+    # ... and the other way round: the k = 0 basis (and a new medium) invalidate the k = 1 setup
+    with pytest.raises(LrbmsError) as e:
+        ctx.k1_run(1)
+    assert e.value.status == LRBMS_E_STATE
+    ctx.k1_set_basis(sc.Phi1)
+    ctx.k1_set_saturation(K1.initial_saturation(sc))
+    ref1 = K1.run(sc, 3)
+    ctx.k1_run(3)
+    assert float(np.max(np.abs(np_(ctx.k1_get_state()[0]) - ref1["s"]))) <= 1e-10

@@ -28,7 +28,11 @@ import torch
 t = 1.0 + rank            # per-rank "elapsed ms"
 m = bench.max_over_ranks(t, world, torch.device("cpu"))
 bench.barrier(world)
-print(json.dumps({{"rank": rank, "world": world, "max": m}}), flush=True)
+# the workload's inputs: rank 0 runs the recipe, the others receive its bases (bitwise the same)
+import hashlib, numpy as np
+sc = bench.shared_scenario("C1", "pod", rank, world, torch.device("cpu"))
+digest = hashlib.sha256(np.ascontiguousarray(sc.Phi).tobytes()).hexdigest()
+print(json.dumps({{"rank": rank, "world": world, "max": m, "phi": digest}}), flush=True)
 import torch.distributed as dist
 dist.destroy_process_group()
 """
@@ -45,6 +49,11 @@ def test_max_over_ranks_gloo(tmp_path):
     lines = [json.loads(m) for m in re.findall(r"\{[^{}]*\}", out.stdout)]   # ranks may share a line
     assert len(lines) == 2
     assert all(l["world"] == 2 and l["max"] == 2.0 for l in lines)
+    from paper_1405_2810_b200 import inputs
+    import hashlib
+    import numpy as np
+    ref = hashlib.sha256(np.ascontiguousarray(inputs.make_scenario("C1").Phi).tobytes()).hexdigest()
+    assert lines[0]["phi"] == lines[1]["phi"] == ref
 
 
 def test_reference_arm_under_torchrun_prints_one_line():
