@@ -1574,7 +1574,8 @@ static lrbms_status launch_project(lrbms_ctx* c) {
     k_theta_partials<<<c->prof_G, 256, 0, c->stream>>>(c->lam_cur(), reinterpret_cast<double*>(c->pws + c->off_lamq),
                                                        c->prof_M, n, part);
     LAUNCH_CHECK(c);
-    k_theta_solve<<<1, 32, 0, c->stream>>>(part, c->prof_G, c->prof_M, reinterpret_cast<double*>(c->pws + c->off_gram),
+    k_theta_solve<<<1, 32 * c->prof_M, 0, c->stream>>>(part, c->prof_G, c->prof_M,
+                                          reinterpret_cast<double*>(c->pws + c->off_gram) + (size_t)c->prof_M * c->prof_M,
                                           theta);
     LAUNCH_CHECK(c);
 #ifndef AFF_GRID
@@ -1970,7 +1971,7 @@ static void profile_layout(const lrbms_ctx* c, int M, size_t* offs, size_t* tota
   offs[0] = take(8 * (size_t)M * n);                 // lambda_{t,q}, internal order
   offs[1] = take(8 * (size_t)M * profile_stride(block_len(c)));   // b_q
   offs[2] = take(8 * (size_t)M * profile_stride(R));              // d_q
-  offs[3] = take(8 * (size_t)M * M);                 // Gram
+  offs[3] = take(8 * (size_t)(2 * M * M + M));       // Gram, then its Cholesky factor and the keep flags
   offs[4] = take(8 * (size_t)M * AFF_PGRID * (size_t)c->sms);   // per-CTA partials
   offs[5] = take(8 * AFF_MAXM);                      // theta
   *total = o;
@@ -2020,6 +2021,9 @@ lrbms_status lrbms_set_profiles(lrbms_ctx* c, const double* s_profiles, int32_t 
     k_gram_row<<<1, 32, 0, c->stream>>>(part, c->prof_G, M, reinterpret_cast<double*>(c->pws + c->off_gram), r);
     LAUNCH_CHECK(c);
   }
+  k_theta_factor<<<1, 32, 0, c->stream>>>(reinterpret_cast<double*>(c->pws + c->off_gram), M,
+                                          reinterpret_cast<double*>(c->pws + c->off_gram) + (size_t)M * M);
+  LAUNCH_CHECK(c);
   c->have_blocks = false;
   // the kernels above replaced the scratch f_w: recompute the mobilities of the current saturation
   k_mobility<<<nb, 256, 0, c->stream>>>(g, c->f, c->s_cur(), c->lam_cur(), c->fw_cur());
@@ -2047,7 +2051,8 @@ lrbms_status lrbms_stage_theta(lrbms_ctx* c, double* theta) {
   k_theta_partials<<<c->prof_G, 256, 0, c->stream>>>(c->lam_cur(), reinterpret_cast<double*>(c->pws + c->off_lamq),
                                                      c->prof_M, c->g.n, part);
   LAUNCH_CHECK(c);
-  k_theta_solve<<<1, 32, 0, c->stream>>>(part, c->prof_G, c->prof_M, reinterpret_cast<double*>(c->pws + c->off_gram), th);
+  k_theta_solve<<<1, 32 * c->prof_M, 0, c->stream>>>(part, c->prof_G, c->prof_M,
+                                        reinterpret_cast<double*>(c->pws + c->off_gram) + (size_t)c->prof_M * c->prof_M, th);
   LAUNCH_CHECK(c);
   if (theta) CUDA_TRY(c, cudaMemcpyAsync(theta, th, 8 * (size_t)c->prof_M, cudaMemcpyDeviceToDevice, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));

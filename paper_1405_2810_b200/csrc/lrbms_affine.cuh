@@ -10,8 +10,9 @@
 //       c = e = 0 under reading R2 (the k = 0 operator and its Dirichlet data are linear in lambda).
 //
 // Per step: k_theta_partials (one pass over lambda and the M profiles, fixed-order per-CTA partials),
-// k_theta_solve (one warp: fixed-order sums, Cholesky of G with dropped pivots for dependent profiles
-// -- the paper's first and last profiles are both constant fields -- and the substitutions), and
+// k_theta_solve (a warp per profile: fixed-order sums; then the substitutions with the Cholesky factor of G
+// formed once by k_theta_factor, with dropped pivots for dependent profiles -- the paper's first and last
+// profiles are both constant fields), and
 // k_affine_combine (blocks = sum_q theta_q b_q, r = sum_q theta_q d_q: a streaming pass over the M
 // precomputed operators, HBM-bound).  Deterministic: no atomics.
 #pragma once
@@ -29,11 +30,27 @@ __global__ void __launch_bounds__(256) k_theta_partials(const double* __restrict
 #pragma unroll
   for (int q = 0; q < AFF_MAXM; ++q) acc[q] = 0.0;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const double xi = x[i];
+  if ((n & 1) == 0) {   // two cells per thread and 16-byte loads (every profile starts 16-byte aligned)
+    const size_t h = n >> 1;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const double2* Y2 = reinterpret_cast<const double2*>(Y);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < h; i += stride) {
+      const double2 xi = __ldg(x2 + i);
 #pragma unroll
-    for (int q = 0; q < AFF_MAXM; ++q)
-      if (q < M) acc[q] = fma(xi, Y[(size_t)q * n + i], acc[q]);
+      for (int q = 0; q < AFF_MAXM; ++q)
+        if (q < M) {
+          const double2 v = __ldcs(Y2 + (size_t)q * h + i);
+          acc[q] = fma(xi.x, v.x, acc[q]);
+          acc[q] = fma(xi.y, v.y, acc[q]);
+        }
+    }
+  } else {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+      const double xi = x[i];
+#pragma unroll
+      for (int q = 0; q < AFF_MAXM; ++q)
+        if (q < M) acc[q] = fma(xi, Y[(size_t)q * n + i], acc[q]);
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -66,45 +83,73 @@ __global__ void k_gram_row(const double* __restrict__ part, int G, int M, double
   sum_partials(part, G, M, gram + (size_t)r * M);
 }
 
-// one warp: h from the partials, then theta from G theta = h.  Cholesky in index order; a pivot
+// Once per set_profiles (one thread): the Cholesky factor of the Gram matrix in index order.  A pivot
 // below 1e-12 of its original diagonal entry marks a profile that depends on the previous ones: its
 // column is dropped (theta_q = 0), which leaves the fitted mobility sum_q theta_q lambda_q -- the
-// least-squares projection -- unchanged.
-__global__ void k_theta_solve(const double* __restrict__ part, int G, int M, const double* __restrict__ gram,
-                              double* __restrict__ theta) {
-  __shared__ double h[AFF_MAXM];
-  sum_partials(part, G, M, h);
-  __syncwarp();
-  if (threadIdx.x != 0) return;
-  double L[AFF_MAXM][AFF_MAXM], y[AFF_MAXM], t[AFF_MAXM];
-  bool keep[AFF_MAXM];
+// least-squares projection -- unchanged.  fac = [L (M x M, row-major)][keep (M, 1.0 / 0.0)].
+__global__ void k_theta_factor(const double* __restrict__ gram, int M, double* __restrict__ fac) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double* L = fac;
+  double* keep = fac + (size_t)M * M;
   for (int i = 0; i < M; ++i)
-    for (int j = 0; j < M; ++j) L[i][j] = gram[(size_t)i * M + j];
+    for (int j = 0; j < M; ++j) L[i * M + j] = gram[(size_t)i * M + j];
   for (int k = 0; k < M; ++k) {
-    double d = L[k][k];
+    double d = L[k * M + k];
     for (int j = 0; j < k; ++j)
-      if (keep[j]) d -= L[k][j] * L[k][j];
-    keep[k] = d > 1e-12 * gram[(size_t)k * M + k] && d > 0.0;
-    const double lkk = keep[k] ? sqrt(d) : 0.0;
+      if (keep[j] != 0.0) d -= L[k * M + j] * L[k * M + j];
+    const bool kp = d > 1e-12 * gram[(size_t)k * M + k] && d > 0.0;
+    keep[k] = kp ? 1.0 : 0.0;
+    const double lkk = kp ? sqrt(d) : 0.0;
     for (int i = k + 1; i < M; ++i) {
-      double v = L[i][k];
+      double v = L[i * M + k];
       for (int j = 0; j < k; ++j)
-        if (keep[j]) v -= L[i][j] * L[k][j];
-      L[i][k] = keep[k] ? v / lkk : 0.0;
+        if (keep[j] != 0.0) v -= L[i * M + j] * L[k * M + j];
+      L[i * M + k] = kp ? v / lkk : 0.0;
     }
-    L[k][k] = lkk;
+    L[k * M + k] = lkk;
   }
-  for (int i = 0; i < M; ++i) {   // L y = h
+}
+
+// Per step, M warps: warp q sums h_q = <lambda_t(s), lambda_q> from the per-CTA partials in a fixed order
+// (lane-strided, then a fixed shuffle tree); then one thread does the two substitutions with the stored
+// factor from shared memory (the factorisation itself is done once, k_theta_factor).
+__global__ void k_theta_solve(const double* __restrict__ part, int G, int M, const double* __restrict__ fac,
+                              double* __restrict__ theta) {
+  __shared__ double h[AFF_MAXM], Ls[AFF_MAXM * AFF_MAXM], ks[AFF_MAXM];
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  if (q < M) {
+    double v = 0.0;
+    for (int b = lane; b < G; b += 32) v += part[(size_t)q * G + b];
+    v = warp_sum(v);
+    if (lane == 0) h[q] = v;
+  }
+  for (int i = threadIdx.x; i < M * M; i += blockDim.x) Ls[i] = fac[i];
+  for (int i = threadIdx.x; i < M; i += blockDim.x) ks[i] = fac[(size_t)M * M + i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double y[AFF_MAXM], t[AFF_MAXM];
+#pragma unroll
+  for (int i = 0; i < AFF_MAXM; ++i) {   // L y = h
+    if (i >= M) break;
     double v = h[i];
-    for (int j = 0; j < i; ++j) v -= L[i][j] * y[j];
-    y[i] = keep[i] ? v / L[i][i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < AFF_MAXM; ++j)
+      if (j < i) v -= Ls[i * M + j] * y[j];
+    y[i] = ks[i] != 0.0 ? v / Ls[i * M + i] : 0.0;
   }
-  for (int i = M - 1; i >= 0; --i) {   // L^T t = y
+#pragma unroll
+  for (int ii = 0; ii < AFF_MAXM; ++ii) {   // L^T t = y
+    const int i = AFF_MAXM - 1 - ii;
+    if (i >= M) continue;
     double v = y[i];
-    for (int j = i + 1; j < M; ++j) v -= L[j][i] * t[j];
-    t[i] = keep[i] ? v / L[i][i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < AFF_MAXM; ++j)
+      if (j > i && j < M) v -= Ls[j * M + i] * t[j];
+    t[i] = ks[i] != 0.0 ? v / Ls[i * M + i] : 0.0;
   }
-  for (int q = 0; q < M; ++q) theta[q] = t[q];
+#pragma unroll
+  for (int qq = 0; qq < AFF_MAXM; ++qq)
+    if (qq < M) theta[qq] = t[qq];
 }
 
 // out[i] = sum_q theta_q X[q * qstride + i] for i < len (the reduced operator or right-hand side), 16-byte
@@ -118,7 +163,26 @@ __global__ void __launch_bounds__(256) k_affine_combine(const double* __restrict
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t h = len >> 1, h2 = qstride >> 1;
   const double2* X2 = reinterpret_cast<const double2*>(X);
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < h; i += stride) {
+#ifndef AFF_UNROLL
+#define AFF_UNROLL 2
+#endif
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; AFF_UNROLL == 2 && i + stride < h; i += 2 * stride) {   // two grid-strides at once: 2 M loads in flight
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < AFF_MAXM; ++q)
+      if (q < M) {
+        const double2 v = __ldcs(X2 + (size_t)q * h2 + i);
+        const double2 w = __ldcs(X2 + (size_t)q * h2 + i + stride);
+        a0 = fma(th[q], v.x, a0);
+        a1 = fma(th[q], v.y, a1);
+        b0 = fma(th[q], w.x, b0);
+        b1 = fma(th[q], w.y, b1);
+      }
+    __stcs(reinterpret_cast<double2*>(out) + i, make_double2(a0, a1));
+    __stcs(reinterpret_cast<double2*>(out) + i + stride, make_double2(b0, b1));
+  }
+  for (; i < h; i += stride) {
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
     for (int q = 0; q < AFF_MAXM; ++q)

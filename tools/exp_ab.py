@@ -15,6 +15,10 @@ if sys.argv[1] == "--child":
     sc = pickle.load(open(sys.argv[2], "rb"))
     n = int(sys.argv[3])
     ctx = LrbmsContext(sc)
+    if os.environ.get("EXP_AFFINE"):   # the paper's affine online variant (NEXT-1)
+        from paper_1405_2810_b200 import inputs
+        ctx.set_profiles(inputs.profile_saturations(sc))
+        ctx.set_online(True)
     ctx.run(5)
     s0 = ctx.stats()
     e0 = torch.cuda.Event(enable_timing=True)
