@@ -66,6 +66,11 @@ SMALL = [
     ("linear_kr", lambda: inputs.custom_scenario(16, 8, 1, 4, 4, 1, 3, seed=24, nw=1.0, no=1.0, mu_o=4.0)),
     ("corey3", lambda: inputs.custom_scenario(12, 12, 1, 4, 4, 1, 5, seed=25, nw=3.0, no=1.5, mu_o=2.0,
                                               swr=0.1, sor=0.05)),
+    # mid-size 3D (64 subdomains): the on-chip PCG runs as one thread-block cluster of 8 CTAs x 8 warps
+    # (cluster barriers, DSMEM partials), with coupling blocks in tensor memory and in shared memory
+    ("cluster3d", lambda: inputs.custom_scenario(12, 12, 8, 3, 3, 2, 9, seed=26, mu_o=10.0, bc="corner_columns_3d")),
+    # 18 subdomains in 2D: a cluster of 3 CTAs with a ragged last CTA
+    ("cluster2d", lambda: inputs.custom_scenario(24, 12, 1, 4, 4, 1, 6, seed=27, mu_o=5.0)),
 ]
 
 
