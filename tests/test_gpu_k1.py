@@ -143,6 +143,20 @@ def test_k1_deterministic_and_dt_fixed():
     assert float(np.max(np.abs(out[0] - ref["s"]))) <= 1e-10
 
 
+def test_k1_porosity_field():
+    """A porosity field enters the CFL step and the mass matrix of the transport (phi |T|)."""
+    sc = case("3d_aniso")
+    sc.phi = np.random.default_rng(1).uniform(0.1, 0.3, sc.n)
+    ref = K1.run(sc, 8, keep=True)
+    ctx = ctx_k1(sc, rtol=1e-13)
+    dts = np_(ctx.k1_run(8, log_dt=True))
+    s1, p1, _, nflag = ctx.k1_get_state()
+    assert rel(dts, ref["dts"]) <= 1e-8
+    assert rel(np_(p1), ref["ps"][-1]) <= 1e-10
+    assert float(np.max(np.abs(np_(s1) - ref["s"]))) <= 1e-10
+    assert nflag == int(ref["last"]["flagged"].sum())
+
+
 def test_k1_errors():
     from paper_1405_2810_b200.lrbms import LrbmsContext, LrbmsError, LRBMS_E_CONFIG, LRBMS_E_STATE
     sc = case("2d")
