@@ -18,7 +18,11 @@
 //   k_recon          a4       p = Phi_E c_E, coalesced streaming read of Phi
 //   k_flux_cfl       a5       face/link fluxes with lambda(s^n), per-cell Q_i, global min dt
 //   k_transport      a6       explicit upwind update, then lambda, f_w of s^{n+1} (a1 of the next step)
-// plus NEXT-1 (lrbms_affine.cuh), NEXT-2 (lrbms_fine.cuh) and the K6 diagnostics (lrbms_diag.cuh).
+//   k_flux_transport a5 + a6  the two above in one cooperative kernel (lrbms_transport.cuh): the default tail
+// k_pcg_tm launch shapes: one CTA (n_s <= 16), one thread-block cluster with hardware cluster barriers
+// (n_s <= 224), else a cooperative grid of >= 8-warp CTAs.
+// plus NEXT-1 (lrbms_affine.cuh), NEXT-2 (lrbms_fine.cuh), NEXT-3 (lrbms_offline.cuh), NEXT-4
+// (lrbms_k1.cuh: the k = 1 SWIP-DG fine space) and the K6 diagnostics (lrbms_diag.cuh).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
