@@ -213,16 +213,21 @@ def test_run_host_pinned_overlapped_copies():
     ctx2.close()
 
 
-def test_determinism_bitwise():
-    sc = inputs.make_scenario("C2", n_steps=10)
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_determinism_bitwise(name):
+    """Bitwise-identical reruns on the three launch shapes of the on-chip PCG (C2: one CTA; C3: one
+    thread-block cluster; C4: a cooperative grid) -- a race or an order-dependent sum would show here
+    (compute-sanitizer is closed on this pool, profiles/r02h)."""
+    sc = inputs.make_scenario(name, n_steps=10)
     outs = []
-    for _ in range(2):
+    for _ in range(3 if name != "C4" else 2):
         ctx = ctx_for(sc)
         ctx.run(10)
         s, p, c = ctx.get_state()
         outs.append((np_(s), np_(p), np_(c)))
-    for a, b in zip(outs[0], outs[1]):
-        assert np.array_equal(a, b)
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
 
 
 def test_metamorphic_viscosity_scaling_bitwise():
