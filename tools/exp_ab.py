@@ -19,6 +19,19 @@ if sys.argv[1] == "--child":
         from paper_1405_2810_b200 import inputs
         ctx.set_profiles(inputs.profile_saturations(sc))
         ctx.set_online(True)
+    if os.environ.get("EXP_FINE"):   # the fine reference scheme (NEXT-2): ms per step, CG iterations
+        ctx.run_fine(1, rtol=1e-12)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(ctx.stream)
+        _, its = ctx.run_fine(n, rtol=1e-12)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        print(json.dumps({"lib": os.environ.get("LRBMS_LIB", "default"), "fine_ms_per_step": round(ms, 3),
+                          "cg_iters_per_step": its / n, "us_per_iter": round(1e3 * ms / (its / n), 2)}), flush=True)
+        sys.exit(0)
     ctx.run(5)
     s0 = ctx.stats()
     e0 = torch.cuda.Event(enable_timing=True)
