@@ -2702,7 +2702,7 @@ lrbms_status lrbms_diagnostics(lrbms_ctx* c, lrbms_diag* o) {
   k_diag<<<g.n_s, nt, 16 * (size_t)g.n_loc, c->stream>>>(D);
   LAUNCH_CHECK(c);
   double* out = D.part + (size_t)g.n_s * DIAG_NP;
-  k_diag_final<<<1, 32, 0, c->stream>>>(D.part, g.n_s, out);
+  k_diag_final<<<1, 32 * DIAG_NP, 0, c->stream>>>(D.part, g.n_s, out);
   LAUNCH_CHECK(c);
   double h[DIAG_NP], sc[3];
   CUDA_TRY(c, cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
