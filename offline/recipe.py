@@ -386,6 +386,114 @@ def pod_bases(sc, P, N, eps_pca=1e-8):
     return Phi, kept, S
 
 
+# ----------------------------------------------------------------------------- greedy basis extension
+
+def _block_basis(sc, cols, cells):
+    """The global reduced basis as a sparse n x R matrix: column (E, k) holds local function k of E."""
+    rows, cidx, vals, off = [], [], [], 0
+    for E in range(sc.n_s):
+        Q = cols[E]
+        m = Q.shape[1]
+        rows.append(np.repeat(cells[E], m))
+        cidx.append(np.tile(off + np.arange(m), len(cells[E])))
+        vals.append(Q.reshape(-1))
+        off += m
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cidx))), shape=(sc.n, off))
+
+
+def greedy_bases(sc, P, LAM, N, lam_bar, eps_tol=0.0, eps_rel=1e-10, complete=True):
+    """The basis extension of alg:lrbmsBasisConstruction with the paper's error measure of the
+    experiments, the TRUE error in the energy norm of a fixed mobility lam_bar:
+        err(mu) = [ a(p_H(mu) - p_h(mu), p_H(mu) - p_h(mu); lam_bar) ]^(1/2).
+    P [J][n]: the fine pressures p_h of the training mobilities LAM [J][n] (the strong greedy needs them
+    all).  The local bases start from the coarse unit function v0 = 1/sqrt(n_loc) (P:1110-1111, A15);
+    every round solves the reduced problem (def:coarseScalePressure) of every training mobility in the
+    current space, picks the worst approximated one, and extends every local basis by the Gram-Schmidt
+    orthonormalisation of that snapshot's restriction (dependent restrictions are skipped, so the local
+    sizes may differ).  Stops when the largest error is <= max(eps_tol, eps_rel x the first round's largest
+    error), when a local basis reaches N (the ABI's fixed size), or when every snapshot has been used.  complete: bases shorter than N are completed by
+    graded monomials (A32).  Returns (Phi [n_s][N][n_loc] or the ragged list, sizes [n_s], selected
+    indices, the history of (max error, argmax) per round, the last round's errors)."""
+    J = P.shape[0]
+    cells = local_cells(sc)
+    nl = sc.n_loc
+    v0 = np.full(nl, 1.0 / np.sqrt(nl))
+    cols = [v0[:, None].copy() for _ in range(sc.n_s)]
+    systems = [fine_system(sc, LAM[j])[:2] for j in range(J)]
+    A_bar = fine_system(sc, lam_bar)[0]
+    selected, history = [], []
+    err = np.zeros(J)
+    while True:
+        Z = _block_basis(sc, cols, cells)
+        for j in range(J):
+            A, b = systems[j]
+            B = (Z.T @ (A @ Z)).tocsc()
+            c = spla.spsolve(B, Z.T @ b)
+            e = Z @ np.atleast_1d(c) - P[j]
+            err[j] = float(np.sqrt(max(e @ (A_bar @ e), 0.0)))
+        jmax = int(np.argmax(err))
+        history.append((float(err[jmax]), jmax))
+        if err[jmax] <= max(eps_tol, eps_rel * history[0][0]) or len(selected) == J or max(q.shape[1] for q in cols) >= N:
+            break
+        if jmax in selected:      # its restrictions were all dependent: nothing left to add for it
+            break
+        selected.append(jmax)
+        for E in range(sc.n_s):
+            v = P[jmax][cells[E]].copy()
+            nv0 = np.linalg.norm(v)
+            for _ in range(2):
+                v -= cols[E] @ (cols[E].T @ v)
+            nv = np.linalg.norm(v)
+            if nv > 1e-10 * nv0 and cols[E].shape[1] < N:
+                v /= nv
+                v *= 1.0 if v[np.argmax(np.abs(v))] > 0 else -1.0
+                cols[E] = np.concatenate([cols[E], v[:, None]], axis=1)
+    sizes = np.array([q.shape[1] for q in cols])
+    if not complete:
+        return cols, sizes, selected, history, err.copy()
+    mono = _graded_monomials(sc, N + 8)
+    Phi = np.empty((sc.n_s, N, nl))
+    for E in range(sc.n_s):
+        Q = cols[E]
+        for c in mono.T:
+            if Q.shape[1] == N:
+                break
+            v = c.copy()
+            for _ in range(2):
+                v -= Q @ (Q.T @ v)
+            nv = np.linalg.norm(v)
+            if nv > 1e-8 * np.linalg.norm(c):
+                v = v / nv
+                v = v * (1.0 if v[np.argmax(np.abs(v))] > 0 else -1.0)
+                Q = np.concatenate([Q, v[:, None]], axis=1)
+        if Q.shape[1] < N:
+            raise ValueError(f"greedy basis: subdomain {E} cannot be completed to N = {N}")
+        Phi[E] = Q.T
+    return Phi, sizes, selected, history, err.copy()
+
+
+def greedy_recipe(sc, seed, M=8, n_train=None, eps_tol=0.0, workers=None):
+    """The offline recipe with the greedy extension instead of the POD of all snapshots: steps 1-5 of
+    the module header, then ``greedy_bases`` with lam_bar the mobility of the barycentre parameter
+    (mu_q = 1/M).  For the configurations whose reduced problems a sparse direct solver handles in
+    seconds (C1-C3)."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        N = sc.N
+        n_train = 2 * N if n_train is None else n_train
+        fl = initial_flow(sc)
+        tau = time_of_flight(sc, fl["p"], fl["faces"], fl["Ff"], fl["link_cells"], fl["Fl"], fl["phiV"])
+        T = sc.n_steps * fl["dt0"]
+        LW, LO = mobility_profiles(sc, tau, T, M=M, s_inj=float(np.max(sc.link_s)))
+        mus = training_parameters(M, n_train, seed)
+        P = snapshots(sc, LW, LO, mus, p0=fl["p"], workers=workers)
+        LAM = mus @ (LW + LO)
+        lam_bar = np.full(M, 1.0 / M) @ (LW + LO)
+        Phi, sizes, selected, history, err = greedy_bases(sc, P, LAM, N, lam_bar, eps_tol=eps_tol)
+    return dict(Phi=Phi, sizes=sizes, selected=selected, history=history, errors=err, mus=mus, P=P, LAM=LAM,
+                lam_bar=lam_bar)
+
+
 # ----------------------------------------------------------------------------- the recipe
 
 @dataclasses.dataclass

@@ -444,6 +444,9 @@ def make_basis(sc: Scenario, basis: str, seed: int) -> np.ndarray:
         return poly_basis(sc, seed)
     if basis == "pod":
         return pod_basis(sc, seed)
+    if basis == "greedy":   # alg:lrbmsBasisConstruction's extension step with the true energy error (C1-C3)
+        from offline import recipe
+        return recipe.greedy_recipe(sc, seed)["Phi"]
     if basis == "full":
         sc.N = sc.n_loc
         return random_full_basis(sc, seed)

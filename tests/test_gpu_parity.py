@@ -295,6 +295,21 @@ def test_full_run_configs(name, steps, basis):
     assert e["dt"] <= DT_BAR
 
 
+@pytest.mark.parametrize("name,steps", [("C1", 20), ("C2", 40)])
+def test_greedy_bases_run_at_parity(name, steps):
+    """Bases from the greedy extension of alg:lrbmsBasisConstruction (offline/recipe.py greedy_recipe:
+    true energy-norm error) are one more shared input: the online step on them matches the
+    oracle's."""
+    sc = inputs.make_scenario(name, basis="greedy")
+    ref = O.run(sc, n_steps=steps, keep=True)
+    ctx = ctx_for(sc)
+    dts = np_(ctx.run(steps, log_dt=True))
+    s, p, c = ctx.get_state()
+    assert rel(dts, ref["dts"]) <= DT_BAR
+    assert rel(np_(c), ref["cs"][-1]) <= 1e-10 and rel(np_(p), ref["ps"][-1]) <= 1e-10
+    assert float(np.max(np.abs(np_(s) - ref["s"]))) <= 1e-10
+
+
 def test_c3_pod_tight_solver():
     """C3 on the paper-recipe bases amplifies round-off (FULL_RUN_S_BAR): with the reduced solve
     iterated to rtol 1e-14 the full 500-step run lands at the level of that amplification."""

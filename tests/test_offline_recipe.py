@@ -172,3 +172,70 @@ def test_pod_spans_snapshots_and_reproduces_them():
         c = O.solve_reduced(sc, blocks, r, method="dense")
         p = O.reconstruct(sc, c)
         assert np.max(np.abs(p - res.P[j])) <= 1e-10 * np.max(np.abs(res.P[j]))
+
+
+# ---------------------------------------------------------------------------- greedy extension
+def _greedy_setup(name="C2", n_train=None):
+    sc = inputs.make_scenario(name, basis="poly")
+    g = R.greedy_recipe(sc, 100 + inputs.CONFIG_INDEX[name], n_train=n_train)
+    return sc, g
+
+
+def test_greedy_first_round_errors_match_an_independent_reduced_solve():
+    """Round 0 of alg:lrbmsBasisConstruction: in the space of the coarse unit functions the
+    energy-norm errors of every training mobility, recomputed with the ORACLE's operator,
+    projection, reduced solve and reconstruction (N = 1), and the worst approximated parameter."""
+    sc, g = _greedy_setup()
+    sc1 = inputs.make_scenario("C2", basis="poly")
+    sc1.N = 1
+    sc1.Phi = np.full((sc1.n_s, 1, sc1.n_loc), 1.0 / np.sqrt(sc1.n_loc))
+    A_bar, _ = O.fine_operator(sc1, g["lam_bar"])
+    errs = []
+    for j in range(len(g["mus"])):
+        A, b = O.fine_operator(sc1, g["LAM"][j])
+        blocks, r = O.project(sc1, A, b)
+        c = O.solve_reduced(sc1, blocks, r, method="dense")
+        e = O.reconstruct(sc1, c) - g["P"][j]
+        errs.append(np.sqrt(e @ (A_bar @ e)))
+    errs = np.array(errs)
+    assert g["history"][0][1] == int(np.argmax(errs))
+    assert g["history"][0][0] == pytest.approx(errs.max(), rel=1e-9)
+    assert g["selected"][0] == int(np.argmax(errs))
+
+
+def test_greedy_reproduces_selected_snapshots_and_reduces_the_error():
+    sc, g = _greedy_setup()
+    e0 = g["history"][0][0]
+    assert all(g["errors"][j] <= 1e-8 * e0 for j in g["selected"])      # Galerkin: a snapshot in W is reproduced
+    assert g["history"][-1][0] <= 1e-2 * e0                              # the training error fell by > 100x
+    assert len(set(g["selected"])) == len(g["selected"])
+    # the bases: orthonormal, coarse unit function first, sizes between 1 and N
+    Phi = g["Phi"]
+    G = np.einsum("ekl,ejl->ekj", Phi, Phi)
+    assert np.max(np.abs(G - np.eye(sc.N)[None])) <= 1e-12
+    assert np.max(np.abs(Phi[:, 0, :] - 1.0 / np.sqrt(sc.n_loc))) <= 1e-15
+    assert g["sizes"].min() >= 1 and g["sizes"].max() == sc.N
+
+
+def test_greedy_with_few_snapshots_spans_what_the_pod_spans():
+    """With fewer independent snapshots than N - 1 the greedy uses them all, and its local spaces
+    span(v0, snapshots|_E) are the POD's (same projectors on the columns that come from snapshots)."""
+    sc, g = _greedy_setup(n_train=4)
+    assert sorted(g["selected"]) == [0, 1, 2, 3]
+    Phi_p, kept, _ = R.pod_bases(sc, g["P"], sc.N, eps_pca=1e-12)
+    for E in range(sc.n_s):
+        m = int(g["sizes"][E])
+        if m != kept[E] + 1:
+            continue            # a restriction at the noise floor: the two rank decisions may differ
+        Pg = g["Phi"][E, :m].T @ g["Phi"][E, :m]
+        Pp = Phi_p[E, :m].T @ Phi_p[E, :m]
+        assert np.max(np.abs(Pg - Pp)) <= 1e-6
+    assert np.mean(g["sizes"] == kept + 1) >= 0.9
+
+
+def test_greedy_stops_at_the_tolerance():
+    sc = inputs.make_scenario("C2", basis="poly")
+    g = R.greedy_recipe(sc, 102, eps_tol=1e9)
+    assert g["selected"] == [] and np.all(g["sizes"] == 1)             # nothing to add: indicators + completion
+    G = np.einsum("ekl,ejl->ekj", g["Phi"], g["Phi"])
+    assert np.max(np.abs(G - np.eye(sc.N)[None])) <= 1e-12
