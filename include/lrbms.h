@@ -114,8 +114,10 @@ typedef struct {
   int64_t total_iters;    /* PCG iterations since set_saturation */
   int32_t coarse_rebuilds;
   double fprime_max;      /* max f_w'(s) used by the CFL step */
-  int64_t ns_guard_trips; /* calls in which a Newton-Schulz update of the coarse inverse was skipped
-                             because max|I - E X| reached 1 (block Jacobi for the rest of the call; rebuilt at the next call) */
+  int64_t ns_guard_trips; /* calls in which a Newton-Schulz update of the coarse inverse was dropped
+                             because max|I - E X| reached 1; the inverse is then rebuilt on the device in
+                             the same step (fp32 Gauss-Jordan), or, where that kernel cannot hold the
+                             matrix, the call continues as block-Jacobi PCG and rebuilds at the next call */
   double ns_resid_max;    /* max_ij |(I - E X)_ij| of the last Newton-Schulz update (0 if none ran) */
 } lrbms_stats;
 

@@ -549,9 +549,14 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& epoch) {
   __syncthreads();
 }
 constexpr int GJ_CH = 256;   // columns per staged chunk of the pivot rows
+// cond != nullptr: the conditional rebuild after a Newton-Schulz step -- run only if that step's guard
+// (max |I - E X|, float bits) reached NS_GUARD_MAX or is NaN, i.e. the update was dropped; otherwise every
+// CTA returns at once (the value is grid-uniform: no barrier is entered).
 __global__ void __launch_bounds__(512, 1) k_coarse_gj32(Geo g, const double* __restrict__ Es, float* __restrict__ out,
-                                                       float* __restrict__ Rk, int n, unsigned* bar, int* bad) {
+                                                       float* __restrict__ Rk, int n, unsigned* bar, int* bad,
+                                                       const unsigned* __restrict__ cond) {
   extern __shared__ __align__(16) float smf[];
+  if (cond != nullptr && __uint_as_float(__ldcg(cond)) < NS_GUARD_MAX) return;
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int R = (n + G - 1) / G;
   const int r0 = blockIdx.x * R, r1 = min(n, r0 + R), nr = max(0, r1 - r0);
@@ -1336,6 +1341,8 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
   }
   CUDA_TRY(c, cudaFuncSetAttribute(k_project<0, 0, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_project<32, 8, 8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_project<24, 16, 16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
+  CUDA_TRY(c, cudaFuncSetAttribute(k_project<16, 10, 10, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->proj_smem));
   CUDA_TRY(c, cudaFuncSetAttribute(k_flux_cfl, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * c->g.n_loc));
   CUDA_TRY(c, cudaFuncSetAttribute(k_coarse_rt_s, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   {  // TMA descriptors (128 x 32 fp32 boxes, 128-byte swizzle) for the tensor-core Newton-Schulz GEMM
@@ -1368,6 +1375,7 @@ lrbms_status lrbms_bind(lrbms_ctx* c, void* ws, size_t bytes, void* stream) {
     CUDA_TRY(c, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     const void* fns[] = {(const void*)k_pcg, (const void*)k_pcg_tm<32>, (const void*)k_pcg_tm<0>,
                          (const void*)k_pcg_tm<0, 512>, (const void*)k_coarse_gj32, (const void*)k_project<0, 0, 0, 0>, (const void*)k_project<32, 8, 8, 8>,
+                         (const void*)k_project<24, 16, 16, 1>, (const void*)k_project<16, 10, 10, 1>,
                          (const void*)k_flux_cfl, (const void*)k_coarse_rt_s, (const void*)k_ns_gemm_tc,
                          (const void*)k_ns_gemm};
     for (const void* fn : fns) {
@@ -1552,10 +1560,20 @@ static lrbms_status launch_project_to(lrbms_ctx* c, const double* lam, double* b
   A.fc = c->at<double2>(c->fc); A.lam = lam;
   A.blocks = blocks; A.rhs = rhs;
   A.tstamp = c->debug_tstamp;
+  // 512 threads for the large subdomains (C5: one 218 KB CTA per SM anyway); 256 for n_loc <= 256, where the
+  // 125 registers per thread would otherwise leave one CTA per SM: two run side by side (C4: 79 -> 5x us)
+#ifndef PROJ_SMALL_NT
+#define PROJ_SMALL_NT 256
+#endif
+  const int pnt = c->g.n_loc <= 256 ? PROJ_SMALL_NT : 512;
   if (c->g.N == 32 && c->g.dim == 3 && c->g.s[0] == 8 && c->g.s[1] == 8 && c->g.s[2] == 8)
-    k_project<32, 8, 8, 8><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
+    k_project<32, 8, 8, 8><<<c->g.n_s, pnt, c->proj_smem, c->stream>>>(A);
+  else if (c->g.N == 24 && c->g.dim == 2 && c->g.s[0] == 16 && c->g.s[1] == 16)   // C4
+    k_project<24, 16, 16, 1><<<c->g.n_s, pnt, c->proj_smem, c->stream>>>(A);
+  else if (c->g.N == 16 && c->g.dim == 2 && c->g.s[0] == 10 && c->g.s[1] == 10)   // C3
+    k_project<16, 10, 10, 1><<<c->g.n_s, pnt, c->proj_smem, c->stream>>>(A);
   else
-    k_project<0, 0, 0, 0><<<c->g.n_s, 512, c->proj_smem, c->stream>>>(A);
+    k_project<0, 0, 0, 0><<<c->g.n_s, pnt, c->proj_smem, c->stream>>>(A);
   LAUNCH_CHECK(c);
   return LRBMS_OK;
 }
@@ -1622,7 +1640,8 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
       unsigned* bar = c->at<unsigned>(c->gjbar);
       int* bad = reinterpret_cast<int*>(bar + 16);
       CUDA_TRY(c, cudaMemsetAsync(bar, 0, 256, c->stream));
-      void* args[] = {&gg, &es, &out, &rk, &n, &bar, &bad};
+      const unsigned* cond = nullptr;
+      void* args[] = {&gg, &es, &out, &rk, &n, &bar, &bad, &cond};
       CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), args,
                                               c->gj32_smem, c->stream));
       c->launches++;
@@ -1660,6 +1679,26 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
       k_ns_gemm_tc<<<nbt * (nbt + 1) / 2, 128, NS_TC_SMEM, c->stream>>>(c->tmX[c->xcur], c->tmRT, X, Xn, n,
                                                                          guard + par, c->at<int>(c->flags) + FLAGW_NSTRIP);
       LAUNCH_CHECK(c);
+#ifndef NS_DEVICE_REBUILD
+#define NS_DEVICE_REBUILD 1
+#endif
+      if (NS_DEVICE_REBUILD && c->gj32_G > 0) {
+        // If the guard tripped (the update was dropped: Xn = 0), rebuild the inverse now, on the device:
+        // the same Gauss-Jordan kernel, which returns at once when the guard is below its bound.
+        // Without it the rest of the call would run as block-Jacobi PCG (C4: ~800 instead of 36
+        // iterations per step until the next call).
+        Geo gg = g;
+        const double* es = c->at<double>(c->Es);
+        float* rk = c->at<float>(c->gjrk);
+        unsigned* bar = c->at<unsigned>(c->gjbar);
+        int* bad = reinterpret_cast<int*>(bar + 16);
+        const unsigned* cond = guard + par;
+        CUDA_TRY(c, cudaMemsetAsync(bar, 0, 256, c->stream));
+        void* args[] = {&gg, &es, &Xn, &rk, &n, &bar, &bad, &cond};
+        CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), args,
+                                                c->gj32_smem, c->stream));
+        c->launches++;
+      }
       c->ns_par ^= 1;
     } else {                 // mma.sync fallback
       k_coarse_r<<<dim3(cdiv(n, 256), n), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es), c->at<float>(c->RTb), n);
@@ -1867,8 +1906,9 @@ static lrbms_status finish(lrbms_ctx* c, int nsteps_iters_known) {
   resolve_events(c);
   c->last_iters = it[0];
   c->total_iters = it[1];
-  if (hf[FLAGW_NSTRIP]) {   // a Newton-Schulz update was skipped (||I - E X||_max too large): rebuild next call
-    c->have_x = false;
+  if (hf[FLAGW_NSTRIP]) {   // a Newton-Schulz update was skipped (||I - E X||_max too large): the device
+                            // rebuilt the inverse at that step when it could; otherwise rebuild next call
+    if (!(NS_DEVICE_REBUILD && c->gj32_G > 0 && c->have_tmaps)) c->have_x = false;
     c->ns_trips++;
     CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->flags) + FLAGW_NSTRIP, 0, 4, c->stream));
   }
