@@ -281,6 +281,7 @@ __device__ __forceinline__ void ns_guard_accum(float m, unsigned* guard, int par
   __syncthreads();
   if (threadIdx.x == 0) {
     atomicMax(guard + par, gmax);
+    atomicMax(guard + 2, gmax);   // the maximum over the call (cleared by the host at the end of a call)
     if (blockIdx.x == 0 && blockIdx.y == 0) guard[1 - par] = 0u;
   }
 }
@@ -888,6 +889,9 @@ struct lrbms_ctx {
   int ft_G = 0, ft_kmax = 0, ft_nt = 0;
   size_t ft_smem = 0;
   int64_t ns_trips = 0;    // calls that ended with a skipped Newton-Schulz update (forced rebuild)
+  float ns_last_resid = -1.f;   // max |I - E X| over the Newton-Schulz steps of the previous call (< 0: unknown)
+  int ns_unarmed_steps = 0;     // Newton-Schulz steps of this call launched without the conditional rebuild
+  int ns_steps_call = 0;        // Newton-Schulz steps of this call
   int gj32_G = 0;          // > 0: fp32 row-resident Gauss-Jordan (k_coarse_gj32) with this grid
   int xcur = 0;            // which of Binv32 / Binv32b holds the current coarse inverse
   CUtensorMap tmX[2], tmRT;  // TMA descriptors of the coarse inverse buffers and of RT
@@ -1486,6 +1490,7 @@ lrbms_status lrbms_set_basis(lrbms_ctx* c, const double* Phi) {
   c->have_blocks = false;
   c->last_rebuild_step = -1;
   c->have_x = false;
+  c->ns_last_resid = -1.f;
   invalidate_profiles(c);   // b_q, d_q were projected onto the old Phi
   c->k1_ready = false;      // the indicator coefficients now belong to the k = 0 basis
   return LRBMS_OK;
@@ -1513,6 +1518,7 @@ lrbms_status lrbms_set_saturation(lrbms_ctx* c, const double* s) {
   c->last_iters = 0;
   c->last_rebuild_step = -1;
   c->have_x = false;
+  c->ns_last_resid = -1.f;
   c->have_sat = true;
   c->have_blocks = false;
   return LRBMS_OK;
@@ -1527,6 +1533,7 @@ lrbms_status lrbms_set_solver(lrbms_ctx* c, const lrbms_solver_opts* o) {
   c->opts = *o;
   c->last_rebuild_step = -1;
   c->have_x = false;
+  c->ns_last_resid = -1.f;
   return LRBMS_OK;
 }
 
@@ -1682,7 +1689,11 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
 #ifndef NS_DEVICE_REBUILD
 #define NS_DEVICE_REBUILD 1
 #endif
-      if (NS_DEVICE_REBUILD && c->gj32_G > 0) {
+#ifndef NS_REBUILD_ARM
+#define NS_REBUILD_ARM 0.1f
+#endif
+      // launched unless the previous call ended far below the guard (C5: 0.004-0.07; C4: 0.1-0.8)
+      if (NS_DEVICE_REBUILD && c->gj32_G > 0 && !(c->ns_last_resid >= 0.f && c->ns_last_resid < NS_REBUILD_ARM)) {
         // If the guard tripped (the update was dropped: Xn = 0), rebuild the inverse now, on the device:
         // the same Gauss-Jordan kernel, which returns at once when the guard is below its bound.
         // Without it the rest of the call would run as block-Jacobi PCG (C4: ~800 instead of 36
@@ -1698,7 +1709,10 @@ static lrbms_status launch_coarse(lrbms_ctx* c) {
         CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_coarse_gj32, dim3(c->gj32_G), dim3(512), args,
                                                 c->gj32_smem, c->stream));
         c->launches++;
+      } else {
+        c->ns_unarmed_steps++;
       }
+      c->ns_steps_call++;
       c->ns_par ^= 1;
     } else {                 // mma.sync fallback
       k_coarse_r<<<dim3(cdiv(n, 256), n), 256, 0, c->stream>>>(g, X, c->at<double>(c->Es), c->at<float>(c->RTb), n);
@@ -1896,10 +1910,10 @@ static lrbms_status launch_transport(lrbms_ctx* c, double cfl, double dt_fixed, 
 
 static lrbms_status finish(lrbms_ctx* c, int nsteps_iters_known) {
   (void)nsteps_iters_known;
-  int hf[4];
+  int hf[7];
   int it[2];
   double sc[3];
-  CUDA_TRY(c, cudaMemcpyAsync(hf, c->at<int>(c->flags), 16, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(hf, c->at<int>(c->flags), 28, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(it, c->at<int>(c->iters), 8, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(sc, c->at<double>(c->scal), 24, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1908,10 +1922,17 @@ static lrbms_status finish(lrbms_ctx* c, int nsteps_iters_known) {
   c->total_iters = it[1];
   if (hf[FLAGW_NSTRIP]) {   // a Newton-Schulz update was skipped (||I - E X||_max too large): the device
                             // rebuilt the inverse at that step when it could; otherwise rebuild next call
-    if (!(NS_DEVICE_REBUILD && c->gj32_G > 0 && c->have_tmaps)) c->have_x = false;
+    if (c->ns_unarmed_steps > 0 || !c->have_tmaps) c->have_x = false;
     c->ns_trips++;
     CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->flags) + FLAGW_NSTRIP, 0, 4, c->stream));
   }
+  c->ns_unarmed_steps = 0;
+  if (c->ns_steps_call > 0) {   // max |I - E X| over the Newton-Schulz steps of this call
+    memcpy(&c->ns_last_resid, &hf[FLAGW_NSMAX + 2], 4);
+    if (!(c->ns_last_resid == c->ns_last_resid)) c->ns_last_resid = 2.f;   // NaN: arm
+    CUDA_TRY(c, cudaMemsetAsync(c->at<int>(c->flags) + FLAGW_NSMAX + 2, 0, 4, c->stream));
+  }
+  c->ns_steps_call = 0;
   if (hf[0]) {
     std::string m;
     if (hf[0] & FLAG_PIVOT) m += "non-positive pivot (B not SPD: rank-deficient Phi_E or lambda <= 0); ";
@@ -2500,6 +2521,7 @@ static void reset_solver_history(lrbms_ctx* c) {
   c->last_iters = 0;
   c->last_rebuild_step = -1;
   c->have_x = false;
+  c->ns_last_resid = -1.f;
   c->have_blocks = false;
 }
 

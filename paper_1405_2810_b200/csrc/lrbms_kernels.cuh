@@ -165,7 +165,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 // error flag bits
 enum : int { FLAG_PIVOT = 1, FLAG_NOCONV = 2, FLAG_NOFLOW = 4, FLAG_NAN = 8, FLAG_BREAKDOWN = 16 };
 // words of the context's 16-int flag array: [0] the error bits above, [1] set_medium's phi check,
-// [2] Newton-Schulz update skipped (guard tripped), [4..5] max |I - E X| of the step (ping-pong)
+// [2] Newton-Schulz update skipped (guard tripped), [4..5] max |I - E X| of the step (ping-pong),
+// [6] its maximum over the call
 enum : int { FLAGW_NSTRIP = 2, FLAGW_NSMAX = 4 };
 // Newton-Schulz safety net: when max_ij |(I - E X)_ij| reaches this (or is NaN) the update would not
 // converge; the coarse inverse is dropped (X = 0: block Jacobi) until the next call rebuilds it
