@@ -377,23 +377,41 @@ def random_basis(sc: Scenario, seed: int) -> np.ndarray:
 # mobility profiles of the paper's affine online variant (NEXT-1): saturation fields only
 # ----------------------------------------------------------------------------
 
-def profile_saturations(sc: Scenario, M: int = 8) -> np.ndarray:
+_TOF_CACHE: dict = {}
+
+
+def profile_saturations(sc: Scenario, M: int = 8, kind: str = "tof") -> np.ndarray:
     """Saturation fields s_q (q = 1..M) whose mobilities are the profiles lambda_{alpha,q} of
     eq:parameterizedMob, following the recipe of P:650-662: q = 1 is S0 everywhere,
     q = M the injected saturation everywhere, and q = 2..M-1 carry the injected saturation where the
-    time of flight is below the q-th threshold.  Reading (A22): the time of flight is
-    replaced by its geometric proxy, the Euclidean distance of the cell centre from the injection
-    cells (links with s_ext > S0), normalised to [0, 1], with thresholds (q - 1) / (M - 1).
+    time of flight of the s0 flow is at most (q - 1) T / (M - 2).
+    kind = "tof" (default): the paper's recipe -- the time of flight and the horizon T = n_steps dt^0
+    come from the host offline recipe (``offline/recipe.py``: fine solve at s0, flow-ordered sweep;
+    readings A22, A31).  kind = "distance": round 1's geometric proxy (the Euclidean distance from the
+    injection cells, normalised, thresholds (q - 1) / (M - 1)).
     Returns [M][n] (natural cell order).  Holds no method arithmetic: the mobilities of these fields
     are evaluated by the oracle and by the library themselves."""
-    from scipy.ndimage import distance_transform_edt
     s_lo = float(np.min(sc.s0)) if sc.s0 is not None else 0.0
-    inj = sc.link_cell[sc.link_s > s_lo]
     s_hi = float(np.max(sc.link_s))
-    mask = np.ones(sc.n, bool)
-    mask[inj] = False
-    d = distance_transform_edt(mask.reshape(sc.nz, sc.ny, sc.nx), sampling=(sc.hz, sc.hy, sc.hx)).reshape(-1)
-    tau = d / max(float(d.max()), 1e-300)
+    if kind == "tof":
+        key = (sc.digest(), sc.n_steps)
+        if key not in _TOF_CACHE:
+            from offline import recipe
+            fl = recipe.initial_flow(sc)
+            tau = recipe.time_of_flight(sc, fl["p"], fl["faces"], fl["Ff"], fl["link_cells"], fl["Fl"], fl["phiV"])
+            _TOF_CACHE[key] = (tau, sc.n_steps * fl["dt0"])
+        tau, T = _TOF_CACHE[key]
+        thr = [(q - 1) * T / (M - 2) for q in range(1, M + 1)]
+    elif kind == "distance":
+        from scipy.ndimage import distance_transform_edt
+        inj = sc.link_cell[sc.link_s > s_lo]
+        mask = np.ones(sc.n, bool)
+        mask[inj] = False
+        d = distance_transform_edt(mask.reshape(sc.nz, sc.ny, sc.nx), sampling=(sc.hz, sc.hy, sc.hx)).reshape(-1)
+        tau = d / max(float(d.max()), 1e-300)
+        thr = [(q - 1) / (M - 1) for q in range(1, M + 1)]
+    else:
+        raise ValueError(kind)
     out = np.empty((M, sc.n))
     for q in range(1, M + 1):
         if q == 1:
@@ -401,7 +419,7 @@ def profile_saturations(sc: Scenario, M: int = 8) -> np.ndarray:
         elif q == M:
             out[q - 1] = s_hi
         else:
-            out[q - 1] = np.where(tau <= (q - 1) / (M - 1), s_hi, s_lo)
+            out[q - 1] = np.where(tau <= thr[q - 1], s_hi, s_lo)
     return out
 
 
@@ -435,7 +453,9 @@ def pod_basis(sc: Scenario, seed: int) -> np.ndarray:
     key = (sc.digest(), sc.N, sc.n_steps, seed)
     if key not in _POD_CACHE:
         from offline import recipe
-        _POD_CACHE[key] = recipe.pod_recipe(sc, seed).Phi
+        res = recipe.pod_recipe(sc, seed)
+        _POD_CACHE[key] = res.Phi
+        _TOF_CACHE[(sc.digest(), sc.n_steps)] = (res.tau, res.T)   # reused by profile_saturations
     return _POD_CACHE[key]
 
 

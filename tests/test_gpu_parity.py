@@ -416,10 +416,16 @@ AFFINE = [
     ("C1", lambda: inputs.make_scenario("C1")),
     ("C2", lambda: inputs.make_scenario("C2")),
     # odd n_s (3 x 3) and odd N: the lengths of b_q (9*3*25) and d_q (45) are odd
-    ("odd_len", lambda: inputs.custom_scenario(15, 15, 1, 5, 5, 1, 5, seed=26, mu_o=5.0)),
+    ("odd_len", lambda: inputs.custom_scenario(15, 15, 1, 5, 5, 1, 5, seed=26, mu_o=5.0, n_steps=40)),
     ("ragged3d", lambda: inputs.custom_scenario(9, 6, 4, 3, 3, 2, 11, seed=22, mu_o=10.0, bc="corner_columns_3d",
-                                                hx=0.5, hy=1.5, hz=2.0)),
+                                                hx=0.5, hy=1.5, hz=2.0, n_steps=40)),
+    # round 1's geometric profiles (Euclidean distance instead of the time of flight)
+    ("C2_distance", lambda: inputs.make_scenario("C2")),
 ]
+
+
+def _profiles(name, sc):
+    return inputs.profile_saturations(sc, kind="distance" if name.endswith("_distance") else "tof")
 
 
 @pytest.mark.parametrize("name,make", AFFINE, ids=[a[0] for a in AFFINE])
@@ -427,7 +433,7 @@ def test_affine_stage_parity(name, make):
     """theta fit (as the fitted mobility sum_q theta_q lambda_q, unique even when profiles are
     dependent), the affine reduced system and its solve against the oracle, on a random saturation."""
     sc = make()
-    sp = inputs.profile_saturations(sc)
+    sp = _profiles(name, sc)
     rng = np.random.default_rng(11)
     sc.s0 = rng.uniform(0.0, 1.0, sc.n)
     ctx = ctx_for(sc)
@@ -453,7 +459,7 @@ def test_affine_stage_parity(name, make):
 def test_affine_full_run(name, make):
     sc = make()
     n = 20
-    sp = inputs.profile_saturations(sc)
+    sp = _profiles(name, sc)
     ref = O.run(sc, n_steps=n, keep=True, s_profiles=sp)
     ctx = ctx_for(sc)
     ctx.set_profiles(sp)

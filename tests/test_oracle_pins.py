@@ -476,8 +476,8 @@ def test_inputs_deterministic_and_shaped():
 # affine online variant (eq:leastSquaresFit P:581-586, sec:offlineOnlineDecomposition P:784-833)
 
 def _affine_case():
-    sc = inputs.custom_scenario(12, 8, 1, 4, 4, 1, 5, seed=31, mu_o=10.0)
-    sp = inputs.profile_saturations(sc, M=6)
+    sc = inputs.custom_scenario(12, 8, 1, 4, 4, 1, 5, seed=31, mu_o=10.0, n_steps=40)
+    sp = inputs.profile_saturations(sc, M=6)   # the paper's recipe: time-of-flight thresholds
     return sc, sp, O.profile_mobilities(sc, sp)
 
 
@@ -487,8 +487,18 @@ def test_profiles_follow_the_recipe():
     assert np.all(sp[0] == 0.0) and np.all(sp[-1] == 1.0)
     filled = [int((q > 0).sum()) for q in sp]
     assert filled == sorted(filled) and filled[1] > 0 and filled[-2] < sc.n
-    inj = sc.link_cell[sc.link_s > 0]
-    assert np.all(sp[1][inj] == 1.0)   # the injection cells are inside the first front
+    assert all(np.all(sp[q] >= sp[q - 1]) for q in range(1, len(sp)))   # the fronts are nested
+    # the thresholds are the time of flight's, (q - 1) T / (M - 2) with T = n_steps dt^0 (A31): recomputed
+    # here from the recipe's time of flight (pinned in tests/test_offline_recipe.py)
+    from offline import recipe as R
+    fl = R.initial_flow(sc)
+    tau = R.time_of_flight(sc, fl["p"], fl["faces"], fl["Ff"], fl["link_cells"], fl["Fl"], fl["phiV"])
+    T = sc.n_steps * fl["dt0"]
+    for q in range(2, 6):
+        assert np.array_equal(sp[q - 1] > 0, tau <= (q - 1) * T / 4)
+    # round 1's geometric proxy is still available
+    sd = inputs.profile_saturations(sc, M=6, kind="distance")
+    assert np.all(sd[0] == 0.0) and np.all(sd[-1] == 1.0) and not np.array_equal(sd, sp)
 
 
 def test_theta_fit_recovers_an_exact_combination():
