@@ -320,7 +320,10 @@ def small_configs(args, device):
         ms = statistics.median(r[0] for r in reps)
         out[cfg] = {"us_per_step": round(1e3 * ms / K, 2), "steps_per_s": round(1e3 * K / ms, 1), "steps": K,
                     "pcg_iters_per_step": reps[0][1], "launches_per_step": reps[0][2] / K,
-                    "cells": sc.n, "reduced_dofs": sc.n_s * sc.N}
+                    "cells": sc.n, "reduced_dofs": sc.n_s * sc.N,
+                    "pcg_launch": ("one CTA" if sc.n_s <= 16 else
+                                   ("one thread-block cluster" if sc.n_s <= 224 else "cooperative grid")),
+                    "ns_guard_trips": int(ctx.stats()["ns_guard_trips"])}
         ctx.close()
     return out
 
