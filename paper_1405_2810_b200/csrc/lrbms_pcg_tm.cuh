@@ -164,6 +164,7 @@ __device__ __forceinline__ double grid_reduce_rel(double v, double* red16, doubl
 #define PCG_NBAR 8
 #endif
 constexpr int PCG_BAR_STRIDE = 32;   // unsigned words between counters
+static_assert(PCG_NBAR >= 1 && PCG_NBAR <= 8, "the context's gbar buffer holds 8 counters (8 x 128 bytes)");
 __device__ __forceinline__ void bar_arrive_wait_n(unsigned* bar, unsigned epoch) {
   const int lane = threadIdx.x & 31, G = gridDim.x;
   if (lane == 0)
