@@ -13,6 +13,11 @@
  *   a5  face fluxes + CFL time step      eq:velocityDG P:366-377 (k = 0), reading R4
  *   a6  explicit upwind transport        eq:saturationDG P:389-399, eq:upwind P:400-417
  *
+ * Beside the online step: the paper's affine online variant (theta fit + sum_q theta_q b_q:
+ * lrbms_set_profiles / lrbms_set_online), the fine-scale reference scheme (lrbms_run_fine), the offline
+ * basis recipe on the GPU (lrbms_offline_basis), the K6 diagnostics (lrbms_diagnostics) and the online
+ * step on the k = 1 SWIP-DG fine space with the P1 transport and the limiter (lrbms_k1_*).
+ *
  * Everything is fp64 on one GPU (sm_100a).  The fine grid is a structured
  * Cartesian grid of nx*ny*nz cells, x fastest (cell c = i + nx*(j + ny*k),
  * P:245-262); the coarse partition is matching: subdomains of
