@@ -6,8 +6,14 @@
 //          sentinel; warp 0 polls the G slots with ld.acquire until none is the sentinel, sums them;
 //          the slot of epoch e - 2 is reset to the sentinel when epoch e is written (no counter)
 //  mode 2: as 1, relaxed polls + one fence.acq_rel after the last poll
+//  mode 3/4: see reduce3
+//  mode 5 (round 2): the whole grid is ONE thread-block cluster (G <= 16): barrier.cluster + partials
+//          written into every CTA's shared memory over DSMEM (the k_pcg_tm launch for 17 <= n_s <= 224);
+//          also run with the L2 reduction of mode 3 at the same grid size for comparison
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cstdio>
+namespace cg = cooperative_groups;
 
 constexpr unsigned long long SENT = 0xFFFFFFFFFFFFFFFFull;
 
@@ -134,6 +140,41 @@ __device__ double reduce1(double v, double* red, unsigned long long* slots, unsi
   return *bc;
 }
 
+__device__ double reduce_cluster(double v, double* red, double (*cpart)[16], unsigned& epoch, double* bc) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+  const int G = (int)cl.num_blocks(), me = (int)cl.block_rank();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  ++epoch;
+  if (warp == 0) {
+    const double t = warp_sum(lane < W ? red[lane] : 0.0);
+    if (lane < G) *cl.map_shared_rank(&cpart[epoch & 1][me], lane) = t;
+  }
+  cl.sync();
+  if (warp == 0) {
+    const double s = warp_sum(lane < G ? cpart[epoch & 1][lane] : 0.0);
+    if (lane == 0) *bc = s;
+  }
+  __syncthreads();
+  return *bc;
+}
+
+__global__ void __launch_bounds__(448, 1) k_bench_cluster(int iters, int mode, double* data, double* partials,
+                                                          unsigned* bar, double* out) {
+  __shared__ double red[16], bc[1], cpart[2][16];
+  unsigned epoch = 0;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int i = 0; i < iters; ++i) {
+    data[(size_t)gw * 32 + lane] = acc + i;
+    const double nb = __ldcg(data + (size_t)((gw + 7) % (gridDim.x * (blockDim.x >> 5))) * 32 + lane);
+    const double v = warp_sum(nb);
+    acc += mode == 5 ? reduce_cluster(v, red, cpart, epoch, bc) : reduce3<3>(v, red, partials, bar, epoch, bc);
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+
 __global__ void __launch_bounds__(448, 1) k_bench(int iters, int mode, double* data, double* partials, unsigned* bar,
                                                   unsigned long long* slots, double* out) {
   __shared__ double red[16], bc[1];
@@ -187,6 +228,37 @@ int main() {
       cudaMemcpy(res, out, 16, cudaMemcpyDeviceToHost);
     }
     printf("mode %d: %.3f us per exchange + reduction  (check %.6e %.6e)\n", mode, best * 1e3 / iters, res[0], res[1]);
+  }
+  // one cluster of 16 CTAs x 8 warps (the C3 launch shape): cluster barriers + DSMEM against the L2 reduction
+  for (int mode = 5; mode >= 3; mode -= 2) {
+    const int Gc = 16, Tc = 256;
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaMemset(bar, 0, 256);
+      cudaMemset(data, 0, (size_t)G * 14 * 32 * 8);
+      int it = iters, md = mode;
+      void* args[] = {&it, &md, &data, &partials, &bar, &out};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(Gc); cfg.blockDim = dim3(Tc);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = Gc; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      cudaFuncSetAttribute(k_bench_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      cudaError_t err = cudaLaunchKernelExC(&cfg, (void*)k_bench_cluster, args);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (err != cudaSuccess) printf("launch: %s\n", cudaGetErrorString(err));
+      best = ms < best ? ms : best;
+    }
+    printf("16 CTAs x 8 warps, %s: %.3f us per exchange + reduction\n",
+           mode == 5 ? "one cluster (barrier.cluster + DSMEM partials)" : "L2 reduction (mode 3)", best * 1e3 / iters);
   }
   return 0;
 }
